@@ -1,0 +1,163 @@
+/*
+ * dgmf.h -- C ABI of the B200-native matrix-free DG operator library.
+ *
+ * Drop-in boundary for the hot path of the reference package `dgins`
+ * (arXiv 1607.01323 velocity-correction DG solver; reference tree
+ * /root/reference/pkg/src/dgins).  Each entry point below replaces one
+ * reference operator/solver function; the citation names the reference
+ * signature it stands in for.  The Python shim paper_1607_01323_b200/
+ * (operators.py, solvers.py) keeps the reference call signatures and
+ * forwards here through ctypes.
+ *
+ * Conventions
+ *  - All vector arguments are DEVICE pointers to fp64 data in element-major
+ *    order: (component, cell, [z,] y, x), x fastest, cell id
+ *    e = ix + nx*(iy + ny*iz) over the cells this context owns
+ *    (the reference serialisation FieldVector.element_major, spaces.py:49-51).
+ *  - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *    on that stream (host-side scalars are returned only by functions whose
+ *    name says so).
+ *  - Outputs are fully overwritten (no hidden accumulation) unless stated.
+ *  - Return value: 0 on success, <0 on error; dg_last_error() gives text.
+ *    DG_EINVAL maps to the reference's ValueError, DG_ECUDA/DG_ENCCL to
+ *    RuntimeError in the shim.
+ */
+#ifndef DGMF_H
+#define DGMF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DG_OK 0
+#define DG_EINVAL -1
+#define DG_ECUDA -2
+#define DG_ENOTSUP -3
+
+/* boundary kinds per tag; velocity semantics as in the reference
+ * (operators.py:189-193: velocity-Dirichlet faces are pressure-Neumann,
+ * velocity-Neumann faces are pressure-Dirichlet) */
+#define DG_BC_NONE 0              /* periodic axis: no boundary faces        */
+#define DG_BC_VELOCITY_DIRICHLET 1 /* reference DirichletBC                  */
+#define DG_BC_VELOCITY_NEUMANN 2  /* reference NeumannBC                     */
+
+typedef struct dg_ctx dg_ctx;
+
+/* Mesh + discretisation description.  Replaces the reference's
+ * build_box_mesh(...) (mesh.py:279-351) + DgSpace(mesh, k) (spaces.py:61-81)
+ * + BoundarySpec.resolve (operators.py:97-131) for axis-aligned boxes. */
+typedef struct {
+  int dim;                    /* 2 or 3                                        */
+  int k;                      /* polynomial degree 1..7 (n = k+1 GLL nodes)    */
+  int n_q_over;               /* convective rule points; 0 -> floor(3k/2)+1    */
+  int counts[3];              /* GLOBAL cells per axis (counts[2]=1 in 2D)     */
+  const double *vertices[3];  /* HOST per-axis vertex coordinates, counts+1    */
+  int periodic[3];            /* per axis                                      */
+  int bc_kind[6];             /* per tag xmin,xmax,ymin,ymax,zmin,zmax          */
+  int slab_begin, slab_end;   /* owned x-cells [begin,end); end<=0 -> all       */
+} dg_mesh_desc;
+
+/* ---- context ------------------------------------------------------------ */
+int dg_ctx_create(const dg_mesh_desc *desc, dg_ctx **out);
+int dg_ctx_destroy(dg_ctx *ctx);
+const char *dg_last_error(void);
+/* local cells / scalar dofs per component owned by this context */
+int dg_ctx_sizes(const dg_ctx *ctx, int64_t *n_cells, int64_t *n_dofs);
+/* copy tau_e (Eq. 18, geometry.py:90-108) of the owned cells to host */
+int dg_ctx_tau(const dg_ctx *ctx, double *tau_e_host);
+
+/* 1D tables on the host, computed in long double: S[q,i]=l_i(x_q),
+ * D[q,i]=l_i'(x_q) on the n_q-point Gauss rule, GLL nodes, Gauss points and
+ * weights, endpoint derivative rows.  Replaces gauss_rule/gll_nodes
+ * (quadrature.py:48-95) and Basis1D (basis.py:61-84). */
+int dg_basis_tables(int k, int n_q, double *S, double *D, double *nodes,
+                    double *points, double *weights, double *left_deriv,
+                    double *right_deriv);
+
+/* ---- operators (replace operators.py functions) ------------------------- */
+/* apply_pressure_laplace(space, p, bcs, tau_scale)  operators.py:187-238 */
+int dg_laplace_vmult(dg_ctx *ctx, const double *src, double *dst,
+                     double tau_scale, void *stream);
+/* laplace_diagonal(space, bcs, tau_scale)  operators.py:717-730 */
+int dg_laplace_diagonal(dg_ctx *ctx, double *diag, double tau_scale,
+                        void *stream);
+/* mass_apply / inverse_mass_apply(space, x)  operators.py:167-181,
+ * kernels.py:95-113; ncomp components stored back to back */
+int dg_mass(dg_ctx *ctx, const double *src, double *dst, int ncomp,
+            void *stream);
+int dg_inverse_mass(dg_ctx *ctx, const double *src, double *dst, int ncomp,
+                    void *stream);
+/* apply_viscous_helmholtz(space, u, gamma0_dt, nu, bcs)  operators.py:418-491;
+ * src/dst hold dim components */
+int dg_helmholtz_vmult(dg_ctx *ctx, const double *src, double *dst,
+                       double gamma0_dt, double nu, void *stream);
+/* apply_projection_operator(space, w, tau_d_e, tau_c_f)  operators.py:372-412.
+ * tau_d: per owned cell (device, or NULL); tau_c: per face, device array of
+ * dim*n_cells entries indexed [d*n_cells + e] = penalty of the face between
+ * cell e and its +d neighbour (NULL -> no jump term). */
+int dg_projection_vmult(dg_ctx *ctx, const double *src, double *dst,
+                        const double *tau_d, const double *tau_c,
+                        void *stream);
+/* eval_convective_rhs(space, bcs, history, betas, ...)  operators.py:533-594
+ * with homogeneous Dirichlet data and no body force (the hot-path case);
+ * hist[j] -> dim-component velocity at history level j. dst overwritten. */
+int dg_convective_rhs(dg_ctx *ctx, int n_hist, const double *const *hist,
+                      const double *betas, double *dst, void *stream);
+
+/* ---- vector kernels for the solvers (solvers.py) ------------------------ */
+/* deterministic fixed-order dot product; result written to device *out */
+int dg_dot(dg_ctx *ctx, const double *x, const double *y, int64_t n,
+           double *out_dev, void *stream);
+/* zero_mean_project_dual (solvers.py:187-198), in place on b (1 component);
+ * zero_mean_project (solvers.py:179-184), in place */
+int dg_zero_mean_dual(dg_ctx *ctx, double *b, void *stream);
+int dg_zero_mean(dg_ctx *ctx, double *p, void *stream);
+
+/* Fused PCG for the SIP Laplacian (solvers.py:30-73), preconditioner
+ * Chebyshev(degree, range, lambda_max) over point Jacobi (solvers.py:93-129)
+ * or plain Jacobi (degree 0), optional dual zero-mean projection of the
+ * operator (pure-Neumann problems).  x: device, initial guess zero.
+ * Residual history sqrt(r.z) per iteration written to hist_host
+ * (max_iter+1 entries) if non-NULL.  Blocking: returns when done. */
+typedef struct {
+  double tau_scale;
+  int project_dual;        /* op = zero_mean_project_dual o L                */
+  int cheb_degree;         /* 0 -> Jacobi                                    */
+  double cheb_range;       /* smoothing range (20)                           */
+  double cheb_lambda_max;  /* safety * Lanczos estimate                      */
+  double rel_tol, abs_tol;
+  int max_iter;
+} dg_pcg_params;
+typedef struct {
+  int iterations;
+  double residual;
+  int converged;
+  int breakdown;
+} dg_pcg_stats;
+int dg_laplace_pcg(dg_ctx *ctx, const double *b, double *x,
+                   const double *diag, const dg_pcg_params *prm,
+                   dg_pcg_stats *stats, double *hist_host, void *stream);
+
+/* ---- multi-GPU x-slabs (ghost cell layers) ------------------------------ */
+/* doubles in one ghost layer: ny*nz cells of one component (n^dim each),
+ * ordered by (iz, iy) -- the size of every send/recv buffer below */
+int dg_halo_count(const dg_ctx *ctx, int64_t *count);
+/* pack the first/last owned x-layer of src into caller-owned device buffers
+ * send_lo / send_hi (either may be NULL) */
+int dg_halo_pack(dg_ctx *ctx, const double *src, double *send_lo,
+                 double *send_hi, void *stream);
+/* attach caller-owned device buffers holding the neighbours' layers; they
+ * are read by subsequent vmults on the sides that have a remote neighbour */
+int dg_halo_attach(dg_ctx *ctx, const double *recv_lo, const double *recv_hi);
+/* part: 0 = all cells, 1 = cells not touching a ghost layer,
+ *       2 = only cells touching a ghost layer (needs recv_* filled) */
+int dg_laplace_vmult_part(dg_ctx *ctx, const double *src, double *dst,
+                          double tau_scale, int part, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGMF_H */

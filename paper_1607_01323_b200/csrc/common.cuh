@@ -1,0 +1,64 @@
+// Shared device-side definitions of the matrix-free DG library (sm_100a, fp64).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+#include "../../include/dgmf.h"
+
+namespace dg {
+
+void set_error(const std::string &msg);
+int cuda_fail(cudaError_t e, const char *where);
+
+#define DG_CUDA_CHECK(expr)                                   \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return ::dg::cuda_fail(_e, #expr); \
+  } while (0)
+
+#define DG_LAUNCH_CHECK(where)                                \
+  do {                                                        \
+    cudaError_t _e = cudaGetLastError();                      \
+    if (_e != cudaSuccess) return ::dg::cuda_fail(_e, where); \
+  } while (0)
+
+constexpr int kMaxN = 8;  // k <= 7
+
+// Edge handling of the owned block of cells, per side
+// (xlo, xhi, ylo, yhi, zlo, zhi).
+enum SideMode : int {
+  kWrap = 0,         // periodic, neighbour is the local cell at the other end
+  kGhost = 1,        // neighbour lives on another rank (x-slabs), ghost layer
+  kBndNone = 2,      // velocity-Dirichlet: pressure-Neumann, no operator term
+  kBndNeumann = 3,   // velocity-Neumann: pressure-Dirichlet term with 2 tau
+};
+
+// Cartesian geometry of the owned cells. All pointers are device pointers.
+struct Geo {
+  int nx, ny, nz;            // owned cells per axis (nz = 1 in 2D)
+  const double *hx, *hy, *hz;  // cell sizes per axis index (owned)
+  const double *tau;         // tau_e per owned cell (Eq. 18)
+  int mode[6];
+  const double *ghost[2];    // x-ghost layers (ny*nz cells each) or null
+  const double *ghost_tau[2];
+  double ghost_h[2];
+};
+
+// 1D reference matrices on [-1,1] for n = k+1 GLL nodes, Gauss rule n_q = n:
+// M = S^T W S, K = D^T W D, endpoint derivative rows.  Passed by value
+// (kernel parameter space -> constant bank operands of DFMA).
+template <int N>
+struct LapTab {
+  double M[N * N];
+  double K[N * N];
+  double dL[N];
+  double dR[N];
+};
+
+template <int N>
+struct TensorTab {  // a single 1D matrix A (N x N) for tensor-product apply
+  double A[N * N];
+};
+
+}  // namespace dg

@@ -1,0 +1,623 @@
+// C-ABI implementation of the B200 matrix-free DG library (include/dgmf.h).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "laplace.cuh"
+#include "tables.h"
+#include "tensor.cuh"
+#include "vector.cuh"
+
+namespace dg {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+int cuda_fail(cudaError_t e, const char *where) {
+  g_err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+  return DG_ECUDA;
+}
+
+static int inval(const std::string &m) {
+  g_err = m;
+  return DG_EINVAL;
+}
+
+}  // namespace dg
+
+using namespace dg;
+
+struct dg_ctx {
+  int dim = 3, k = 1, n = 2, nq_over = 2;
+  int gcounts[3] = {1, 1, 1};
+  int counts[3] = {1, 1, 1};
+  int slab_begin = 0, slab_end = 0;
+  int periodic[3] = {0, 0, 0};
+  int bc[6] = {0, 0, 0, 0, 0, 0};
+  int mode[6] = {0, 0, 0, 0, 0, 0};
+  Basis1D basis, over;
+  std::vector<double> gvert[3];
+  std::vector<double> hx, hy, hz, tau;  // host, owned
+  double ghost_h[2] = {1.0, 1.0};
+  std::vector<double> ghost_tau_h[2];
+  double *d_hx = nullptr, *d_hy = nullptr, *d_hz = nullptr, *d_tau = nullptr;
+  double *d_ghost_tau[2] = {nullptr, nullptr};
+  const double *d_recv[2] = {nullptr, nullptr};  // caller-owned ghost layers
+  int64_t halo_count = 0;
+  int64_t n_cells = 0, n_dofs = 0, np = 0;
+  double volume = 0.0;  // |Omega| of the GLOBAL mesh
+  double *d_red = nullptr;     // reduction partials (kRedBlocks) + scalars
+  double *d_scal = nullptr;    // 16 device scalars
+  double *h_scal = nullptr;    // pinned mirror
+  std::vector<double *> work;  // solver work vectors (n_dofs each)
+  std::mutex mu;
+
+  Geo geo() const {
+    Geo g;
+    g.nx = counts[0];
+    g.ny = counts[1];
+    g.nz = counts[2];
+    g.hx = d_hx;
+    g.hy = d_hy;
+    g.hz = d_hz;
+    g.tau = d_tau;
+    for (int i = 0; i < 6; ++i) g.mode[i] = mode[i];
+    for (int s = 0; s < 2; ++s) {
+      g.ghost[s] = d_recv[s];
+      g.ghost_tau[s] = d_ghost_tau[s];
+      g.ghost_h[s] = ghost_h[s];
+    }
+    return g;
+  }
+};
+
+// tau_e of GLOBAL cell (gx, gy, gz), Eq. 18 (geometry.py:90-108): every
+// boundary face counts in A_bnd (also walls without a pressure term),
+// periodic faces count as interior.
+static double tau_global(const dg_ctx *c, int gx, int gy, int gz) {
+  const int gi[3] = {gx, gy, gz};
+  double h[3] = {1.0, 1.0, 1.0};
+  for (int d = 0; d < c->dim; ++d) h[d] = c->gvert[d][gi[d] + 1] - c->gvert[d][gi[d]];
+  double vol = 1.0;
+  for (int d = 0; d < c->dim; ++d) vol *= h[d];
+  double aint = 0.0, abnd = 0.0;
+  for (int d = 0; d < c->dim; ++d) {
+    double area = 1.0;
+    for (int dd = 0; dd < c->dim; ++dd)
+      if (dd != d) area *= h[dd];
+    for (int s = 0; s < 2; ++s) {
+      const bool edge = s ? (gi[d] == c->gcounts[d] - 1) : (gi[d] == 0);
+      if (edge && !c->periodic[d]) abnd += area;
+      else aint += area;
+    }
+  }
+  const double kp = (double)(c->k + 1);
+  return kp * kp * (0.5 * aint + abnd) / vol;
+}
+
+template <typename T>
+static int upload(T **dst, const std::vector<T> &src) {
+  DG_CUDA_CHECK(cudaMalloc((void **)dst, sizeof(T) * (src.empty() ? 1 : src.size())));
+  if (!src.empty())
+    DG_CUDA_CHECK(cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+extern "C" {
+
+const char *dg_last_error(void) { return g_err.c_str(); }
+
+int dg_basis_tables(int k, int n_q, double *S, double *D, double *nodes, double *points,
+                    double *weights, double *left_deriv, double *right_deriv) {
+  if (k < 1 || k > 7) return inval("polynomial degree must be in 1..7");
+  if (n_q < 1) return inval("need at least one quadrature point");
+  Basis1D b;
+  basis_tables(k, n_q, b);
+  if (S) std::memcpy(S, b.S.data(), sizeof(double) * b.S.size());
+  if (D) std::memcpy(D, b.D.data(), sizeof(double) * b.D.size());
+  if (nodes) std::memcpy(nodes, b.nodes.data(), sizeof(double) * b.nodes.size());
+  if (points) std::memcpy(points, b.pts.data(), sizeof(double) * b.pts.size());
+  if (weights) std::memcpy(weights, b.wts.data(), sizeof(double) * b.wts.size());
+  if (left_deriv) std::memcpy(left_deriv, b.ld.data(), sizeof(double) * b.ld.size());
+  if (right_deriv) std::memcpy(right_deriv, b.rd.data(), sizeof(double) * b.rd.size());
+  return DG_OK;
+}
+
+int dg_ctx_create(const dg_mesh_desc *desc, dg_ctx **out) {
+  if (!desc || !out) return inval("null argument");
+  *out = nullptr;
+  if (desc->dim != 2 && desc->dim != 3) return inval("dim must be 2 or 3");
+  if (desc->k < 1 || desc->k > 7)
+    return inval("polynomial degree must be in 1..7 (got " + std::to_string(desc->k) + ")");
+  dg_ctx *c = new dg_ctx();
+  c->dim = desc->dim;
+  c->k = desc->k;
+  c->n = desc->k + 1;
+  c->nq_over = desc->n_q_over > 0 ? desc->n_q_over : (3 * desc->k) / 2 + 1;
+  for (int d = 0; d < 3; ++d) {
+    c->gcounts[d] = (d < c->dim) ? desc->counts[d] : 1;
+    c->periodic[d] = (d < c->dim) ? desc->periodic[d] : 0;
+    if (c->gcounts[d] < 1) {
+      delete c;
+      return inval("counts must be >= 1 per axis");
+    }
+  }
+  for (int d = 0; d < c->dim; ++d) {
+    if (!desc->vertices[d]) {
+      delete c;
+      return inval("missing vertex coordinates");
+    }
+    c->gvert[d].assign(desc->vertices[d], desc->vertices[d] + c->gcounts[d] + 1);
+    for (int i = 0; i < c->gcounts[d]; ++i)
+      if (!(c->gvert[d][i + 1] > c->gvert[d][i])) {
+        delete c;
+        return inval("non-positive mapping Jacobian (vertex coordinates must increase)");
+      }
+  }
+  c->gvert[2].assign({0.0, 2.0});
+  if (c->dim == 2) c->gvert[2] = {0.0, 2.0};
+  for (int t = 0; t < 6; ++t) c->bc[t] = (t < 2 * c->dim) ? desc->bc_kind[t] : 0;
+  for (int d = 0; d < c->dim; ++d)
+    for (int s = 0; s < 2; ++s) {
+      const int kind = c->bc[2 * d + s];
+      if (!c->periodic[d] && kind != DG_BC_VELOCITY_DIRICHLET && kind != DG_BC_VELOCITY_NEUMANN) {
+        delete c;
+        static const char *names[6] = {"xmin", "xmax", "ymin", "ymax", "zmin", "zmax"};
+        return inval(std::string("boundary tags without a condition: {'") + names[2 * d + s] + "'}");
+      }
+    }
+  c->slab_begin = desc->slab_begin;
+  c->slab_end = desc->slab_end > 0 ? desc->slab_end : c->gcounts[0];
+  if (c->slab_begin < 0 || c->slab_end > c->gcounts[0] || c->slab_begin >= c->slab_end) {
+    delete c;
+    return inval("invalid slab range");
+  }
+  c->counts[0] = c->slab_end - c->slab_begin;
+  c->counts[1] = c->gcounts[1];
+  c->counts[2] = c->gcounts[2];
+  const bool whole_x = (c->slab_begin == 0 && c->slab_end == c->gcounts[0]);
+  auto bnd_mode = [&](int t) { return c->bc[t] == DG_BC_VELOCITY_NEUMANN ? kBndNeumann : kBndNone; };
+  // x sides
+  if (c->slab_begin > 0) c->mode[0] = kGhost;
+  else if (c->periodic[0]) c->mode[0] = whole_x ? kWrap : kGhost;
+  else c->mode[0] = bnd_mode(0);
+  if (c->slab_end < c->gcounts[0]) c->mode[1] = kGhost;
+  else if (c->periodic[0]) c->mode[1] = whole_x ? kWrap : kGhost;
+  else c->mode[1] = bnd_mode(1);
+  for (int d = 1; d < 3; ++d)
+    for (int s = 0; s < 2; ++s)
+      c->mode[2 * d + s] = (d >= c->dim || c->periodic[d]) ? kWrap : bnd_mode(2 * d + s);
+
+  basis_tables(c->k, c->n, c->basis);
+  basis_tables(c->k, c->nq_over, c->over);
+  c->np = 1;
+  for (int d = 0; d < c->dim; ++d) c->np *= c->n;
+  c->n_cells = (int64_t)c->counts[0] * c->counts[1] * c->counts[2];
+  c->n_dofs = c->n_cells * c->np;
+
+  c->hx.resize(c->counts[0]);
+  for (int i = 0; i < c->counts[0]; ++i)
+    c->hx[i] = c->gvert[0][c->slab_begin + i + 1] - c->gvert[0][c->slab_begin + i];
+  c->hy.resize(c->counts[1]);
+  for (int i = 0; i < c->counts[1]; ++i) c->hy[i] = c->gvert[1][i + 1] - c->gvert[1][i];
+  c->hz.resize(c->counts[2]);
+  for (int i = 0; i < c->counts[2]; ++i) c->hz[i] = c->gvert[2][i + 1] - c->gvert[2][i];
+  c->tau.resize(c->n_cells);
+  for (int iz = 0; iz < c->counts[2]; ++iz)
+    for (int iy = 0; iy < c->counts[1]; ++iy)
+      for (int ix = 0; ix < c->counts[0]; ++ix)
+        c->tau[ix + (size_t)c->counts[0] * (iy + (size_t)c->counts[1] * iz)] =
+            tau_global(c, c->slab_begin + ix, iy, iz);
+  c->volume = 1.0;
+  for (int d = 0; d < c->dim; ++d) c->volume *= (c->gvert[d].back() - c->gvert[d].front());
+  // ghost layers
+  const int64_t layer = (int64_t)c->counts[1] * c->counts[2];
+  c->halo_count = layer * c->np;
+  int rc = 0;
+  for (int s = 0; s < 2; ++s) {
+    int gx;
+    if (s == 0) gx = c->slab_begin > 0 ? c->slab_begin - 1 : c->gcounts[0] - 1;
+    else gx = c->slab_end < c->gcounts[0] ? c->slab_end : 0;
+    c->ghost_h[s] = c->gvert[0][gx + 1] - c->gvert[0][gx];
+    c->ghost_tau_h[s].resize(layer);
+    for (int iz = 0; iz < c->counts[2]; ++iz)
+      for (int iy = 0; iy < c->counts[1]; ++iy)
+        c->ghost_tau_h[s][iy + (size_t)c->counts[1] * iz] = tau_global(c, gx, iy, iz);
+    if (c->mode[2 * 0 + s] == kGhost) {
+      if ((rc = upload(&c->d_ghost_tau[s], c->ghost_tau_h[s]))) goto fail;
+    }
+  }
+  if ((rc = upload(&c->d_hx, c->hx))) goto fail;
+  if ((rc = upload(&c->d_hy, c->hy))) goto fail;
+  if ((rc = upload(&c->d_hz, c->hz))) goto fail;
+  if ((rc = upload(&c->d_tau, c->tau))) goto fail;
+  if (cudaMalloc((void **)&c->d_red, sizeof(double) * (kRedBlocks + 64)) != cudaSuccess) goto cfail;
+  if (cudaMalloc((void **)&c->d_scal, sizeof(double) * 32) != cudaSuccess) goto cfail;
+  if (cudaMemset(c->d_scal, 0, sizeof(double) * 32) != cudaSuccess) goto cfail;
+  if (cudaMallocHost((void **)&c->h_scal, sizeof(double) * 32) != cudaSuccess) goto cfail;
+  *out = c;
+  return DG_OK;
+cfail:
+  rc = cuda_fail(cudaGetLastError(), "dg_ctx_create allocation");
+fail:
+  dg_ctx_destroy(c);
+  return rc ? rc : DG_ECUDA;
+}
+
+int dg_ctx_destroy(dg_ctx *c) {
+  if (!c) return DG_OK;
+  cudaFree(c->d_hx);
+  cudaFree(c->d_hy);
+  cudaFree(c->d_hz);
+  cudaFree(c->d_tau);
+  for (int s = 0; s < 2; ++s) {
+    cudaFree(c->d_ghost_tau[s]);
+  }
+  cudaFree(c->d_red);
+  cudaFree(c->d_scal);
+  if (c->h_scal) cudaFreeHost(c->h_scal);
+  for (double *w : c->work) cudaFree(w);
+  delete c;
+  return DG_OK;
+}
+
+int dg_ctx_sizes(const dg_ctx *c, int64_t *n_cells, int64_t *n_dofs) {
+  if (!c) return inval("null context");
+  if (n_cells) *n_cells = c->n_cells;
+  if (n_dofs) *n_dofs = c->n_dofs;
+  return DG_OK;
+}
+
+int dg_ctx_tau(const dg_ctx *c, double *tau_e_host) {
+  if (!c || !tau_e_host) return inval("null argument");
+  std::memcpy(tau_e_host, c->tau.data(), sizeof(double) * c->tau.size());
+  return DG_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Laplace vmult dispatch
+
+template <int N>
+static LapTab<N> lap_tab(const Basis1D &b) {
+  LapTab<N> t;
+  for (int i = 0; i < N * N; ++i) {
+    t.M[i] = b.M[i];
+    t.K[i] = b.K[i];
+  }
+  for (int i = 0; i < N; ++i) {
+    t.dL[i] = b.ld[i];
+    t.dR[i] = b.rd[i];
+  }
+  return t;
+}
+
+template <int DIM, int N, int BX, int BY, int BZ>
+static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
+                          cudaStream_t st) {
+  using C = LapCfg<DIM, N, BX, BY, BZ>;
+  auto kern = laplace_vmult_kernel<DIM, N, BX, BY, BZ>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  const Geo g = c->geo();
+  const int nb = ((g.nx + BX - 1) / BX) * ((g.ny + BY - 1) / BY) * ((g.nz + BZ - 1) / BZ);
+  kern<<<nb, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part);
+  DG_LAUNCH_CHECK("laplace_vmult_kernel");
+  return DG_OK;
+}
+
+static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
+                            cudaStream_t st) {
+  if (c->dim == 3) {
+    switch (c->n) {
+      case 2: return launch_laplace<3, 2, 8, 4, 4>(c, src, dst, tau_scale, part, st);
+      case 3: return launch_laplace<3, 3, 4, 4, 4>(c, src, dst, tau_scale, part, st);
+      case 4: return launch_laplace<3, 4, 4, 4, 2>(c, src, dst, tau_scale, part, st);
+      case 5: return launch_laplace<3, 5, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+      case 6: return launch_laplace<3, 6, 2, 2, 2>(c, src, dst, tau_scale, part, st);
+      case 7: return launch_laplace<3, 7, 2, 2, 2>(c, src, dst, tau_scale, part, st);
+      case 8: return launch_laplace<3, 8, 2, 2, 2>(c, src, dst, tau_scale, part, st);
+    }
+  } else {
+    switch (c->n) {
+      case 2: return launch_laplace<2, 2, 16, 16, 1>(c, src, dst, tau_scale, part, st);
+      case 3: return launch_laplace<2, 3, 16, 8, 1>(c, src, dst, tau_scale, part, st);
+      case 4: return launch_laplace<2, 4, 16, 8, 1>(c, src, dst, tau_scale, part, st);
+      case 5: return launch_laplace<2, 5, 8, 8, 1>(c, src, dst, tau_scale, part, st);
+      case 6: return launch_laplace<2, 6, 8, 8, 1>(c, src, dst, tau_scale, part, st);
+      case 7: return launch_laplace<2, 7, 8, 8, 1>(c, src, dst, tau_scale, part, st);
+      case 8: return launch_laplace<2, 8, 8, 8, 1>(c, src, dst, tau_scale, part, st);
+    }
+  }
+  return inval("unsupported degree");
+}
+
+// ---------------------------------------------------------------------------
+// element-wise helpers
+
+// w_i = integral of the nodal basis function i: prod_d (h_d/2) wint[i_d]
+struct WInt {
+  double w[kMaxN];
+};
+
+__device__ __forceinline__ double dual_weight(const Geo &g, int dim, int n, const WInt &wi,
+                                              int64_t i) {
+  const int64_t np = (dim == 3) ? (int64_t)n * n * n : (int64_t)n * n;
+  const int64_t e = i / np;
+  int o = (int)(i % np);
+  const int x = o % n;
+  o /= n;
+  const int y = o % n;
+  const int z = (dim == 3) ? o / n : 0;
+  const int ix = (int)(e % g.nx);
+  const int64_t r = e / g.nx;
+  const int iy = (int)(r % g.ny);
+  const int iz = (int)(r / g.ny);
+  double v = 0.5 * g.hx[ix] * wi.w[x] * 0.5 * g.hy[iy] * wi.w[y];
+  if (dim == 3) v *= 0.5 * g.hz[iz] * wi.w[z];
+  return v;
+}
+
+__global__ void wdot_partial_kernel(const double *__restrict__ p, int64_t n, Geo g, int dim,
+                                    int nn, WInt wi, double *__restrict__ partial) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    acc += p[i] * dual_weight(g, dim, nn, wi, i);
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+
+// b_i -= (s / vol) * w_i   (mode 0, dual projection)   or   p_i -= s / vol (mode 1)
+__global__ void zero_mean_apply_kernel(double *__restrict__ b, int64_t n, Geo g, int dim, int nn,
+                                       WInt wi, const double *__restrict__ s, double vol,
+                                       int mode) {
+  const double coef = __ddiv_rn(*s, vol);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    if (mode == 0) b[i] = __dsub_rn(b[i], __dmul_rn(coef, dual_weight(g, dim, nn, wi, i)));
+    else b[i] = __dsub_rn(b[i], coef);
+  }
+}
+
+static WInt wint_of(const dg_ctx *c) {
+  WInt w;
+  for (int i = 0; i < kMaxN; ++i) w.w[i] = i < c->n ? c->basis.wint[i] : 0.0;
+  return w;
+}
+
+static int reduce_sum(dg_ctx *c, const double *x, const double *y, int64_t n, double *out,
+                      cudaStream_t st) {
+  dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(x, y, n, c->d_red);
+  sum_partials_kernel<<<1, 1024, 0, st>>>(c->d_red, kRedBlocks, out);
+  DG_LAUNCH_CHECK("dot");
+  return DG_OK;
+}
+
+static int grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return (int)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+extern "C" {
+
+int dg_laplace_vmult(dg_ctx *c, const double *src, double *dst, double tau_scale, void *stream) {
+  if (!c || !src || !dst) return inval("null argument");
+  if ((c->mode[0] == kGhost && !c->d_recv[0]) || (c->mode[1] == kGhost && !c->d_recv[1]))
+    return inval("x-slab context: attach ghost layers (dg_halo_attach) first");
+  return laplace_dispatch(c, src, dst, tau_scale, 0, (cudaStream_t)stream);
+}
+
+int dg_laplace_vmult_part(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
+                          void *stream) {
+  if (!c || !src || !dst) return inval("null argument");
+  if (part < 0 || part > 2) return inval("part must be 0, 1 or 2");
+  if (part != 1 &&
+      ((c->mode[0] == kGhost && !c->d_recv[0]) || (c->mode[1] == kGhost && !c->d_recv[1])))
+    return inval("x-slab context: attach ghost layers (dg_halo_attach) first");
+  return laplace_dispatch(c, src, dst, tau_scale, part, (cudaStream_t)stream);
+}
+
+int dg_dot(dg_ctx *c, const double *x, const double *y, int64_t n, double *out_dev,
+           void *stream) {
+  if (!c || !x || !out_dev) return inval("null argument");
+  return reduce_sum(c, x, y, n, out_dev, (cudaStream_t)stream);
+}
+
+int dg_zero_mean_dual(dg_ctx *c, double *b, void *stream) {
+  if (!c || !b) return inval("null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = reduce_sum(c, b, nullptr, c->n_dofs, c->d_scal + 8, st);
+  if (rc) return rc;
+  zero_mean_apply_kernel<<<grid_for(c->n_dofs), 256, 0, st>>>(b, c->n_dofs, c->geo(), c->dim, c->n,
+                                                               wint_of(c), c->d_scal + 8, c->volume, 0);
+  DG_LAUNCH_CHECK("zero_mean_dual");
+  return DG_OK;
+}
+
+int dg_zero_mean(dg_ctx *c, double *p, void *stream) {
+  if (!c || !p) return inval("null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  wdot_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(p, c->n_dofs, c->geo(), c->dim, c->n,
+                                                          wint_of(c), c->d_red);
+  sum_partials_kernel<<<1, 1024, 0, st>>>(c->d_red, kRedBlocks, c->d_scal + 9);
+  zero_mean_apply_kernel<<<grid_for(c->n_dofs), 256, 0, st>>>(p, c->n_dofs, c->geo(), c->dim, c->n,
+                                                               wint_of(c), c->d_scal + 9, c->volume, 1);
+  DG_LAUNCH_CHECK("zero_mean");
+  return DG_OK;
+}
+
+int dg_halo_count(const dg_ctx *c, int64_t *count) {
+  if (!c || !count) return inval("null argument");
+  *count = c->halo_count;
+  return DG_OK;
+}
+
+int dg_halo_attach(dg_ctx *c, const double *recv_lo, const double *recv_hi) {
+  if (!c) return inval("null context");
+  if ((c->mode[0] == kGhost && !recv_lo) || (c->mode[1] == kGhost && !recv_hi))
+    return inval("a remote side needs a ghost buffer");
+  c->d_recv[0] = recv_lo;
+  c->d_recv[1] = recv_hi;
+  return DG_OK;
+}
+
+int dg_halo_pack(dg_ctx *c, const double *src, double *send_lo, double *send_hi, void *stream) {
+  if (!c || !src) return inval("null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t row = sizeof(double) * c->np;
+  const size_t pitch = row * c->counts[0];
+  const size_t rows = (size_t)c->counts[1] * c->counts[2];
+  if (send_lo)
+    DG_CUDA_CHECK(cudaMemcpy2DAsync(send_lo, row, src, pitch, row, rows,
+                                    cudaMemcpyDeviceToDevice, st));
+  if (send_hi)
+    DG_CUDA_CHECK(cudaMemcpy2DAsync(send_hi, row, src + (size_t)(c->counts[0] - 1) * c->np,
+                                    pitch, row, rows, cudaMemcpyDeviceToDevice, st));
+  return DG_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// mass / inverse mass (tensor-product apply), diagonal
+
+template <int DIM, int N>
+static int launch_tensor(dg_ctx *c, const double *src, double *dst, int ncomp, bool inverse,
+                         cudaStream_t st) {
+  TensorTab<N> t;
+  const std::vector<double> &A = inverse ? c->basis.Minv : c->basis.M;
+  for (int i = 0; i < N * N; ++i) t.A[i] = A[i];
+  using TC = TensorCfg<DIM, N>;
+  const int64_t cells = c->n_cells * ncomp;
+  const int nb = (int)((cells + TC::NC - 1) / TC::NC);
+  tensor_apply_kernel<DIM, N><<<nb, TC::THREADS, TC::SMEM, st>>>(src, dst, c->geo(), t, cells,
+                                                                  inverse ? 1 : 0);
+  DG_LAUNCH_CHECK("tensor_apply_kernel");
+  return DG_OK;
+}
+
+static int tensor_dispatch(dg_ctx *c, const double *src, double *dst, int ncomp, bool inverse,
+                           cudaStream_t st) {
+#define DG_T(D, NN) \
+  case NN: return launch_tensor<D, NN>(c, src, dst, ncomp, inverse, st);
+  if (c->dim == 3) {
+    switch (c->n) { DG_T(3, 2) DG_T(3, 3) DG_T(3, 4) DG_T(3, 5) DG_T(3, 6) DG_T(3, 7) DG_T(3, 8) }
+  } else {
+    switch (c->n) { DG_T(2, 2) DG_T(2, 3) DG_T(2, 4) DG_T(2, 5) DG_T(2, 6) DG_T(2, 7) DG_T(2, 8) }
+  }
+#undef DG_T
+  return inval("unsupported degree");
+}
+
+struct DiagTab {
+  double Mdiag[kMaxN], Kdiag[kMaxN];
+  double dL0, dRn;
+};
+
+// exact diagonal of the element block (operators.py:675-730): volume
+// sum_d s_d (2/h_d) K_ii prod M_jj plus the own-side face terms at end nodes
+__global__ void laplace_diag_kernel(double *__restrict__ diag, Geo g, int dim, int n, DiagTab t,
+                                    double tau_scale, int64_t ndofs) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t np = (dim == 3) ? (int64_t)n * n * n : (int64_t)n * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndofs; i += stride) {
+    const int64_t e = i / np;
+    int o = (int)(i % np);
+    int idx[3];
+    idx[0] = o % n;
+    o /= n;
+    idx[1] = o % n;
+    idx[2] = (dim == 3) ? o / n : 0;
+    int cc[3];
+    cc[0] = (int)(e % g.nx);
+    cc[1] = (int)((e / g.nx) % g.ny);
+    cc[2] = (int)(e / ((int64_t)g.nx * g.ny));
+    const double h[3] = {g.hx[cc[0]], g.hy[cc[1]], dim == 3 ? g.hz[cc[2]] : 2.0};
+    const double taue = g.tau[e];
+    double acc = 0.0;
+    for (int d = 0; d < dim; ++d) {
+      double sfac = 1.0, tang = 1.0;
+      for (int dd = 0; dd < dim; ++dd)
+        if (dd != d) {
+          sfac *= 0.5 * h[dd];
+          tang *= t.Mdiag[idx[dd]];
+        }
+      double line = 2.0 / h[d] * t.Kdiag[idx[d]];
+      for (int s = 0; s < 2; ++s) {
+        if (idx[d] != (s ? n - 1 : 0)) continue;
+        // neighbour kind
+        const int nmax = d == 0 ? g.nx : d == 1 ? g.ny : g.nz;
+        const bool at_edge = s ? (cc[d] == nmax - 1) : (cc[d] == 0);
+        int kind = 0;
+        double taun = 0.0;
+        if (at_edge) {
+          const int m = g.mode[2 * d + s];
+          if (m == kBndNone || m == kBndNeumann) kind = m;
+          else if (m == kGhost) taun = g.ghost_tau[s][cc[1] + (int64_t)g.ny * cc[2]];
+          else {
+            int c2[3] = {cc[0], cc[1], cc[2]};
+            c2[d] = s ? 0 : nmax - 1;
+            taun = g.tau[c2[0] + (int64_t)g.nx * (c2[1] + (int64_t)g.ny * c2[2])];
+          }
+        } else {
+          int c2[3] = {cc[0], cc[1], cc[2]};
+          c2[d] += s ? 1 : -1;
+          taun = g.tau[c2[0] + (int64_t)g.nx * (c2[1] + (int64_t)g.ny * c2[2])];
+        }
+        const double dend = s ? t.dRn : t.dL0;  // own derivative row at own end node
+        const double sg = s ? -1.0 : 1.0;
+        if (kind == 0) line += sg * 2.0 * dend / h[d] + tau_scale * fmax(taue, taun);
+        else if (kind == kBndNeumann) line += sg * 4.0 * dend / h[d] + 2.0 * tau_scale * taue;
+      }
+      acc += sfac * tang * line;
+    }
+    diag[i] = acc;
+  }
+}
+
+extern "C" {
+
+int dg_mass(dg_ctx *c, const double *src, double *dst, int ncomp, void *stream) {
+  if (!c || !src || !dst || ncomp < 1) return inval("invalid argument");
+  return tensor_dispatch(c, src, dst, ncomp, false, (cudaStream_t)stream);
+}
+
+int dg_inverse_mass(dg_ctx *c, const double *src, double *dst, int ncomp, void *stream) {
+  if (!c || !src || !dst || ncomp < 1) return inval("invalid argument");
+  return tensor_dispatch(c, src, dst, ncomp, true, (cudaStream_t)stream);
+}
+
+int dg_laplace_diagonal(dg_ctx *c, double *diag, double tau_scale, void *stream) {
+  if (!c || !diag) return inval("null argument");
+  DiagTab t;
+  for (int i = 0; i < c->n; ++i) {
+    t.Mdiag[i] = c->basis.M[i * c->n + i];
+    t.Kdiag[i] = c->basis.K[i * c->n + i];
+  }
+  t.dL0 = c->basis.ld[0];
+  t.dRn = c->basis.rd[c->n - 1];
+  laplace_diag_kernel<<<grid_for(c->n_dofs), 256, 0, (cudaStream_t)stream>>>(
+      diag, c->geo(), c->dim, c->n, t, tau_scale, c->n_dofs);
+  DG_LAUNCH_CHECK("laplace_diag_kernel");
+  return DG_OK;
+}
+
+}  // extern "C"
+
+#include "pcg.inc"
+
+// ---------------------------------------------------------------------------
+// vector-valued operators (Helmholtz, projection, convective) live in
+// vecops.inc
+#include "vecops.inc"

@@ -1,0 +1,162 @@
+"""DgSpace: mesh + degree + device contexts (reference spaces.py:61-163).
+
+A space owns one device context per boundary-kind assignment (the reference
+passes ``bcs`` per operator call; the context bakes the per-tag kinds into
+its face modes).  Contexts hold the Cartesian geometry (cell sizes per axis),
+tau_e per cell (Eq. 18, geometry.py:90-108) and the 1D tables.
+
+Device vectors are torch CUDA tensors in element-major order
+(component, cell, [z,] y, x); ``to_device`` / ``to_host`` convert the
+reference's 2D kernel layout (m, ne, m) (spaces.py:18-58).
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .mesh import BoxMesh, TAG_NAMES
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise _lib.DgError("no CUDA device: the DG operators run only on the GPU "
+                           "(there is no CPU fallback)")
+    return torch
+
+
+class DeviceContext:
+    """Owns one dg_ctx (include/dgmf.h)."""
+
+    def __init__(self, mesh, k, bc_kinds, n_q_over=0, slab=None):
+        _torch()
+        L = _lib.lib()
+        self._verts = [np.ascontiguousarray(v, dtype=np.float64)
+                       for v in mesh.axis_vertices]
+        desc = _lib.MeshDesc()
+        desc.dim = mesh.dim
+        desc.k = k
+        desc.n_q_over = int(n_q_over or 0)
+        for d in range(3):
+            desc.counts[d] = mesh.counts[d] if d < mesh.dim else 1
+            desc.periodic[d] = int(mesh.periodic[d]) if d < mesh.dim else 0
+        for d in range(mesh.dim):
+            desc.vertices[d] = self._verts[d].ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        for t in range(6):
+            desc.bc_kind[t] = bc_kinds[t]
+        desc.slab_begin, desc.slab_end = slab if slab is not None else (0, 0)
+        h = ctypes.c_void_p()
+        _lib.check(L.dg_ctx_create(ctypes.byref(desc), ctypes.byref(h)))
+        self.handle = h
+        nc, nd = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(L.dg_ctx_sizes(h, ctypes.byref(nc), ctypes.byref(nd)))
+        self.n_cells, self.n_dofs = nc.value, nd.value
+        self._L = L
+
+    def tau(self):
+        out = np.empty(self.n_cells)
+        _lib.check(self._L.dg_ctx_tau(self.handle, out.ctypes.data_as(
+            ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._L.dg_ctx_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+class DgSpace:
+    def __init__(self, mesh: BoxMesh, k: int, n_q_over=None):
+        if k < 1:
+            raise ValueError(f"polynomial degree must be >= 1, got k={k}")
+        if k > 7:
+            raise ValueError("the device path supports k <= 7")
+        self.mesh = mesh
+        self.dim = mesh.dim
+        self.k = k
+        self.n_q_over = n_q_over or ((3 * k) // 2 + 1)
+        self._ctx = {}
+
+    @property
+    def n_local(self):
+        return (self.k + 1) ** self.dim
+
+    @property
+    def n_dofs(self):
+        return self.mesh.n_elements * self.n_local
+
+    def field_shape(self, ncomp=None):
+        s = (self.mesh.n_elements,) + (self.k + 1,) * self.dim
+        return s if ncomp is None else (ncomp,) + s
+
+    def ctx(self, bc_kinds=(0, 0, 0, 0, 0, 0), slab=None) -> DeviceContext:
+        key = (tuple(bc_kinds), slab)
+        if key not in self._ctx:
+            self._ctx[key] = DeviceContext(self.mesh, self.k, bc_kinds,
+                                           self.n_q_over, slab)
+        return self._ctx[key]
+
+    def default_kinds(self):
+        """Velocity-Dirichlet on every boundary tag (any kind gives the same
+        mass / inverse-mass / zero-mean result)."""
+        kinds = [0] * 6
+        for d in range(self.dim):
+            if not self.mesh.periodic[d]:
+                kinds[2 * d] = kinds[2 * d + 1] = _lib.BC_VELOCITY_DIRICHLET
+        return tuple(kinds)
+
+    def node_coords(self):
+        """Physical GLL node coordinates, (dim, ne, [z,] y, x)."""
+        from .basis import gll_nodes
+        xi = gll_nodes(self.k)
+        m = self.k + 1
+        out = []
+        idx = np.indices(self.mesh.counts[::-1]).reshape(self.dim, -1)[::-1]  # ix, iy, iz
+        for d in range(self.dim):
+            v = self.mesh.axis_vertices[d]
+            lo = v[idx[d]]
+            h = np.diff(v)[idx[d]]
+            c = lo[:, None] + 0.5 * (xi[None, :] + 1.0) * h[:, None]
+            shape = [self.mesh.n_elements] + [1] * self.dim
+            shape[self.dim - d] = m
+            out.append(np.broadcast_to(c.reshape(shape), self.field_shape()))
+        return np.stack(out)
+
+    # --- layout conversion (reference kernel layout <-> element-major) ---
+    def is_reference_layout(self, a, ncomp):
+        """2D reference kernel layout (m, ne, m) / (ncomp, m, ne, m)."""
+        if self.dim != 2:
+            return False
+        m, ne = self.k + 1, self.mesh.n_elements
+        want = (m, ne, m) if ncomp == 1 else (ncomp, m, ne, m)
+        return tuple(a.shape) == want and (ne != m or ncomp != 1)
+
+    def to_element_major(self, a, ncomp):
+        a = np.asarray(a, dtype=np.float64)
+        if self.dim == 2 and a.ndim == (3 if ncomp == 1 else 4) and \
+                a.shape[-3:] == (self.k + 1, self.mesh.n_elements, self.k + 1):
+            if ncomp == 1:
+                return np.ascontiguousarray(a.transpose(1, 0, 2))
+            return np.ascontiguousarray(a.transpose(0, 2, 1, 3))
+        return np.ascontiguousarray(a.reshape(self.field_shape(None if ncomp == 1 else ncomp)))
+
+    def from_element_major(self, a, ncomp, like_shape):
+        if self.dim == 2 and len(like_shape) == (3 if ncomp == 1 else 4) and \
+                tuple(like_shape[-3:]) == (self.k + 1, self.mesh.n_elements, self.k + 1):
+            a = a.reshape(self.field_shape(None if ncomp == 1 else ncomp))
+            if ncomp == 1:
+                return np.ascontiguousarray(a.transpose(1, 0, 2))
+            return np.ascontiguousarray(a.transpose(0, 2, 1, 3))
+        return a.reshape(like_shape)
+
+
+def tag_kinds_tuple(space, kinds_by_tag):
+    out = [0] * 6
+    for t, kind in kinds_by_tag.items():
+        out[TAG_NAMES.index(t)] = kind
+    return tuple(out)

@@ -168,8 +168,9 @@ def main():
         rng2 = np.random.default_rng(987)
         seed_vec = rng2.standard_normal(diag.shape)   # reference layout draw
         seed_vec = sol.zero_mean_project(space, seed_vec)
+        # multigrid.py:106-113: est_op = project(L(p)), project = zero_mean_project
         lmax, _ = sol.eigen_estimate_via_cg(
-            lambda v: sol.zero_mean_project(space, op(v)), diag, seed_vec, 20)
+            lambda v: sol.zero_mean_project(space, L(v)), diag, seed_vec, 20)
         cfg = sol.ChebyshevConfig(5, 20.0, 1.1 * lmax)
         out[key + "_seed"] = em(space, seed_vec)
         out[key + "_lmax"] = np.array(lmax)

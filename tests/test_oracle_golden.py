@@ -88,7 +88,7 @@ def test_solver_histories_match_reference(k, nx):
     op = lambda p: O.zero_mean_project_dual(space, L(p))
     diag = O.laplace_diagonal(space, bcs)
     seed = O.zero_mean_project(space, Z[key + "_seed"].reshape(sh))
-    lmax, _ = O.eigen_estimate_via_cg(lambda v: O.zero_mean_project(space, op(v)),
+    lmax, _ = O.eigen_estimate_via_cg(lambda v: O.zero_mean_project(space, L(v)),
                                       diag, seed, 20)
     assert abs(lmax - float(Z[key + "_lmax"])) < 1e-12 * lmax
     cfg = O.ChebyshevConfig(5, 20.0, 1.1 * lmax)
