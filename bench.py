@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark of the matrix-free DG hot path (BASELINE.json metric).
+
+Headline: SIP Laplace vmult DoF/s (fp64) on BASELINE config 5 -- unit cube,
+128^3 Cartesian cells, Q4 (262,144,000 DoFs), walls -- split into x-slabs
+across N GPUs (strong scaling, NCCL halo exchange overlapped with interior
+cells).  A "step" is one vmult over the whole mesh.  Inputs are larger than
+L2 (2.1 GB per vector), so no L2 flush is needed between steps.
+
+Also reported on the same JSON line (rank 0):
+  roofline      HBM roofline of the vmult kernel (16 B/DoF algorithmic)
+  fp64          fp64 issue-rate view of the same kernel (flop count by design)
+  e2e           the same metric through the public API with host buffers
+                (pinned H2D of the input + D2H of the result every step)
+  cg            BASELINE config 2: Chebyshev(5)-Jacobi PCG to 1e-10 on
+                32^3 Q4 (N=1 only)
+  cpu_baseline  the numpy oracle (restated reference algorithm) on a
+                bounded sample, on this host (N=1, rank 0)
+  clocks        SM clocks / throttle reasons sampled (NVML) during the
+                timed region
+
+--impl reference: the reference algorithm on the host CPU (numpy port in
+oracle/, all host threads), same metric, bounded sample per step.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6553.3
+BYTES_PER_DOF = 16.0          # read src + write dst, fp64
+# fp64 instruction count per DoF of laplace_vmult_kernel:
+# 7 sweeps x n FMA + face terms; flops = 2 per FMA
+FMA_PER_DOF = {n: 7 * n + 18 for n in range(2, 9)}
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake", 0x100: "display_clocks"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cells", type=int, default=128, help="cells per axis (C5: 128)")
+    ap.add_argument("--k", type=int, default=4)
+    ap.add_argument("--no-cg", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep", action="store_true",
+                    help="also print the Q2-Q7 degree sweep at 64^3 (extra lines)")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons in a thread."""
+
+    def __init__(self, index, period=0.02):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        r = [name for bit, name in REASONS.items() if self.reasons & bit]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": r}
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(k):
+    """DRAM bytes per launch of laplace_vmult_kernel from the committed ncu
+    --set full summary (profiles/ncu_laplace.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_laplace.json")) as f:
+            d = json.load(f)
+        return d.get(f"k{k}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def oracle_sample(k, cells, threads_all):
+    """Reference algorithm (numpy port in oracle/) on a bounded sample:
+    cells^3 box, walls, Q_k; returns (DoF/s, dofs, seconds per vmult)."""
+    import numpy as np
+    from oracle import dg_oracle as O
+    m = O.build_box_mesh(((0, 1),) * 3, (cells,) * 3)
+    sp = O.DgSpace(m, k)
+    b = O.BoundarySpec({t: O.zero_dirichlet(3) for t in m.tag_names}).resolve(sp)
+    p = np.random.default_rng(4).uniform(-1, 1, sp.field_shape())
+    O.apply_pressure_laplace(sp, p, b)
+    return sp, b, p
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's algorithm on the host CPU."""
+    if rank != 0:
+        return
+    import numpy as np
+    try:
+        import threadpoolctl
+        threadpoolctl.threadpool_limits(os.cpu_count())
+    except Exception:
+        pass
+    from oracle import dg_oracle as O
+    cells = 24 if args.k <= 4 else 16
+    sp, b, p = oracle_sample(args.k, cells, True)
+    for _ in range(args.warmup):
+        O.apply_pressure_laplace(sp, p, b)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.apply_pressure_laplace(sp, p, b)
+    dt = time.perf_counter() - t0
+    val = p.size * args.steps / dt
+    cores = len(os.sched_getaffinity(0))
+    line = {
+        "impl": "reference", "metric": "SIP Laplace vmult DoF/s (fp64)", "value": val,
+        "unit": "DoF/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C5-shaped SIP Laplace vmult sample: {cells}^3 cells, Q{args.k}, "
+                               f"walls, uniform[-1,1] seed 4 (numpy port of the reference "
+                               f"algorithm; the reference package itself is 2D-only)",
+                   "cells": cells, "k": args.k},
+        "cpu_baseline": {"value": val, "unit": "DoF/s", "cores": cores, "kind": "port",
+                         "sample": f"{cells}^3 Q{args.k} vmult x {args.steps}"},
+        "e2e": {"value": val, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(k):
+    """Oracle port on 1 core, ~10-20 s of CPU work."""
+    try:
+        import threadpoolctl
+        threadpoolctl.threadpool_limits(1)
+    except Exception:
+        pass
+    from oracle import dg_oracle as O
+    cells = 24 if k <= 4 else 16
+    sp, b, p = oracle_sample(k, cells, False)
+    reps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < 10.0:
+        O.apply_pressure_laplace(sp, p, b)
+        reps += 1
+    dt = time.perf_counter() - t0
+    return {"value": p.size * reps / dt, "unit": "DoF/s", "cores": 1, "kind": "port",
+            "sample": f"{cells}^3 cells Q{k} walls vmult x {reps} (numpy port, 1 thread)"}
+
+
+def run_cg(dist_on):
+    """BASELINE config 2: 32^3, Q4, periodic x,z, walls y, pure Neumann,
+    rhs = zero_mean_project_dual(M (sin 2pi x cos pi y sin 2pi z + 1e-3 N(0,1),
+    seed 1)), Chebyshev(5, 20) over Jacobi, rel_tol 1e-10."""
+    import numpy as np
+    import torch
+    from paper_1607_01323_b200 import mesh as M, operators as ops, solvers as sol
+    from paper_1607_01323_b200.spaces import DgSpace
+    mesh = M.build_box_mesh(((0, 1),) * 3, (32, 32, 32), periodic=(True, False, True))
+    space = DgSpace(mesh, 4)
+    bcs = ops.BoundarySpec({"ymin": ops.DirichletBC(None),
+                            "ymax": ops.DirichletBC(None)}).resolve(space)
+    xn = space.node_coords()
+    f = np.sin(2 * np.pi * xn[0]) * np.cos(np.pi * xn[1]) * np.sin(2 * np.pi * xn[2])
+    f = f + 1e-3 * np.random.default_rng(1).standard_normal(f.shape)
+    b = sol.zero_mean_project_dual(space, ops.mass_apply(space, torch.as_tensor(
+        f.ravel(), device="cuda")))
+    diag = ops.laplace_diagonal(space, bcs)
+    lmax = sol.lanczos_lambda_max(space, bcs, diag, project=True)
+    cfg = sol.ChebyshevConfig(5, 20.0, lmax)
+    sol.laplace_pcg(space, bcs, b, project_dual=True, cheb=cfg, diag=diag, rel_tol=1e-10,
+                    max_iter=5)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    x, st = sol.laplace_pcg(space, bcs, b, project_dual=True, cheb=cfg, diag=diag,
+                            rel_tol=1e-10, max_iter=5000)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    return {"config": "C2: 32^3 Q4 periodic x,z / walls y, Chebyshev(5,20)-Jacobi PCG, rel_tol 1e-10",
+            "dofs": space.n_dofs, "iterations": st.iterations, "converged": st.converged,
+            "solve_ms": 1e3 * dt, "ms_per_iteration": 1e3 * dt / max(st.iterations, 1),
+            "dof_per_s_per_iteration": space.n_dofs * st.iterations / dt,
+            "lambda_max": lmax}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1607_01323_b200 import mesh as M, _lib
+    from paper_1607_01323_b200.parallel import SlabLaplace
+
+    n, k = args.cells, args.k
+    mesh = M.build_box_mesh(((0, 1),) * 3, (n, n, n))
+    kinds = (_lib.BC_VELOCITY_DIRICHLET,) * 6
+    op = SlabLaplace(mesh, k, kinds, rank, world)
+    nd = op.n_dofs
+    total = mesh.n_elements * (k + 1) ** 3
+    g = torch.Generator(device="cuda").manual_seed(4 + rank)
+    src = torch.rand(nd, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    dst = torch.empty_like(src)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        op.vmult(src, dst)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            op.vmult(src, dst)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    ms_step = ms / args.steps
+    value = total / (ms_step * 1e-3)
+
+    # end to end through the public API: pinned host in -> device -> host out
+    e2e = None
+    if not args.no_e2e:
+        K2 = max(3, min(args.steps, 10))
+        h_in = torch.empty(nd, dtype=torch.float64, pin_memory=True)
+        h_in.copy_(src.cpu())
+        h_out = torch.empty(nd, dtype=torch.float64, pin_memory=True)
+        d_in = torch.empty_like(src)
+        for _ in range(2):
+            d_in.copy_(h_in, non_blocking=True)
+            op.vmult(d_in, dst)
+            h_out.copy_(dst, non_blocking=True)
+        torch.cuda.synchronize()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(K2):
+            d_in.copy_(h_in, non_blocking=True)
+            op.vmult(d_in, dst)
+            h_out.copy_(dst, non_blocking=True)
+        f1.record()
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": total / (ems / K2 * 1e-3), "unit": "DoF/s",
+               "h2d_bytes_per_step": 8 * total, "d2h_bytes_per_step": 8 * total,
+               "ms_per_step": ems / K2, "steps": K2}
+
+    cg = None
+    if rank == 0 and world == 1 and not args.no_cg:
+        cg = run_cg(False)
+    sweep = []
+    if rank == 0 and world == 1 and args.sweep:
+        sweep = run_sweep()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(k)
+
+    if rank == 0:
+        peak, peak_kind = hbm_peak()
+        per_rank_dofs = nd
+        achieved = per_rank_dofs * BYTES_PER_DOF / (ms_step * 1e-3) / 1e9
+        clocks = clk.summary()
+        fma = FMA_PER_DOF.get(k + 1)
+        sm_mhz = clocks["sm_mhz"] or 1965.0
+        fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+        fp64_ach = per_rank_dofs * 2 * fma / (ms_step * 1e-3) / 1e12 if fma else None
+        line = {
+            "metric": "SIP Laplace vmult DoF/s (fp64)",
+            "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: uniform[-1,1] input vector (torch generator seed 4+rank)",
+            "config": {"workload": f"C5: SIP Laplace vmult, unit cube {n}^3 Cartesian cells, "
+                                   f"Q{k} DG (GLL nodes, {k + 1} Gauss points), velocity-Dirichlet "
+                                   f"walls, x-slabs over {world} GPU(s)",
+                       "cells": n, "k": k, "dofs": total, "parallelism": f"x-slabs{world}",
+                       "l2": "inputs (8 B/DoF x dofs) larger than L2; no flush"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(k),
+                         "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_dof": BYTES_PER_DOF,
+                         "kernel": "laplace_vmult_kernel"},
+            "fp64": {"fma_per_dof": fma, "achieved_tflops": fp64_ach,
+                     "peak_tflops_at_clock": fp64_peak,
+                     "frac": (fp64_ach / fp64_peak) if fma else None,
+                     "peak_kind": "nominal 64 DFMA/clk/SM x 148 SMs x median SM clock"},
+            "gpu_launches": args.steps * (1 if world == 1 else 2),
+            "clocks": clocks,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cg:
+            line["cg"] = cg
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+        for s in sweep:
+            print(json.dumps(s), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_sweep():
+    """Degree sweep Q2-Q7 at 64^3 cells on one GPU (config 5 second part)."""
+    import torch
+    from paper_1607_01323_b200 import mesh as M, _lib
+    from paper_1607_01323_b200.parallel import SlabLaplace
+    out = []
+    mesh = M.build_box_mesh(((0, 1),) * 3, (64, 64, 64))
+    peak, _ = hbm_peak()
+    for k in range(2, 8):
+        op = SlabLaplace(mesh, k, (_lib.BC_VELOCITY_DIRICHLET,) * 6, 0, 1)
+        src = torch.rand(op.n_dofs, dtype=torch.float64, device="cuda")
+        dst = torch.empty_like(src)
+        for _ in range(5):
+            op.vmult(src, dst)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 50
+        e0.record()
+        for _ in range(reps):
+            op.vmult(src, dst)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        dofs = op.n_dofs
+        out.append({"sweep": "laplace_vmult_64cubed", "k": k, "dofs": dofs, "ms": ms,
+                    "dof_per_s": dofs / (ms * 1e-3),
+                    "hbm_frac": dofs * BYTES_PER_DOF / (ms * 1e-3) / 1e9 / peak})
+        del op, src, dst
+        torch.cuda.empty_cache()
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -159,8 +159,7 @@ int dg_ctx_create(const dg_mesh_desc *desc, dg_ctx **out) {
         return inval("non-positive mapping Jacobian (vertex coordinates must increase)");
       }
   }
-  c->gvert[2].assign({0.0, 2.0});
-  if (c->dim == 2) c->gvert[2] = {0.0, 2.0};
+  if (c->dim == 2) c->gvert[2] = {0.0, 2.0};  // unit-free dummy z extent
   for (int t = 0; t < 6; ++t) c->bc[t] = (t < 2 * c->dim) ? desc->bc_kind[t] : 0;
   for (int d = 0; d < c->dim; ++d)
     for (int s = 0; s < 2; ++s) {

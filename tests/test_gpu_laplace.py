@@ -193,7 +193,10 @@ def test_generic_pcg_callables_match_fused():
     x1, s1 = sol.pcg(op, lambda r: sol.chebyshev_smooth(L, diag, cfg, r), b, rel_tol=1e-10)
     x2, s2 = sol.laplace_pcg(space, bcs, b, project_dual=True, cheb=cfg, diag=diag, rel_tol=1e-10)
     assert s1.iterations == s2.iterations
-    np.testing.assert_allclose(s1.history, s2.history, rtol=1e-9)
+    # torch (cuBLAS) vs deterministic fixed-order dots: histories agree to
+    # 1e-10 of the initial residual (summation-order sensitivity)
+    np.testing.assert_allclose(s1.history, s2.history, rtol=1e-7,
+                               atol=1e-10 * s1.history[0])
     assert relerr(host(x1), host(x2)) < 1e-9
 
 
