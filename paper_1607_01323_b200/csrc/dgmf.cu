@@ -308,15 +308,25 @@ static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_
     attr = true;
   }
   const Geo g = c->geo();
-  const int nb = ((g.nx + BX - 1) / BX) * ((g.ny + BY - 1) / BY) * ((g.nz + BZ - 1) / BZ);
-  kern<<<nb, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part);
+  const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, (g.nz + BZ - 1) / BZ);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part);
   DG_LAUNCH_CHECK("laplace_vmult_kernel");
   return DG_OK;
 }
 
 static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                             cudaStream_t st) {
+  static const int variant = [] {
+    const char *v = getenv("DG_LAP_VARIANT");  // brick-shape experiments
+    return v ? atoi(v) : 0;
+  }();
   if (c->dim == 3) {
+    if (c->n == 5 && variant == 1) return launch_laplace<3, 5, 2, 2, 2>(c, src, dst, tau_scale, part, st);
+    if (c->n == 5 && variant == 2) return launch_laplace<3, 5, 4, 4, 1>(c, src, dst, tau_scale, part, st);
+    if (c->n == 5 && variant == 3) return launch_laplace<3, 5, 2, 2, 1>(c, src, dst, tau_scale, part, st);
+    if (c->n == 4 && variant == 1) return launch_laplace<3, 4, 2, 2, 2>(c, src, dst, tau_scale, part, st);
+    if (c->n == 4 && variant == 2) return launch_laplace<3, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+    if (c->n == 4 && variant == 3) return launch_laplace<3, 4, 4, 4, 1>(c, src, dst, tau_scale, part, st);
     switch (c->n) {
       case 2: return launch_laplace<3, 2, 8, 4, 4>(c, src, dst, tau_scale, part, st);
       case 3: return launch_laplace<3, 3, 4, 4, 4>(c, src, dst, tau_scale, part, st);
