@@ -10,6 +10,7 @@
 #include "laplace.cuh"
 #include "tables.h"
 #include "tensor.cuh"
+#include "vecops.cuh"
 #include "vector.cuh"
 
 namespace dg {

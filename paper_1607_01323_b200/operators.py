@@ -191,30 +191,31 @@ def apply_viscous_helmholtz(space: DgSpace, u, gamma0_dt: float, nu: float,
     return a.result(out)
 
 
-def face_penalty_layout(space, tau_c_f, f_em, f_sm):
-    """Reference per-face tau_C (interior faces listed by minus element/slot)
-    -> device layout [d*ne + e] = penalty of the face between e and its +d
-    neighbour."""
-    ne = space.mesh.n_elements
-    out = np.zeros(space.dim * ne)
-    for t, e, s in zip(tau_c_f, f_em, f_sm):
-        d, side = divmod(int(s), 2)
-        if side == 1:
-            out[d * ne + int(e)] = t
-        else:  # minus side stored on its low face: owner is the -d neighbour
-            raise ValueError("minus side of an interior face must be its +d slot")
+def face_penalty_layout(space, tau_c_f):
+    """Reference per-face tau_C, one entry per interior face in the order of
+    ``space.interior_faces()`` (InteriorFaces, mesh.py:46-59) -> device layout
+    [d*ne + e] = penalty of the face between cell e and its +d neighbour."""
+    em, sm, _, _ = space.interior_faces()
+    tau_c_f = np.asarray(tau_c_f, dtype=np.float64)
+    if tau_c_f.shape != em.shape:
+        raise ValueError(f"tau_c_f needs one entry per interior face ({em.size})")
+    out = np.zeros(space.dim * space.mesh.n_elements)
+    out[(sm // 2) * space.mesh.n_elements + em] = tau_c_f
     return out
 
 
 def apply_projection_operator(space: DgSpace, w, tau_d_e, tau_c_f):
     """M + tau_D div-div + tau_C interior jump penalty (operators.py:372-412).
-    tau_d_e: per cell; tau_c_f: per cell and direction, layout [d*ne + e]
-    (penalty of the face between e and its +d neighbour), or None."""
+
+    tau_d_e: per cell (or None).  tau_c_f: per interior face in the order of
+    ``space.interior_faces()`` as the reference passes it, or already in the
+    device layout [d*ne + e] (a CUDA tensor of dim*ne entries), or None."""
     torch = _torch()
     a = _Arg(space, w, space.dim)
     out = a.new_out()
     ctx = space.ctx(space.default_kinds())
     keep = []
+    ne = space.mesh.n_elements
 
     def dev(x, n):
         if x is None:
@@ -227,7 +228,8 @@ def apply_projection_operator(space: DgSpace, w, tau_d_e, tau_c_f):
         keep.append(t)
         return ctypes_ptr(t.data_ptr())
 
-    ne = space.mesh.n_elements
+    if tau_c_f is not None and not isinstance(tau_c_f, torch.Tensor):
+        tau_c_f = face_penalty_layout(space, tau_c_f)
     _lib.call("dg_projection_vmult", ctx.handle, a.ptr(), ctypes_ptr(out.data_ptr()),
               dev(tau_d_e, ne), dev(tau_c_f, space.dim * ne), _stream())
     return a.result(out)

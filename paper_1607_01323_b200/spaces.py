@@ -110,6 +110,31 @@ class DgSpace:
                 kinds[2 * d] = kinds[2 * d + 1] = _lib.BC_VELOCITY_DIRICHLET
         return tuple(kinds)
 
+    def interior_faces(self):
+        """Interior (incl. periodic) faces as (em, sm, ep, sp) arrays, the
+        reference's InteriorFaces SoA (mesh.py:46-59): direction-major, the
+        minus side is the lower cell with slot 2d+1, the plus side slot 2d."""
+        if getattr(self, "_faces", None) is None:
+            counts = self.mesh.counts
+            e = np.arange(self.mesh.n_elements)
+            idx, rem = [], e
+            for d in range(self.dim):
+                idx.append(rem % counts[d])
+                rem = rem // counts[d]
+            stride = np.cumprod((1,) + counts[:-1])
+            em, sm, ep, sp = [], [], [], []
+            for d in range(self.dim):
+                n = counts[d]
+                lo = e[idx[d] < n - 1]
+                em.append(lo); sm.append(np.full(lo.size, 2 * d + 1))
+                ep.append(lo + stride[d]); sp.append(np.full(lo.size, 2 * d))
+                if self.mesh.periodic[d]:
+                    last = e[idx[d] == n - 1]
+                    em.append(last); sm.append(np.full(last.size, 2 * d + 1))
+                    ep.append(last - (n - 1) * stride[d]); sp.append(np.full(last.size, 2 * d))
+            self._faces = tuple(np.concatenate(a).astype(np.int64) for a in (em, sm, ep, sp))
+        return self._faces
+
     def node_coords(self):
         """Physical GLL node coordinates, (dim, ne, [z,] y, x)."""
         from .basis import gll_nodes
