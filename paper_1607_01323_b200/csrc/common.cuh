@@ -50,10 +50,16 @@ struct Geo {
 // (kernel parameter space -> constant bank operands of DFMA).
 template <int N>
 struct LapTab {
+  static constexpr int H = N / 2, NE = (N + 1) / 2;
   double M[N * N];
   double K[N * N];
   double dL[N];
   double dR[N];
+  // even-odd (centro-symmetric) splits: A v = merge(Ae e, Ao o) with
+  // e_j = v_j + v_{N-1-j}, o_j = v_j - v_{N-1-j} (e_H = v_H for odd N)
+  double Me[NE * NE], Mo[H * H > 0 ? H * H : 1];
+  double Ke[NE * NE], Ko[H * H > 0 ? H * H : 1];
+  double dLe[NE], dLo[H > 0 ? H : 1];
 };
 
 template <int N>

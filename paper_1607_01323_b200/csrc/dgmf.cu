@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "laplace.cuh"
+#include "laplace_warp.cuh"
 #include "tables.h"
 #include "tensor.cuh"
 #include "vecops.cuh"
@@ -295,6 +296,23 @@ static LapTab<N> lap_tab(const Basis1D &b) {
     t.dL[i] = b.ld[i];
     t.dR[i] = b.rd[i];
   }
+  // even-odd splits of the centro-symmetric M, K (A[i][j] = A[N-1-i][N-1-j])
+  // and of the antisymmetric endpoint derivative rows (dR_j = -dL_{N-1-j})
+  constexpr int H = N / 2, NE = (N + 1) / 2;
+  for (int i = 0; i < NE; ++i)
+    for (int j = 0; j < NE; ++j) {
+      const bool mid = (j == H);  // only for odd N
+      t.Me[i * NE + j] = mid ? b.M[i * N + j] : 0.5 * (b.M[i * N + j] + b.M[i * N + N - 1 - j]);
+      t.Ke[i * NE + j] = mid ? b.K[i * N + j] : 0.5 * (b.K[i * N + j] + b.K[i * N + N - 1 - j]);
+    }
+  for (int i = 0; i < H; ++i)
+    for (int j = 0; j < H; ++j) {
+      t.Mo[i * H + j] = 0.5 * (b.M[i * N + j] - b.M[i * N + N - 1 - j]);
+      t.Ko[i * H + j] = 0.5 * (b.K[i * N + j] - b.K[i * N + N - 1 - j]);
+    }
+  for (int j = 0; j < NE; ++j)
+    t.dLe[j] = (j == H) ? b.ld[j] : 0.5 * (b.ld[j] + b.ld[N - 1 - j]);
+  for (int j = 0; j < H; ++j) t.dLo[j] = 0.5 * (b.ld[j] - b.ld[N - 1 - j]);
   return t;
 }
 
@@ -315,12 +333,34 @@ static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_
   return DG_OK;
 }
 
+template <int N, int BX, int BY, int BZ, int NW>
+static int launch_laplace_warp(dg_ctx *c, const double *src, double *dst, double tau_scale,
+                               int part, cudaStream_t st) {
+  using C = WarpLapCfg<N, BX, BY, BZ, NW>;
+  auto kern = laplace_warp_kernel<N, BX, BY, BZ, NW>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  const Geo g = c->geo();
+  const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, (g.nz + BZ - 1) / BZ);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part);
+  DG_LAUNCH_CHECK("laplace_warp_kernel");
+  return DG_OK;
+}
+
 static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                             cudaStream_t st) {
   static const int variant = [] {
     const char *v = getenv("DG_LAP_VARIANT");  // brick-shape experiments
     return v ? atoi(v) : 0;
   }();
+  if (c->dim == 3 && variant == 0) {
+    if (c->n == 3) return launch_laplace_warp<3, 4, 4, 4, 8>(c, src, dst, tau_scale, part, st);
+    if (c->n == 4) return launch_laplace_warp<4, 4, 4, 4, 8>(c, src, dst, tau_scale, part, st);
+    if (c->n == 5) return launch_laplace_warp<5, 4, 4, 2, 8>(c, src, dst, tau_scale, part, st);
+  }
   if (c->dim == 3) {
     if (c->n == 5 && variant == 1) return launch_laplace<3, 5, 2, 2, 2>(c, src, dst, tau_scale, part, st);
     if (c->n == 5 && variant == 2) return launch_laplace<3, 5, 4, 4, 1>(c, src, dst, tau_scale, part, st);

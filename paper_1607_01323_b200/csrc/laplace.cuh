@@ -15,12 +15,19 @@
 // tangential masses, so face terms need no extra sweeps.  7 one-dimensional
 // sweeps per cell in 3D (4 in 2D) plus rank-2 face lifts.
 //
+// Every 1D sweep runs in even-odd form: M and K are centro-symmetric and the
+// endpoint derivative rows anti-symmetric, so each n x n product becomes a
+// ceil(n/2)^2 + floor(n/2)^2 product on the even/odd halves of the line --
+// fewer fp64 operations and a coefficient set small enough to stay in
+// uniform registers.  Face lifts are applied in the same even/odd domain.
+//
 // CTA = brick of BX*BY*BZ cells in shared memory; one thread per line per
 // phase (x-, y-, z-lines).  Neighbour functionals come from the brick or,
 // across the brick surface, from halo cells read once from L2 with their
-// tangential masses applied.  Per-cell side data (neighbour kind/index,
-// 1/h of the neighbour, face penalty) is resolved once per CTA into a small
-// shared table, so the face arithmetic is divide-free.
+// tangential masses applied.  The face coupling of every (cell, side) is
+// reduced once per CTA to six coefficients (own value/derivative,
+// neighbour value/derivative) and one shared-memory offset, so the face
+// arithmetic is branch- and divide-free.
 // No atomics: every output DoF is written once by its own cell
 // (the reference's gather-then-scatter determinism, spaces.py:151-158).
 #pragma once
@@ -105,16 +112,16 @@ struct LapCfg {
   static constexpr int HSIZE = NSLOT * 2 * LPC;  // [slot][v|g][LPC]
   static constexpr int BUF = NC * CS;
   static constexpr int FBUF = NC * 4 * LPC;      // [cell][v0,g0,v1,g1][LPC]
-  static constexpr int CELLT = 8;                // per cell: 1/h_d, s_d
+  static constexpr int SIDEC = 6;                // face coefficients per (cell, side)
   // shared memory carve-up (doubles, then pointers, then ints)
   static constexpr int OFF_BUF1 = BUF;
   static constexpr int OFF_FBUF = 2 * BUF;
   static constexpr int OFF_HRAW = OFF_FBUF + FBUF;
   static constexpr int OFF_HBUF = OFF_HRAW + HSIZE;
-  static constexpr int OFF_SIDE = OFF_HBUF + HSIZE;          // [cell][side] (1/hn, tau)
-  static constexpr int OFF_CELL = OFF_SIDE + 2 * NC * NSIDE;
-  static constexpr int OFF_PTR = OFF_CELL + CELLT * NC;       // halo sources
-  static constexpr int OFF_BAR = OFF_PTR + NSLOT;             // mbarrier (TMA)
+  static constexpr int OFF_SIDE = OFF_HBUF + HSIZE;          // [cell][side][6]
+  static constexpr int OFF_CELL = OFF_SIDE + SIDEC * NC * NSIDE;  // [cell][4]: s_d scaled K
+  static constexpr int OFF_PTR = OFF_CELL + 4 * NC;          // halo sources
+  static constexpr int OFF_BAR = OFF_PTR + NSLOT;            // mbarrier (TMA)
   static constexpr int NDBL = OFF_BAR + 1;
   static constexpr size_t SMEM = sizeof(double) * (size_t)NDBL + sizeof(int) * NC * NSIDE;
 };
@@ -157,36 +164,46 @@ __device__ __forceinline__ int slot_of(int d, int s, int pos) {
                 : (d == 1 ? C::SLOT1 + s * C::NS1 + pos : C::SLOT2 + s * C::NS2 + pos);
 }
 
-// SIP face coefficients (value row cv, derivative row cd) for one line end.
-// vo/go own value / reference derivative at the face, vn/gn neighbour's,
-// hi = 1/h own, hni = 1/h neighbour, tau = scaled face penalty.
-__device__ __forceinline__ void sip_coeffs(int kind, int s, double vo, double go, double vn,
-                                           double gn, double hi, double hni, double tau,
-                                           double &cv, double &cd) {
-  if (kind <= 1) {  // interior face (operators.py:217-225)
-    if (s) {          // own cell is the minus side
-      const double jump = vo - vn;
-      const double avg = go * hi + gn * hni;
-      cv = tau * jump - avg;
-      cd = -jump * hi;
-    } else {          // own cell is the plus side
-      const double jump = vn - vo;
-      const double avg = gn * hni + go * hi;
-      cv = avg - tau * jump;
-      cd = -jump * hi;
-    }
-  } else if (kind == kBndNeumann) {  // pressure-Dirichlet face (operators.py:227-233)
-    if (s) {
-      cv = 2.0 * (tau * vo - hi * go);
-      cd = -2.0 * vo * hi;
-    } else {
-      cv = 2.0 * (hi * go + tau * vo);
-      cd = 2.0 * vo * hi;
-    }
-  } else {
-    cv = 0.0;
-    cd = 0.0;
+// ---- even-odd helpers on register arrays ------------------------------------
+template <int N>
+__device__ __forceinline__ void eo_split(const double *v, double *e, double *o) {
+  constexpr int H = N / 2;
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    e[j] = v[j] + v[N - 1 - j];
+    o[j] = v[j] - v[N - 1 - j];
   }
+  if (N & 1) e[H] = v[H];
+}
+// E = sc * Ae e ; O = sc * Ao o  (accumulate = false) or E += ..., O += ...
+template <int N, bool ACC>
+__device__ __forceinline__ void eo_apply(const double *Ae, const double *Ao, const double *e,
+                                         const double *o, double sc, double *E, double *O) {
+  constexpr int H = N / 2, NE = (N + 1) / 2;
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < NE; ++j) a += Ae[i * NE + j] * e[j];
+    E[i] = ACC ? E[i] + sc * a : sc * a;
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) a += Ao[i * H + j] * o[j];
+    O[i] = ACC ? O[i] + sc * a : sc * a;
+  }
+}
+template <int N>
+__device__ __forceinline__ void eo_merge(const double *E, const double *O, double *y) {
+  constexpr int H = N / 2;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    y[i] = E[i] + O[i];
+    y[N - 1 - i] = E[i] - O[i];
+  }
+  if (N & 1) y[H] = E[H];
 }
 
 // part: 0 all cells, 1 skip bricks touching a ghost side, 2 only those
@@ -196,6 +213,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
                      const LapTab<N> T, const double tau_scale, const int part) {
   using C = LapCfg<DIM, N, BX, BY, BZ>;
   constexpr int RP = C::RP, LPC = C::LPC, CS = C::CS, NP = C::NP, NSIDE = C::NSIDE;
+  constexpr int H = N / 2, NE = (N + 1) / 2;
   extern __shared__ double smem[];
   double *buf0 = smem;
   double *buf1 = smem + C::OFF_BUF1;
@@ -205,7 +223,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   double *sside = smem + C::OFF_SIDE;
   double *scell = smem + C::OFF_CELL;
   const double **hsrc = reinterpret_cast<const double **>(smem + C::OFF_PTR);
-  int *skind = reinterpret_cast<int *>(smem + C::NDBL);
+  int *soff = reinterpret_cast<int *>(smem + C::NDBL);
 
   const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
   const int x0 = bx * BX, y0 = by * BY, z0 = bz * BZ;
@@ -217,12 +235,13 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   }
   const int tid = threadIdx.x;
 
-  // ---- setup: per (cell, side) neighbour table; per cell geometry ---------
+  // ---- setup: per (cell, side) face coefficients + neighbour data offset ---
   for (int it = tid; it < C::NC * NSIDE; it += blockDim.x) {
     const int c = it / NSIDE, side = it % NSIDE;
+    const int d = side >> 1, s = side & 1;
     const int jx = c % BX, jy = (c / BX) % BY, jz = c / (BX * BY);
-    int kind = 2, idx = 0;
-    double hni = 0.0, tau = 0.0;
+    double a_vo = 0.0, a_go = 0.0, a_vn = 0.0, a_gn = 0.0, b_vo = 0.0, b_vn = 0.0;
+    int off = C::OFF_FBUF + (c * 4 + (s ? 2 : 0)) * LPC;  // own data (any valid)
     const double *hsrc_cell = nullptr;
     if (jx < ex && jy < ey && jz < ez) {
       const int ix = x0 + jx, iy = y0 + jy, iz = z0 + jz;
@@ -239,26 +258,37 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
       }
 #undef DG_RES
       const double taue = g.tau[(size_t)ix + (size_t)g.nx * (iy + (size_t)g.ny * iz)];
-      kind = nb.kind;
-      if (kind == 0) idx = nb.cb;
-      if (kind == 1) {
-        const int d = side >> 1, s = side & 1;
-        const int pos = d == 0 ? jy + BY * jz : (d == 1 ? jx + BX * jz : jx + BX * jy);
-        idx = slot_of<C>(d, s, pos);
-        hsrc_cell = nb.src;
+      const double h0 = g.hx[ix], h1 = g.hy[iy], h2 = (DIM == 3) ? g.hz[iz] : 2.0;
+      const double hd = d == 0 ? h0 : (d == 1 ? h1 : h2);
+      double sfac;  // s_d = prod of the other half sizes
+      if (DIM == 3) sfac = d == 0 ? 0.25 * h1 * h2 : (d == 1 ? 0.25 * h0 * h2 : 0.25 * h0 * h1);
+      else sfac = d == 0 ? 0.5 * h1 : 0.5 * h0;
+      const double hi = 1.0 / hd;
+      const double sg = s ? -1.0 : 1.0;  // sign of the own outward normal flips go terms
+      if (nb.kind <= 1) {                // interior face (operators.py:217-225)
+        const double hni = 1.0 / nb.h;
+        const double tau = tau_scale * fmax(taue, nb.tau);
+        a_vo = tau; a_go = sg * hi; a_vn = -tau; a_gn = sg * hni;
+        b_vo = sg * hi; b_vn = -sg * hi;
+        if (nb.kind == 0) {
+          off = C::OFF_FBUF + (nb.cb * 4 + (s ? 0 : 2)) * LPC;
+        } else {
+          const int pos = d == 0 ? jy + BY * jz : (d == 1 ? jx + BX * jz : jx + BX * jy);
+          const int slot = slot_of<C>(d, s, pos);
+          off = (d == 0 ? C::OFF_HRAW : C::OFF_HBUF) + slot * 2 * LPC;
+          hsrc_cell = nb.src;
+        }
+      } else if (nb.kind == kBndNeumann) {  // pressure-Dirichlet face (operators.py:227-233)
+        const double tau = tau_scale * taue;
+        a_vo = 2.0 * tau; a_go = 2.0 * sg * hi;
+        b_vo = 2.0 * sg * hi;
       }
-      if (kind <= 1) {
-        hni = 1.0 / nb.h;
-        tau = tau_scale * fmax(taue, nb.tau);
-      } else {
-        tau = tau_scale * taue;
-      }
+      a_vo *= sfac; a_go *= sfac; a_vn *= sfac; a_gn *= sfac; b_vo *= sfac; b_vn *= sfac;
     }
-    skind[it] = kind | (idx << 4);
-    sside[2 * it] = hni;
-    sside[2 * it + 1] = tau;
+    double *sc = sside + C::SIDEC * it;
+    sc[0] = a_vo; sc[1] = a_go; sc[2] = a_vn; sc[3] = a_gn; sc[4] = b_vo; sc[5] = b_vn;
+    soff[it] = off;
     {  // every halo slot is written exactly once, by its brick-edge cell
-      const int d = side >> 1, s = side & 1;
       const bool edge = d == 0 ? jx == (s ? ex - 1 : 0)
                                : (d == 1 ? jy == (s ? ey - 1 : 0) : jz == (s ? ez - 1 : 0));
       if (edge) {
@@ -275,13 +305,16 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
       h1 = g.hy[y0 + jy];
       if (DIM == 3) h2 = g.hz[z0 + jz];
     }
-    double *ct = scell + C::CELLT * cc;
-    ct[0] = 1.0 / h0;
-    ct[1] = 1.0 / h1;
-    ct[2] = 1.0 / h2;
-    ct[3] = 0.5 * h1 * (DIM == 3 ? 0.5 * h2 : 1.0);
-    ct[4] = 0.5 * h0 * (DIM == 3 ? 0.5 * h2 : 1.0);
-    ct[5] = 0.25 * h0 * h1;
+    double *ct = scell + 4 * cc;  // (2/h_d) s_d: scale of K along d
+    if (DIM == 3) {
+      ct[0] = 0.5 * h1 * h2 / h0;
+      ct[1] = 0.5 * h0 * h2 / h1;
+      ct[2] = 0.5 * h0 * h1 / h2;
+    } else {
+      ct[0] = h1 / h0;
+      ct[1] = h0 / h1;
+      ct[2] = 0.0;
+    }
   }
   // ---- own cells -> buf0: rows of x-adjacent cells are contiguous in both
   // global and (odd N, unpadded) shared memory -> one TMA bulk copy per row
@@ -385,48 +418,46 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   const bool active = has_line && jx < ex && jy < ey && jz < ez;
   const size_t e = (size_t)(x0 + jx) + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz));
   const int ta = (DIM == 3) ? t / N : 0, tb = (DIM == 3) ? t - ta * N : t;
-  double v[N], w[N], g0 = 0.0, g1 = 0.0;
+  double v[N], ev[NE], ov[H > 0 ? H : 1], E[NE], O[H > 0 ? H : 1];
+  double v0 = 0.0, v1 = 0.0, g0 = 0.0, g1 = 0.0;
 
+  // own face functionals of line v (even/odd split ev/ov): values and
+  // reference derivatives at both ends -> fbuf
   auto functionals = [&]() {
-    g0 = 0.0;
-    g1 = 0.0;
+    double ge = 0.0, go = 0.0;
 #pragma unroll
-    for (int q = 0; q < N; ++q) {
-      g0 += T.dL[q] * v[q];
-      g1 += T.dR[q] * v[q];
-    }
-    fbuf[(c * 4 + 0) * LPC + t] = v[0];
+    for (int j = 0; j < NE; ++j) ge += T.dLe[j] * ev[j];
+#pragma unroll
+    for (int j = 0; j < H; ++j) go += T.dLo[j] * ov[j];
+    v0 = v[0];
+    v1 = v[N - 1];
+    g0 = ge + go;
+    g1 = go - ge;
+    fbuf[(c * 4 + 0) * LPC + t] = v0;
     fbuf[(c * 4 + 1) * LPC + t] = g0;
-    fbuf[(c * 4 + 2) * LPC + t] = v[N - 1];
+    fbuf[(c * 4 + 2) * LPC + t] = v1;
     fbuf[(c * 4 + 3) * LPC + t] = g1;
   };
-  // w += sfac * (SIP lifts of direction d) for the own line v (functionals
-  // g0/g1 from the first pass); halo data of x-sides is raw, y/z mass-applied
-  auto add_lifts = [&](auto dconst, double hi, double sfac) {
+  // E/O += even/odd form of the SIP lifts of direction d (coefficients and
+  // neighbour locations from the per-CTA side table)
+  auto add_lifts = [&](auto dconst) {
     constexpr int d = decltype(dconst)::value;
-    const double *hb = (d == 0) ? hraw : hbuf;
+    const int s0 = c * NSIDE + 2 * d, s1 = s0 + 1;
+    const double *c0 = sside + C::SIDEC * s0, *c1 = sside + C::SIDEC * s1;
+    const double vn0 = smem[soff[s0] + t], gn0 = smem[soff[s0] + LPC + t];
+    const double vn1 = smem[soff[s1] + t], gn1 = smem[soff[s1] + LPC + t];
+    const double cv0 = c0[0] * v0 + c0[1] * g0 + c0[2] * vn0 + c0[3] * gn0;
+    const double cd0 = c0[4] * v0 + c0[5] * vn0;
+    const double cv1 = c1[0] * v1 + c1[1] * g1 + c1[2] * vn1 + c1[3] * gn1;
+    const double cd1 = c1[4] * v1 + c1[5] * vn1;
+    // value rows e_0 / e_{N-1}; derivative rows dL, dR = -reverse(dL)
+    E[0] += 0.5 * (cv0 + cv1);
+    if (H > 0) O[0] += 0.5 * (cv0 - cv1);
+    const double dm = cd0 - cd1, dp = cd0 + cd1;
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int st = c * NSIDE + 2 * d + s;
-      const int kv = skind[st];
-      const int kind = kv & 15, idx = kv >> 4;
-      double vn = 0.0, gn = 0.0;
-      if (kind == 0) {
-        vn = fbuf[(idx * 4 + (s ? 0 : 2)) * LPC + t];
-        gn = fbuf[(idx * 4 + (s ? 1 : 3)) * LPC + t];
-      } else if (kind == 1) {
-        vn = hb[(idx * 2 + 0) * LPC + t];
-        gn = hb[(idx * 2 + 1) * LPC + t];
-      }
-      double cv, cd;
-      sip_coeffs(kind, s, s ? v[N - 1] : v[0], s ? g1 : g0, vn, gn, hi, sside[2 * st],
-                 sside[2 * st + 1], cv, cd);
-      cv *= sfac;
-      cd *= sfac;
-      w[s ? N - 1 : 0] += cv;
+    for (int i = 0; i < NE; ++i) E[i] += T.dLe[i] * dm;
 #pragma unroll
-      for (int q = 0; q < N; ++q) w[q] += cd * (s ? T.dR[q] : T.dL[q]);
-    }
+    for (int i = 0; i < H; ++i) O[i] += T.dLo[i] * dp;
   };
 
   // ---- phase X: x-lines of u --------------------------------------------------
@@ -434,6 +465,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   if (has_line) {
 #pragma unroll
     for (int q = 0; q < N; ++q) v[q] = buf0[xbase + q];
+    eo_split<N>(v, ev, ov);
     functionals();
   }
   __syncthreads();  // #2
@@ -456,23 +488,16 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
     }
   }
   if (active) {
-    const double *ct = scell + C::CELLT * c;
-    const double ihx = ct[0], sx = ct[3];
-    const double kx = 2.0 * sx * ihx;
+    double y[N];
+    eo_apply<N, false>(T.Me, T.Mo, ev, ov, 1.0, E, O);
+    eo_merge<N>(E, O, y);
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double a = 0.0, b = 0.0;
+    for (int i = 0; i < N; ++i) buf0[xbase + i] = y[i];  // P = M_x u (own line only)
+    eo_apply<N, false>(T.Ke, T.Ko, ev, ov, scell[4 * c + 0], E, O);
+    add_lifts(std::integral_constant<int, 0>());
+    eo_merge<N>(E, O, y);
 #pragma unroll
-      for (int q = 0; q < N; ++q) {
-        a += T.K[i * N + q] * v[q];
-        b += T.M[i * N + q] * v[q];
-      }
-      w[i] = kx * a;
-      buf0[xbase + i] = b;  // P = M_x u (own line only)
-    }
-    add_lifts(std::integral_constant<int, 0>(), ihx, sx);
-#pragma unroll
-    for (int i = 0; i < N; ++i) buf1[xbase + i] = w[i];
+    for (int i = 0; i < N; ++i) buf1[xbase + i] = y[i];
   }
   __syncthreads();  // #3
   // halo step B (3D): z-sides Q = M_y (M_x raw), columns along y, in place
@@ -497,39 +522,31 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   if (has_line) {
 #pragma unroll
     for (int q = 0; q < N; ++q) v[q] = buf0[ybase + q * RP];
+    eo_split<N>(v, ev, ov);
     functionals();
   }
   __syncthreads();  // #4
   if (active) {
-    const double *ct = scell + C::CELLT * c;
-    const double ihy = ct[1], sy = ct[4];
-    const double ky = 2.0 * sy * ihy;
-    double tl[N];
+    double y[N], te[NE], to[H > 0 ? H : 1];
 #pragma unroll
-    for (int q = 0; q < N; ++q) tl[q] = buf1[ybase + q * RP];
+    for (int q = 0; q < N; ++q) y[q] = buf1[ybase + q * RP];
+    eo_split<N>(y, te, to);
+    if (DIM == 3) {  // Q = M_y P (own line; P was read before barrier #4)
+      eo_apply<N, false>(T.Me, T.Mo, ev, ov, 1.0, E, O);
+      eo_merge<N>(E, O, y);
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double a = 0.0, b = 0.0;
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        a += T.K[i * N + q] * v[q];
-        b += T.M[i * N + q] * tl[q];
-      }
-      w[i] = b + ky * a;
+      for (int i = 0; i < N; ++i) buf0[ybase + i * RP] = y[i];
     }
-    add_lifts(std::integral_constant<int, 1>(), ihy, sy);
+    eo_apply<N, false>(T.Me, T.Mo, te, to, 1.0, E, O);           // M_y T
+    eo_apply<N, true>(T.Ke, T.Ko, ev, ov, scell[4 * c + 1], E, O);  // + s_y Kh_y P
+    add_lifts(std::integral_constant<int, 1>());
+    eo_merge<N>(E, O, y);
     if (DIM == 2) {
 #pragma unroll
-      for (int i = 0; i < N; ++i) out[e * NP + i * N + tb] = w[i];
+      for (int i = 0; i < N; ++i) out[e * NP + i * N + tb] = y[i];
     } else {
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double b = 0.0;
-#pragma unroll
-        for (int q = 0; q < N; ++q) b += T.M[i * N + q] * v[q];
-        buf0[ybase + i * RP] = b;     // Q = M_y P
-        buf1[ybase + i * RP] = w[i];  // G
-      }
+      for (int i = 0; i < N; ++i) buf1[ybase + i * RP] = y[i];  // G
     }
   }
   if (DIM == 2) return;
@@ -539,29 +556,21 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   if (has_line) {
 #pragma unroll
     for (int q = 0; q < N; ++q) v[q] = buf0[zbase + q * N * RP];
+    eo_split<N>(v, ev, ov);
     functionals();
   }
   __syncthreads();  // #6
   if (active) {
-    const double *ct = scell + C::CELLT * c;
-    const double ihz = ct[2], sz = ct[5];
-    const double kz = 2.0 * sz * ihz;
-    double gl[N];
+    double y[N], ge[NE], go[H > 0 ? H : 1];
 #pragma unroll
-    for (int q = 0; q < N; ++q) gl[q] = buf1[zbase + q * N * RP];
+    for (int q = 0; q < N; ++q) y[q] = buf1[zbase + q * N * RP];
+    eo_split<N>(y, ge, go);
+    eo_apply<N, false>(T.Me, T.Mo, ge, go, 1.0, E, O);           // M_z G
+    eo_apply<N, true>(T.Ke, T.Ko, ev, ov, scell[4 * c + 2], E, O);  // + s_z Kh_z Q
+    add_lifts(std::integral_constant<int, 2>());
+    eo_merge<N>(E, O, y);
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double a = 0.0, b = 0.0;
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        a += T.K[i * N + q] * v[q];
-        b += T.M[i * N + q] * gl[q];
-      }
-      w[i] = b + kz * a;
-    }
-    add_lifts(std::integral_constant<int, 2>(), ihz, sz);
-#pragma unroll
-    for (int i = 0; i < N; ++i) out[e * NP + (i * N + ta) * N + tb] = w[i];
+    for (int i = 0; i < N; ++i) out[e * NP + (i * N + ta) * N + tb] = y[i];
   }
 }
 
