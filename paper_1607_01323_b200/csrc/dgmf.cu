@@ -356,7 +356,7 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
     const char *v = getenv("DG_LAP_VARIANT");  // brick-shape experiments
     return v ? atoi(v) : 0;
   }();
-  if (c->dim == 3 && variant == 0) {
+  if (c->dim == 3 && variant == 20) {  // barrier-free warp-per-cell kernel
     if (c->n == 3) return launch_laplace_warp<3, 4, 4, 4, 8>(c, src, dst, tau_scale, part, st);
     if (c->n == 4) return launch_laplace_warp<4, 4, 4, 4, 8>(c, src, dst, tau_scale, part, st);
     if (c->n == 5) return launch_laplace_warp<5, 4, 4, 2, 8>(c, src, dst, tau_scale, part, st);
