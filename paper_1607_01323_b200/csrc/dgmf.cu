@@ -8,9 +8,11 @@
 
 #include "common.cuh"
 #include "laplace.cuh"
+#include "laplace_persist.cuh"
 #include "laplace_warp.cuh"
 #include "tables.h"
 #include "tensor.cuh"
+#include "tensor_fast.cuh"
 #include "vecops.cuh"
 #include "vector.cuh"
 
@@ -333,6 +335,28 @@ static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_
   return DG_OK;
 }
 
+template <int N, int BX, int BY, int BZ>
+static int launch_laplace_persist(dg_ctx *c, const double *src, double *dst, double tau_scale,
+                                  cudaStream_t st) {
+  using C = PersistCfg<N, BX, BY, BZ>;
+  using L = LapCfg<3, N, BX, BY, BZ>;
+  auto kern = laplace_persist_kernel<N, BX, BY, BZ>;
+  static int nsm = 0;
+  if (!nsm) {
+    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    int dev = 0;
+    DG_CUDA_CHECK(cudaGetDevice(&dev));
+    DG_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const Geo g = c->geo();
+  const int nbx = (g.nx + BX - 1) / BX, nby = (g.ny + BY - 1) / BY, nbz = (g.nz + BZ - 1) / BZ;
+  const int nb = nbx * nby * nbz;
+  const int grid = nb < 2 * nsm ? nb : 2 * nsm;
+  kern<<<grid, L::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, nbx, nby, nb);
+  DG_LAUNCH_CHECK("laplace_persist_kernel");
+  return DG_OK;
+}
+
 template <int N, int BX, int BY, int BZ, int NW>
 static int launch_laplace_warp(dg_ctx *c, const double *src, double *dst, double tau_scale,
                                int part, cudaStream_t st) {
@@ -356,6 +380,10 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
     const char *v = getenv("DG_LAP_VARIANT");  // brick-shape experiments
     return v ? atoi(v) : 0;
   }();
+  if (c->dim == 3 && part == 0 && variant == 30) {  // persistent pipelined
+    if (c->n == 5) return launch_laplace_persist<5, 4, 2, 2>(c, src, dst, tau_scale, st);
+    if (c->n == 3) return launch_laplace_persist<3, 4, 4, 4>(c, src, dst, tau_scale, st);
+  }
   if (c->dim == 3 && variant == 20) {  // barrier-free warp-per-cell kernel
     if (c->n == 3) return launch_laplace_warp<3, 4, 4, 4, 8>(c, src, dst, tau_scale, part, st);
     if (c->n == 4) return launch_laplace_warp<4, 4, 4, 4, 8>(c, src, dst, tau_scale, part, st);
@@ -550,6 +578,22 @@ static int launch_tensor(dg_ctx *c, const double *src, double *dst, int ncomp, b
   for (int i = 0; i < N * N; ++i) t.A[i] = A[i];
   using TC = TensorCfg<DIM, N>;
   const int64_t cells = c->n_cells * ncomp;
+  if constexpr (DIM == 3 && (N & 1)) {
+    // runs of contiguous cells: TMA in, even-odd sweeps, TMA out
+    constexpr int CPB = N <= 3 ? 32 : (N <= 5 ? 16 : 8);
+    EOTab<N> eo;
+    constexpr int H = N / 2, NE = (N + 1) / 2;
+    for (int i = 0; i < NE; ++i)
+      for (int j = 0; j < NE; ++j)
+        eo.Ae[i * NE + j] = (j == H) ? A[i * N + j] : 0.5 * (A[i * N + j] + A[i * N + N - 1 - j]);
+    for (int i = 0; i < H; ++i)
+      for (int j = 0; j < H; ++j) eo.Ao[i * H + j] = 0.5 * (A[i * N + j] - A[i * N + N - 1 - j]);
+    const int nb = (int)((cells + CPB - 1) / CPB);
+    tensor_fast_kernel<N, CPB><<<nb, ((CPB * N * N + 31) / 32) * 32, 0, st>>>(
+        src, dst, c->geo(), eo, cells, inverse ? 1 : 0);
+    DG_LAUNCH_CHECK("tensor_fast_kernel");
+    return DG_OK;
+  }
   const int nb = (int)((cells + TC::NC - 1) / TC::NC);
   tensor_apply_kernel<DIM, N><<<nb, TC::THREADS, TC::SMEM, st>>>(src, dst, c->geo(), t, cells,
                                                                   inverse ? 1 : 0);
