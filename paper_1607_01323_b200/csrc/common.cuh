@@ -43,6 +43,7 @@ struct Geo {
   const double *ghost[2];    // x-ghost layers (ny*nz cells each) or null
   const double *ghost_tau[2];
   double ghost_h[2];
+  int exp_flags;             // timing experiments (DG_EXP env); 0 in production
 };
 
 // 1D reference matrices on [-1,1] for n = k+1 GLL nodes, Gauss rule n_q = n:

@@ -59,6 +59,8 @@ struct dg_ctx {
   double *d_scal = nullptr;    // 16 device scalars
   double *h_scal = nullptr;    // pinned mirror
   std::vector<double *> work;  // solver work vectors (n_dofs each)
+  double *d_partials = nullptr;  // per-brick partial sums of the fused vmult epilogue
+  int64_t partials_n = 0;
   std::mutex mu;
 
   Geo geo() const {
@@ -76,6 +78,11 @@ struct dg_ctx {
       g.ghost_tau[s] = d_ghost_tau[s];
       g.ghost_h[s] = ghost_h[s];
     }
+    static const int exp_flags = [] {
+      const char *v = getenv("DG_EXP");
+      return v ? atoi(v) : 0;
+    }();
+    g.exp_flags = exp_flags;
     return g;
   }
 };
@@ -265,6 +272,7 @@ int dg_ctx_destroy(dg_ctx *c) {
   cudaFree(c->d_scal);
   if (c->h_scal) cudaFreeHost(c->h_scal);
   for (double *w : c->work) cudaFree(w);
+  cudaFree(c->d_partials);
   delete c;
   return DG_OK;
 }
@@ -318,11 +326,11 @@ static LapTab<N> lap_tab(const Basis1D &b) {
   return t;
 }
 
-template <int DIM, int N, int BX, int BY, int BZ>
+template <int DIM, int N, int BX, int BY, int BZ, int EPI = kEpiStore>
 static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
-                          cudaStream_t st) {
+                          cudaStream_t st, const EpiArgs &ea = EpiArgs{}) {
   using C = LapCfg<DIM, N, BX, BY, BZ>;
-  auto kern = laplace_vmult_kernel<DIM, N, BX, BY, BZ>;
+  auto kern = laplace_vmult_kernel<DIM, N, BX, BY, BZ, EPI>;
   static bool attr = false;
   if (!attr) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -330,9 +338,39 @@ static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_
   }
   const Geo g = c->geo();
   const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, (g.nz + BZ - 1) / BZ);
-  kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part, ea);
   DG_LAUNCH_CHECK("laplace_vmult_kernel");
   return DG_OK;
+}
+
+// number of CTAs (bricks) of the default Laplace configuration: the size of
+// the kEpiDot partial-sum array
+static int64_t laplace_bricks(const dg_ctx *c) {
+  int bx = 0, by = 0, bz = 1;
+  if (c->dim == 3) {
+    static const int B[9][3] = {{0, 0, 0}, {0, 0, 0}, {8, 4, 4}, {4, 4, 4}, {4, 4, 2},
+                                {4, 2, 2}, {2, 2, 2}, {2, 2, 2}, {2, 2, 2}};
+    bx = B[c->n][0]; by = B[c->n][1]; bz = B[c->n][2];
+  } else {
+    static const int B[9][2] = {{0, 0}, {0, 0}, {16, 16}, {16, 8}, {16, 8}, {8, 8}, {8, 8}, {8, 8}, {8, 8}};
+    bx = B[c->n][0]; by = B[c->n][1];
+  }
+  return (int64_t)((c->counts[0] + bx - 1) / bx) * ((c->counts[1] + by - 1) / by) *
+         ((c->counts[2] + bz - 1) / bz);
+}
+
+// fused-epilogue vmults for the CG / Chebyshev loop (default bricks, k = 2..5)
+static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, double tau_scale,
+                                int epi, const EpiArgs &ea, cudaStream_t st) {
+#define DG_E(D, NN, X, Y, Z)                                                                     \
+  if (c->dim == D && c->n == NN) {                                                               \
+    if (epi == kEpiCheb) return launch_laplace<D, NN, X, Y, Z, kEpiCheb>(c, src, dst, tau_scale, 0, st, ea); \
+    if (epi == kEpiDot) return launch_laplace<D, NN, X, Y, Z, kEpiDot>(c, src, dst, tau_scale, 0, st, ea);   \
+  }
+  DG_E(3, 3, 4, 4, 4) DG_E(3, 4, 4, 4, 2) DG_E(3, 5, 4, 2, 2) DG_E(3, 6, 2, 2, 2)
+  DG_E(2, 3, 16, 8, 1) DG_E(2, 4, 16, 8, 1) DG_E(2, 5, 8, 8, 1) DG_E(2, 6, 8, 8, 1)
+#undef DG_E
+  return DG_ENOTSUP;
 }
 
 template <int N, int BX, int BY, int BZ>

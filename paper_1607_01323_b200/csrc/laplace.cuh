@@ -206,11 +206,73 @@ __device__ __forceinline__ void eo_merge(const double *E, const double *O, doubl
   if (N & 1) y[H] = E[H];
 }
 
+// Epilogues fused into the vmult's output loop (CG / Chebyshev vector phases,
+// reference solvers.py:56-71 and :121-128):
+//   kEpiStore  out = L u
+//   kEpiCheb   rc -= L u ; dnew = a*u + b*(rc/diag) ; x += dnew   (one
+//              Chebyshev step; u is the current direction d, out unused)
+//   kEpiDot    out = L u and per-CTA partial sums of u.Lu, sum(Lu), u.w
+//              (w = integrals of the basis functions, the dual zero-mean
+//              weights) for pAp of the projected operator
+enum LapEpi : int { kEpiStore = 0, kEpiCheb = 1, kEpiDot = 2 };
+struct EpiArgs {
+  double *rc;
+  const double *diag;
+  double *x;
+  double *dnew;
+  double a, b;
+  double *partials;      // [brick][4]
+  double wint[kMaxN];    // integrals of the 1D basis functions on [-1,1]
+};
+
+template <int EPI, int DIM, int N>
+__device__ __forceinline__ void epi_store(const double *__restrict__ u, double *__restrict__ out,
+                                          const EpiArgs &ea, size_t gi, double y, double wq,
+                                          double *acc) {
+  if (EPI == kEpiStore) {
+    out[gi] = y;
+  } else if (EPI == kEpiCheb) {
+    const double r = __dsub_rn(ea.rc[gi], y);
+    const double dn = __dadd_rn(__dmul_rn(ea.a, u[gi]), __dmul_rn(ea.b, __ddiv_rn(r, ea.diag[gi])));
+    ea.rc[gi] = r;
+    ea.dnew[gi] = dn;
+    ea.x[gi] = __dadd_rn(ea.x[gi], dn);
+  } else {
+    out[gi] = y;
+    const double p = u[gi];
+    acc[0] += p * y;
+    acc[1] += y;
+    acc[2] += p * wq;
+  }
+}
+
+// deterministic CTA reduction of acc[0..2] -> ea.partials[blk*4 + k]
+__device__ __forceinline__ void epi_reduce(double *acc, double *red, const EpiArgs &ea, int blk) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    acc[k] = v;
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();  // red may alias data of the last phase
+  if (lane == 0)
+    for (int k = 0; k < 3; ++k) red[k * 32 + w] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double s = 0.0;
+    for (int i = 0; i < nw; ++i) s += red[threadIdx.x * 32 + i];
+    ea.partials[(size_t)blk * 4 + threadIdx.x] = s;
+  }
+}
+
 // part: 0 all cells, 1 skip bricks touching a ghost side, 2 only those
-template <int DIM, int N, int BX, int BY, int BZ>
+template <int DIM, int N, int BX, int BY, int BZ, int EPI = kEpiStore>
 __global__ void __launch_bounds__(LapCfg<DIM, N, BX, BY, BZ>::THREADS, (N >= 7 ? 1 : 2))
 laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g,
-                     const LapTab<N> T, const double tau_scale, const int part) {
+                     const LapTab<N> T, const double tau_scale, const int part,
+                     const EpiArgs ea = EpiArgs{}) {
   using C = LapCfg<DIM, N, BX, BY, BZ>;
   constexpr int RP = C::RP, LPC = C::LPC, CS = C::CS, NP = C::NP, NSIDE = C::NSIDE;
   constexpr int H = N / 2, NE = (N + 1) / 2;
@@ -359,7 +421,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   // ---- halo: raw face functionals of neighbour cells outside the brick ----
   // flat (slot, face point) items spread over all threads; every thread
   // issues all of its L2 loads before consuming any (memory-level parallelism)
-  {
+  if (!(g.exp_flags & 1)) {  // exp_flags bit 0: skip halo (timing experiments only)
     constexpr int NIT = C::NSLOT * LPC;
     constexpr int ROUNDS = (NIT + C::THREADS - 1) / C::THREADS;
     double x[ROUNDS][N];
@@ -420,6 +482,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   const int ta = (DIM == 3) ? t / N : 0, tb = (DIM == 3) ? t - ta * N : t;
   double v[N], ev[NE], ov[H > 0 ? H : 1], E[NE], O[H > 0 ? H : 1];
   double v0 = 0.0, v1 = 0.0, g0 = 0.0, g1 = 0.0;
+  double eacc[3] = {0.0, 0.0, 0.0};  // kEpiDot partial sums
 
   // own face functionals of line v (even/odd split ev/ov): values and
   // reference derivatives at both ends -> fbuf
@@ -442,6 +505,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   // neighbour locations from the per-CTA side table)
   auto add_lifts = [&](auto dconst) {
     constexpr int d = decltype(dconst)::value;
+    if (g.exp_flags & 2) return;  // timing experiment: no face terms
     const int s0 = c * NSIDE + 2 * d, s1 = s0 + 1;
     const double *c0 = sside + C::SIDEC * s0, *c1 = sside + C::SIDEC * s1;
     const double vn0 = smem[soff[s0] + t], gn0 = smem[soff[s0] + LPC + t];
@@ -470,7 +534,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   }
   __syncthreads();  // #2
   // halo step A: y-sides P = M_x raw (rows along x); z-sides first M_x
-  {
+  if (!(g.exp_flags & 4)) {
     constexpr int ROWS = LPC / N;  // rows per (slot, which)
     for (int i = tid; i < (C::NSLOT - C::SLOT1) * 2 * ROWS; i += blockDim.x) {
       const int sw = i / ROWS, a = i - sw * ROWS;  // sw = (slot - SLOT1)*2 + which
@@ -501,7 +565,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   }
   __syncthreads();  // #3
   // halo step B (3D): z-sides Q = M_y (M_x raw), columns along y, in place
-  if (DIM == 3) {
+  if (DIM == 3 && !(g.exp_flags & 4)) {
     for (int i = tid; i < 2 * C::NS2 * 2 * N; i += blockDim.x) {
       const int sw = i / N, xcol = i - sw * N;  // sw = (slot - SLOT2)*2 + which
       double *col = hbuf + (C::SLOT2 * 2 + sw) * LPC + xcol;
@@ -542,14 +606,19 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
     add_lifts(std::integral_constant<int, 1>());
     eo_merge<N>(E, O, y);
     if (DIM == 2) {
+      const double wx = EPI == kEpiDot ? 0.25 * g.hx[x0 + jx] * g.hy[y0 + jy] * ea.wint[tb] : 0.0;
 #pragma unroll
-      for (int i = 0; i < N; ++i) out[e * NP + i * N + tb] = y[i];
+      for (int i = 0; i < N; ++i)
+        epi_store<EPI, DIM, N>(u, out, ea, e * NP + i * N + tb, y[i], wx * ea.wint[i], eacc);
     } else {
 #pragma unroll
       for (int i = 0; i < N; ++i) buf1[ybase + i * RP] = y[i];  // G
     }
   }
-  if (DIM == 2) return;
+  if (DIM == 2) {
+    if (EPI == kEpiDot) epi_reduce(eacc, fbuf, ea, bx + gridDim.x * (by + gridDim.y * bz));
+    return;
+  }
   __syncthreads();  // #5
   // ---- phase Z: z-lines of Q and G --------------------------------------------
   const int zbase = c * CS + ta * RP + tb;  // (y, x) line along z, stride N*RP
@@ -569,9 +638,15 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
     eo_apply<N, true>(T.Ke, T.Ko, ev, ov, scell[4 * c + 2], E, O);  // + s_z Kh_z Q
     add_lifts(std::integral_constant<int, 2>());
     eo_merge<N>(E, O, y);
+    const double wxy = EPI == kEpiDot ? 0.125 * g.hx[x0 + jx] * g.hy[y0 + jy] * g.hz[z0 + jz] *
+                                            ea.wint[tb] * ea.wint[ta]
+                                      : 0.0;
 #pragma unroll
-    for (int i = 0; i < N; ++i) out[e * NP + (i * N + ta) * N + tb] = y[i];
+    for (int i = 0; i < N; ++i)
+      epi_store<EPI, DIM, N>(u, out, ea, e * NP + (i * N + ta) * N + tb, y[i], wxy * ea.wint[i],
+                             eacc);
   }
+  if (EPI == kEpiDot) epi_reduce(eacc, fbuf, ea, bx + gridDim.x * (by + gridDim.y * bz));
 }
 
 }  // namespace dg

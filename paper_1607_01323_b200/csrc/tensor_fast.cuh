@@ -64,10 +64,14 @@ tensor_fast_kernel(const double *__restrict__ u, double *__restrict__ out, const
 #pragma unroll
     for (int q = 0; q < N; ++q) buf[base + q * stride] = v[q];
   };
-  if (act) sweep(c * NP + (a * N + b) * N, 1, 1.0);  // x-lines (z=a, y=b)
-  __syncthreads();
-  if (act) sweep(c * NP + a * N * N + b, N, 1.0);    // y-lines (z=a, x=b)
-  __syncthreads();
+  // timing experiment (DG_EXP bit 3): 7 sweeps like the Laplace kernel
+  const int reps = (g.exp_flags & 8) ? 3 : 1;
+  for (int rep = 0; rep < reps; ++rep) {
+    if (act) sweep(c * NP + (a * N + b) * N, 1, 1.0);  // x-lines (z=a, y=b)
+    __syncthreads();
+    if (act) sweep(c * NP + a * N * N + b, N, 1.0);    // y-lines (z=a, x=b)
+    __syncthreads();
+  }
   if (act) {                                          // z-lines (y=a, x=b) + scale
     const int64_t cell = (c0 + c) % ((int64_t)g.nx * g.ny * g.nz);
     const int ix = (int)(cell % g.nx), iy = (int)((cell / g.nx) % g.ny);
