@@ -102,10 +102,69 @@ int dg_projection_vmult(dg_ctx *ctx, const double *src, double *dst,
                         const double *tau_d, const double *tau_c,
                         void *stream);
 /* eval_convective_rhs(space, bcs, history, betas, ...)  operators.py:533-594
- * with homogeneous Dirichlet data and no body force (the hot-path case);
+ * with homogeneous Dirichlet data and no body force (the C3 hot-path case;
+ * dg_convective_rhs_ex below takes the data);
  * hist[j] -> dim-component velocity at history level j. dst overwritten. */
 int dg_convective_rhs(dg_ctx *ctx, int n_hist, const double *const *hist,
                       const double *betas, double *dst, void *stream);
+/* The full eval_convective_rhs: g_data[j*6 + side] = Dirichlet data g of
+ * history level j at time times[j] on the over-integration face points
+ * (layout of the boundary data below, dim components; NULL entries or a NULL
+ * array = zero data); body = body force f(x, t_np1) at the over-integration
+ * volume points, [comp][cell][n_q_over^dim] (NULL = none). */
+int dg_convective_rhs_ex(dg_ctx *ctx, int n_hist, const double *const *hist,
+                         const double *betas, const double *const *g_data,
+                         const double *body, double *dst, void *stream);
+
+/* ---- once-per-step right-hand sides (operators.py:241-366, 494-527,
+ * 610-672) and the element-local PCG (solvers.py:201-256) --------------
+ *
+ * Boundary data: bnd[side] (side = 2*d + s: xmin, xmax, ymin, ymax, zmin,
+ * zmax) is NULL (zero data) or a device array [ntan][ncomp][n_f] over the
+ * boundary cells of that side, ntan = product of the two (one in 2D) other
+ * cell counts with the tangential cell index (slow, fast) in decreasing axis
+ * order (d=0: iz*ny+iy, d=1: iz*nx+ix, d=2: iy*nx+ix; 2D: iy or ix), and the
+ * n_f = n^(dim-1) face Gauss points [slow][fast] in the same axis order.  The
+ * caller evaluates the reference's boundary callables at those points. */
+
+/* eval_divergence_rhs(space, u, bcs, scale, form)  operators.py:265-316;
+ * form 0 standard, 1 weak (central flux, interior trace on boundaries),
+ * 2 strong.  src: dim components; dst: scalar. */
+int dg_divergence_rhs(dg_ctx *ctx, const double *src, double *dst, double scale,
+                      int form, void *stream);
+/* eval_pressure_gradient_rhs(space, p, bcs, scale, form)  operators.py:322-366;
+ * form 0 standard, 1 weak.  src: scalar; dst: dim components. */
+int dg_pressure_gradient_rhs(dg_ctx *ctx, const double *src, double *dst,
+                             double scale, int form, void *stream);
+/* compute_vorticity(space, u)  operators.py:610-618: element-local L2
+ * projection of curl u; dst: 1 component in 2D, 3 in 3D (no aliasing). */
+int dg_vorticity(dg_ctx *ctx, const double *src, double *dst, void *stream);
+/* eval_pressure_neumann_rhs(space, bcs, history, vorticity_history, betas, nu,
+ * t, body_force)  operators.py:621-672 on velocity-Dirichlet sides.
+ * hist[j]: dim-component velocity, vort[j]: its vorticity (1 or 3 comps);
+ * bnd[side]: dim components of dg/dt - f at the face points (or NULL). */
+int dg_pressure_neumann_rhs(dg_ctx *ctx, int n_hist, const double *const *hist,
+                            const double *const *vort, const double *betas,
+                            double nu, const double *const *bnd, double *dst,
+                            void *stream);
+/* gp_dirichlet_rhs(space, bcs, t, tau_scale)  operators.py:241-259 on
+ * velocity-Neumann sides; bnd[side]: 1 component (g_p). dst: scalar. */
+int dg_gp_dirichlet_rhs(dg_ctx *ctx, const double *const *bnd, double tau_scale,
+                        double *dst, void *stream);
+/* viscous_rhs_bc(space, bcs, t, nu)  operators.py:494-527.  bnd[side]:
+ * velocity-Dirichlet sides dim components (g); velocity-Neumann sides dim+1
+ * components (h, g_p).  dst: dim components. */
+int dg_viscous_rhs_bc(dg_ctx *ctx, const double *const *bnd, double nu,
+                      double *dst, void *stream);
+/* element_local_pcg(op_local, prec_local, b, rel_tol, max_iter, floor_factor)
+ * solvers.py:201-256 with op_local = apply_projection_operator(space, ., tau_d,
+ * None) and prec_local = inverse_mass_apply (the V3 projection).  b, x: dim
+ * components (no aliasing); tau_d: per cell (device, NULL = 0); iters /
+ * converged: per-cell int32 device arrays (may be NULL). */
+int dg_element_local_pcg(dg_ctx *ctx, const double *b, double *x,
+                         const double *tau_d, double rel_tol, int max_iter,
+                         double floor_factor, int *iters, int *converged,
+                         void *stream);
 
 /* ---- vector kernels for the solvers (solvers.py) ------------------------ */
 /* deterministic fixed-order dot product; result written to device *out */

@@ -240,6 +240,86 @@ class DenseOracle:
                 A[np.ix_(dofs, dofs)] += blk
         return A
 
+    def _boundary_faces(self, bcs):
+        for groups in (bcs.dirichlet, bcs.neumann):
+            for eb, sb, _ in groups:
+                yield from zip(eb, sb)
+
+    def divergence_form_matrix(self, bcs, scale, form):
+        """a(q, u), rows pressure / columns velocity (oracle.py:244-295);
+        'standard' or 'weak' (central flux, interior trace on boundaries)."""
+        sp, g, dim = self.space, self.space.geom, self.dim
+        A = np.zeros((self.n_scalar, dim * self.n_scalar))
+        t = self.tables
+        for e in range(self.ne):
+            val, ph, w = self._vol_phys(e, g, t)
+            if form == "standard":
+                blk = np.concatenate([-scale * val.T @ (w[:, None] * ph[a])
+                                      for a in range(dim)], axis=1)
+            else:
+                blk = np.concatenate([scale * ph[a].T @ (w[:, None] * val)
+                                      for a in range(dim)], axis=1)
+            A[np.ix_(self._sd(e), self._vd(e))] += blk
+        if form == "standard":
+            return A
+        f = sp.mesh.interior
+        for i in range(f.n):
+            em, sm, ep, spp = f.em[i], f.sm[i], f.ep[i], f.sp[i]
+            Tm, _ = self._face_phys(em, sm, g, t)
+            Tp, _ = self._face_phys(ep, spp, g, t)
+            n = self._normal(g, sm, em)
+            w = self._sj(g, sm, em)
+            # {u}.n^- over columns [u_a^- ..., u_a^+ ...]
+            Un = np.concatenate([0.5 * Tm * n[a] for a in range(dim)]
+                                + [0.5 * Tp * n[a] for a in range(dim)], axis=1)
+            cols = np.concatenate([self._vd(em), self._vd(ep)])
+            A[np.ix_(self._sd(em), cols)] += -scale * Tm.T @ (w[:, None] * Un)
+            A[np.ix_(self._sd(ep), cols)] += scale * Tp.T @ (w[:, None] * Un)
+        for e, s in self._boundary_faces(bcs):
+            T, _ = self._face_phys(e, s, g, t)
+            n = self._normal(g, s, e)
+            w = self._sj(g, s, e)
+            Un = np.concatenate([T * n[a] for a in range(dim)], axis=1)
+            A[np.ix_(self._sd(e), self._vd(e))] += -scale * T.T @ (w[:, None] * Un)
+        return A
+
+    def pressure_gradient_matrix(self, bcs, scale, form):
+        """b(v, p), rows velocity / columns pressure (oracle.py:297-348)."""
+        sp, g, dim = self.space, self.space.geom, self.dim
+        A = np.zeros((dim * self.n_scalar, self.n_scalar))
+        t = self.tables
+        for e in range(self.ne):
+            val, ph, w = self._vol_phys(e, g, t)
+            if form == "standard":
+                blk = np.concatenate([-scale * val.T @ (w[:, None] * ph[a])
+                                      for a in range(dim)], axis=0)
+            else:
+                blk = np.concatenate([scale * ph[a].T @ (w[:, None] * val)
+                                      for a in range(dim)], axis=0)
+            A[np.ix_(self._vd(e), self._sd(e))] += blk
+        if form == "standard":
+            return A
+        f = sp.mesh.interior
+        for i in range(f.n):
+            em, sm, ep, spp = f.em[i], f.sm[i], f.ep[i], f.sp[i]
+            Tm, _ = self._face_phys(em, sm, g, t)
+            Tp, _ = self._face_phys(ep, spp, g, t)
+            n = self._normal(g, sm, em)
+            w = self._sj(g, sm, em)
+            cols = np.concatenate([self._sd(em), self._sd(ep)])
+            avg = 0.5 * np.concatenate([Tm, Tp], axis=1)
+            A[np.ix_(self._vd(em), cols)] += np.concatenate(
+                [-scale * (Tm * n[a]).T @ (w[:, None] * avg) for a in range(dim)], axis=0)
+            A[np.ix_(self._vd(ep), cols)] += np.concatenate(
+                [scale * (Tp * n[a]).T @ (w[:, None] * avg) for a in range(dim)], axis=0)
+        for e, s in self._boundary_faces(bcs):
+            T, _ = self._face_phys(e, s, g, t)
+            n = self._normal(g, s, e)
+            w = self._sj(g, s, e)
+            A[np.ix_(self._vd(e), self._sd(e))] += np.concatenate(
+                [-scale * (T * n[a]).T @ (w[:, None] * T) for a in range(dim)], axis=0)
+        return A
+
     def convective_residual(self, bcs, history_flat, betas, times, t_np1,
                             body_force=None):
         """oracle.py:350-426."""

@@ -929,6 +929,194 @@ def compute_penalty_parameters(space, u, dt, cfl, zeta_d_star=1.0,
 
 
 # ---------------------------------------------------------------------------
+# once-per-step right-hand sides (reference operators.py:241-366, 494-527,
+# 610-672), DIM-generic
+
+def _bshape(space):
+    return (-1,) + (1,) * (space.dim - 1)
+
+
+def gp_dirichlet_rhs(space, bcs, t, tau_scale=1.0):
+    """Pressure-Dirichlet data g_p on velocity-Neumann faces
+    (operators.py:241-259)."""
+    b, g, dim = space.basis, space.geom, space.dim
+    q = b.n_q
+    Vc, = _zeros_faces(space, 1, q)
+    D = _zeros_faces(space, dim, q)
+    for eb, sb, bc in bcs.neumann:
+        gp = bc.g_p(_face_points(space, g, b, eb, sb), t)
+        sjb = g.sjxw[sb, eb]
+        taub = tau_scale * space.tau_e[eb].reshape(_bshape(space))
+        Vc[sb, eb] = 2.0 * taub * gp * sjb
+        for a in range(dim):
+            D[a][sb, eb] = -gp * g.normal[a][sb, eb] * sjb
+    out = np.zeros(space.field_shape())
+    face_lift_values(Vc, b, out, dim)
+    face_lift_gradients(_ref_test(_face_jit(space, g), D), b, out, dim)
+    return out
+
+
+def _divergence_at_q(space, u):
+    b, g, dim = space.basis, space.geom, space.dim
+    div = 0.0
+    for c in range(dim):
+        div = div + _phys_grad(g.jinvT, vol_gradients(u[c], b, dim))[c]
+    return div
+
+
+def eval_divergence_rhs(space, u, bcs, scale, form="standard"):
+    """a(q, u) scaled: standard / weak (central flux) / strong
+    (operators.py:265-316)."""
+    b, g, dim = space.basis, space.geom, space.dim
+    q = b.n_q
+    if form == "standard":
+        return vol_integrate_values(-scale * _divergence_at_q(space, u) * g.jxw,
+                                    b, dim)
+    if form not in ("weak", "strong"):
+        raise ValueError(f"unknown divergence form {form!r}")
+    f = [face_values(u[c], b, dim) for c in range(dim)]
+    un = sum(g.normal[a] * f[a] for a in range(dim))
+    Vc, = _zeros_faces(space, 1, q)
+    sj = g.sjxw[space.f_sm, space.f_em]
+    unm, unp = space.gather_minus(un), space.gather_plus(un)
+    if form == "weak":
+        data = [scale * vol_values(u[c], b, dim) * g.jxw for c in range(dim)]
+        out = vol_integrate_gradients(_ref_test(g.jinvT, data), b, dim)
+        Vm = -scale * 0.5 * (unm - unp) * sj
+        space.scatter_faces(Vm, -Vm, Vc)
+        for groups in (bcs.dirichlet, bcs.neumann):
+            for eb, sb, _ in groups:
+                Vc[sb, eb] = -scale * un[sb, eb] * g.sjxw[sb, eb]
+        face_lift_values(Vc, b, out, dim)
+        return out
+    out = vol_integrate_values(-scale * _divergence_at_q(space, u) * g.jxw, b, dim)
+    Vm = scale * 0.5 * (unm + unp) * sj
+    space.scatter_faces(Vm, Vm, Vc)
+    face_lift_values(Vc, b, out, dim)
+    return out
+
+
+def eval_pressure_gradient_rhs(space, p, bcs, scale, form="standard"):
+    """b(v, p) scaled: standard -(v, scale grad p) or weak with central flux
+    (operators.py:322-366)."""
+    b, g, dim = space.basis, space.geom, space.dim
+    q = b.n_q
+    out = np.empty(space.field_shape(dim))
+    if form == "standard":
+        ph = _phys_grad(g.jinvT, vol_gradients(p, b, dim))
+        for a in range(dim):
+            out[a] = vol_integrate_values(-scale * ph[a] * g.jxw, b, dim)
+        return out
+    if form != "weak":
+        raise ValueError(f"unknown pressure-gradient form {form!r}")
+    s = scale * vol_values(p, b, dim) * g.jxw
+    for a in range(dim):
+        data = [s if c == a else np.zeros_like(s) for c in range(dim)]
+        out[a] = vol_integrate_gradients(_ref_test(g.jinvT, data), b, dim)
+    fv = face_values(p, b, dim)
+    sj = g.sjxw[space.f_sm, space.f_em]
+    avg = 0.5 * (space.gather_minus(fv) + space.gather_plus(fv))
+    for a in range(dim):
+        V, = _zeros_faces(space, 1, q)
+        Vm = -scale * avg * g.normal[a][space.f_sm, space.f_em] * sj
+        space.scatter_faces(Vm, -Vm, V)
+        for groups in (bcs.dirichlet, bcs.neumann):
+            for eb, sb, _ in groups:
+                V[sb, eb] = -scale * fv[sb, eb] * g.normal[a][sb, eb] * g.sjxw[sb, eb]
+        face_lift_values(V, b, out[a], dim)
+    return out
+
+
+def viscous_rhs_bc(space, bcs, t, nu):
+    """Boundary-data terms of the viscous solve (operators.py:494-527)."""
+    b, g, dim = space.basis, space.geom, space.dim
+    q = b.n_q
+    V = _zeros_faces(space, dim, q)
+    Dd = [_zeros_faces(space, dim, q) for _ in range(dim)]
+    for eb, sb, bc in bcs.dirichlet:
+        gu = bc.g(_face_points(space, g, b, eb, sb), t)
+        sjb = g.sjxw[sb, eb]
+        nb = [g.normal[a][sb, eb] for a in range(dim)]
+        taub = space.tau_e[eb].reshape(_bshape(space)) * nu
+        for a in range(dim):
+            V[a][sb, eb] = 2.0 * taub * gu[a] * sjb
+            for c in range(dim):
+                Dd[a][c][sb, eb] = -nu * (gu[a] * nb[c] + gu[c] * nb[a]) * sjb
+    for eb, sb, bc in bcs.neumann:
+        xb = _face_points(space, g, b, eb, sb)
+        h, gp = bc.h(xb, t), bc.g_p(xb, t)
+        sjb = g.sjxw[sb, eb]
+        for a in range(dim):
+            V[a][sb, eb] = (h[a] + gp * g.normal[a][sb, eb]) * sjb
+    out = np.zeros(space.field_shape(dim))
+    jf = _face_jit(space, g)
+    for a in range(dim):
+        face_lift_values(V[a], b, out[a], dim)
+        face_lift_gradients(_ref_test(jf, Dd[a]), b, out[a], dim)
+    return out
+
+
+def _curl(grad):
+    """curl from grad[c][a] = d u_c / d x_a: scalar in 2D, 3-vector in 3D."""
+    if len(grad) == 2:
+        return grad[1][0] - grad[0][1]
+    return [grad[2][1] - grad[1][2], grad[0][2] - grad[2][0], grad[1][0] - grad[0][1]]
+
+
+def compute_vorticity(space, u):
+    """Element-local L2 projection of curl u (operators.py:610-618); a scalar
+    field in 2D (the reference), the three curl components in 3D."""
+    b, g, dim = space.basis, space.geom, space.dim
+    grad = [_phys_grad(g.jinvT, vol_gradients(u[c], b, dim)) for c in range(dim)]
+    w = _curl(grad)
+    if dim == 2:
+        return apply_inverse_mass(vol_integrate_values(w * g.jxw, b, dim), b, g.jxw, dim)
+    return np.stack([apply_inverse_mass(vol_integrate_values(wc * g.jxw, b, dim),
+                                        b, g.jxw, dim) for wc in w])
+
+
+def eval_pressure_neumann_rhs(space, bcs, history, vorticity_history, betas, nu,
+                              t_np1, body_force=None):
+    """Consistent pressure Neumann data on velocity-Dirichlet faces:
+    -(dg/dt + sum_i beta_i (div(u u) + nu curl w) - f) . n (operators.py:621-672).
+    In 3D the vorticity is a 3-vector and curl w its vector curl."""
+    b, g, dim = space.basis, space.geom, space.dim
+    q = b.n_q
+    out = np.zeros(space.field_shape())
+    if not bcs.dirichlet:
+        return out
+    jf = _face_jit(space, g)
+    hp = [0.0] * dim
+    for beta, u, w in zip(betas, history, vorticity_history):
+        f = [face_values(u[c], b, dim) for c in range(dim)]
+        gr = [_phys_grad(jf, face_gradients(u[c], b, dim)) for c in range(dim)]
+        div = sum(gr[c][c] for c in range(dim))
+        conv = [f[a] * div + sum(f[c] * gr[a][c] for c in range(dim)) for a in range(dim)]
+        if dim == 2:
+            gw = _phys_grad(jf, face_gradients(w, b, dim))
+            curlw = [gw[1], -gw[0]]
+        else:
+            curlw = _curl([_phys_grad(jf, face_gradients(w[c], b, dim)) for c in range(dim)])
+        for a in range(dim):
+            hp[a] = hp[a] + beta * (conv[a] + nu * curlw[a])
+    Vc, = _zeros_faces(space, 1, q)
+    for eb, sb, bc in bcs.dirichlet:
+        xb = _face_points(space, g, b, eb, sb)
+        if bc.dg_dt is not None:
+            dgdt = bc.dg_dt(xb, t_np1)
+        else:
+            dgdt = np.zeros((dim,) + xb.shape[1:])
+        h = [dgdt[a] + hp[a][sb, eb] for a in range(dim)]
+        if body_force is not None:
+            fb = body_force(xb, t_np1)
+            h = [h[a] - fb[a] for a in range(dim)]
+        hn = sum(h[a] * g.normal[a][sb, eb] for a in range(dim))
+        Vc[sb, eb] = -hn * g.sjxw[sb, eb]
+    face_lift_values(Vc, b, out, dim)
+    return out
+
+
+# ---------------------------------------------------------------------------
 # solvers (reference solvers.py; dimension-agnostic)
 
 @dataclass
@@ -1062,6 +1250,54 @@ def eigen_estimate_via_cg(op, prec_diag, b, n_iter=20):
         T[i, i - 1] = T[i - 1, i] = off
     ev = np.linalg.eigvalsh(T)
     return float(ev[-1]), float(max(ev[0], 1e-12 * ev[-1]))
+
+
+def element_local_pcg(op_local, prec_local, b, rel_tol=1e-12, max_iter=200,
+                      floor_factor=8.0):
+    """Batched per-cell CG with per-cell stopping and the eps*lambda_max floor
+    from the running Lanczos diagonal (solvers.py:201-256).  Layout
+    (ncomp, ne, ...): the cell axis is axis 1 here (axis 2 in the reference's
+    (ncomp, m, ne, m) kernel layout)."""
+    ne = b.shape[1]
+    red = (0,) + tuple(range(2, b.ndim))
+    bc = (None, slice(None)) + (None,) * (b.ndim - 2)
+
+    def edot(u, v):
+        return (u * v).sum(axis=red)
+
+    x = np.zeros_like(b)
+    r = b.copy()
+    z = prec_local(r)
+    rz = edot(r, z)
+    norm0 = np.sqrt(np.maximum(rz, 0.0))
+    active = norm0 > rel_tol * norm0
+    iters = np.zeros(ne, dtype=int)
+    p = z.copy()
+    eps = np.finfo(float).eps
+    lan_max = np.ones(ne)
+    alpha_prev = np.ones(ne)
+    beta_prev = np.zeros(ne)
+    for it in range(1, max_iter + 1):
+        if not active.any():
+            break
+        Ap = op_local(p)
+        pAp = edot(p, Ap)
+        safe = np.where(active & (pAp > 0), pAp, 1.0)
+        alpha = np.where(active, rz / safe, 1.0)
+        lan_max = np.maximum(lan_max, 1.0 / alpha + beta_prev / alpha_prev)
+        x += np.where(active, alpha, 0.0)[bc] * p
+        r -= np.where(active, alpha, 0.0)[bc] * Ap
+        z = prec_local(r)
+        rz_new = edot(r, z)
+        norm = np.sqrt(np.maximum(rz_new, 0.0))
+        iters[active] = it
+        tol = np.maximum(rel_tol, floor_factor * eps * lan_max) * norm0
+        active = active & (norm > tol)
+        beta = np.where(active, rz_new / np.where(rz > 0, rz, 1.0), 0.0)
+        alpha_prev, beta_prev = alpha, beta
+        p = z + beta[bc] * p
+        rz = rz_new
+    return x, iters, ~active
 
 
 def zero_mean_project(space, p):

@@ -23,20 +23,35 @@ BC_NONE, BC_VELOCITY_DIRICHLET, BC_VELOCITY_NEUMANN = 0, 1, 2
 
 
 def sources():
-    return [os.path.join(CSRC, f) for f in ("dgmf.cu", "tables.cpp")]
+    names = ["dgmf.cu", "vecops.cu", "vec_over.cu", "tables.cpp"]
+    names += [f"vec_lin{d}_{p}.cu" for d in (2, 3) for p in ("00", "01", "10", "11")]
+    return [os.path.join(CSRC, f) for f in names]
 
 
 def build(verbose=False, force=False):
-    """Compile libdgmf.so for sm_100a with nvcc (in-tree, travels with the repo)."""
+    """Compile libdgmf.so for sm_100a with nvcc (in-tree, travels with the repo).
+    One nvcc per translation unit, run in parallel, then one link."""
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(ROOT, "include", "dgmf.h"))
     if (not force and os.path.exists(LIB_PATH) and
             os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(d) for d in deps)):
         return LIB_PATH
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc] + NVCC_FLAGS + ["-o", LIB_PATH + ".tmp"] + sources()
-    if verbose:
-        print(" ".join(cmd))
+    objdir = os.path.join(HERE, "_build")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    procs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc] + compile_flags + ["-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd))
+        procs.append((subprocess.Popen(cmd, cwd=HERE), src))
+        objs.append(obj)
+    failed = [src for p, src in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc {failed}")
+    cmd = [nvcc] + NVCC_FLAGS + ["-o", LIB_PATH + ".tmp"] + objs
     subprocess.run(cmd, check=True, cwd=HERE)
     os.replace(LIB_PATH + ".tmp", LIB_PATH)
     return LIB_PATH
@@ -83,6 +98,14 @@ PROTOTYPES = {
     "dg_helmholtz_vmult": [_P, _P, _P, _D, _D, _P],
     "dg_projection_vmult": [_P, _P, _P, _P, _P, _P],
     "dg_convective_rhs": [_P, _I, _P, _P, _P, _P],
+    "dg_convective_rhs_ex": [_P, _I, _P, _P, _P, _P, _P, _P],
+    "dg_divergence_rhs": [_P, _P, _P, _D, _I, _P],
+    "dg_pressure_gradient_rhs": [_P, _P, _P, _D, _I, _P],
+    "dg_vorticity": [_P, _P, _P, _P],
+    "dg_pressure_neumann_rhs": [_P, _I, _P, _P, _P, _D, _P, _P, _P],
+    "dg_gp_dirichlet_rhs": [_P, _P, _D, _P, _P],
+    "dg_viscous_rhs_bc": [_P, _P, _D, _P, _P],
+    "dg_element_local_pcg": [_P, _P, _P, _P, _D, _I, _D, _P, _P, _P],
     "dg_dot": [_P, _P, _P, _L, _P, _P],
     "dg_zero_mean_dual": [_P, _P, _P],
     "dg_zero_mean": [_P, _P, _P],

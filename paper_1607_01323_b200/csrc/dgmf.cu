@@ -7,13 +7,13 @@
 #include <vector>
 
 #include "common.cuh"
+#include "ctx.h"
 #include "laplace.cuh"
 #include "laplace_persist.cuh"
 #include "laplace_warp.cuh"
 #include "tables.h"
 #include "tensor.cuh"
 #include "tensor_fast.cuh"
-#include "vecops.cuh"
 #include "vector.cuh"
 
 namespace dg {
@@ -27,7 +27,7 @@ int cuda_fail(cudaError_t e, const char *where) {
   return DG_ECUDA;
 }
 
-static int inval(const std::string &m) {
+int inval(const std::string &m) {
   g_err = m;
   return DG_EINVAL;
 }
@@ -35,57 +35,6 @@ static int inval(const std::string &m) {
 }  // namespace dg
 
 using namespace dg;
-
-struct dg_ctx {
-  int dim = 3, k = 1, n = 2, nq_over = 2;
-  int gcounts[3] = {1, 1, 1};
-  int counts[3] = {1, 1, 1};
-  int slab_begin = 0, slab_end = 0;
-  int periodic[3] = {0, 0, 0};
-  int bc[6] = {0, 0, 0, 0, 0, 0};
-  int mode[6] = {0, 0, 0, 0, 0, 0};
-  Basis1D basis, over;
-  std::vector<double> gvert[3];
-  std::vector<double> hx, hy, hz, tau;  // host, owned
-  double ghost_h[2] = {1.0, 1.0};
-  std::vector<double> ghost_tau_h[2];
-  double *d_hx = nullptr, *d_hy = nullptr, *d_hz = nullptr, *d_tau = nullptr;
-  double *d_ghost_tau[2] = {nullptr, nullptr};
-  const double *d_recv[2] = {nullptr, nullptr};  // caller-owned ghost layers
-  int64_t halo_count = 0;
-  int64_t n_cells = 0, n_dofs = 0, np = 0;
-  double volume = 0.0;  // |Omega| of the GLOBAL mesh
-  double *d_red = nullptr;     // reduction partials (kRedBlocks) + scalars
-  double *d_scal = nullptr;    // 16 device scalars
-  double *h_scal = nullptr;    // pinned mirror
-  std::vector<double *> work;  // solver work vectors (n_dofs each)
-  double *d_partials = nullptr;  // per-brick partial sums of the fused vmult epilogue
-  int64_t partials_n = 0;
-  std::mutex mu;
-
-  Geo geo() const {
-    Geo g;
-    g.nx = counts[0];
-    g.ny = counts[1];
-    g.nz = counts[2];
-    g.hx = d_hx;
-    g.hy = d_hy;
-    g.hz = d_hz;
-    g.tau = d_tau;
-    for (int i = 0; i < 6; ++i) g.mode[i] = mode[i];
-    for (int s = 0; s < 2; ++s) {
-      g.ghost[s] = d_recv[s];
-      g.ghost_tau[s] = d_ghost_tau[s];
-      g.ghost_h[s] = ghost_h[s];
-    }
-    static const int exp_flags = [] {
-      const char *v = getenv("DG_EXP");
-      return v ? atoi(v) : 0;
-    }();
-    g.exp_flags = exp_flags;
-    return g;
-  }
-};
 
 // tau_e of GLOBAL cell (gx, gy, gz), Eq. 18 (geometry.py:90-108): every
 // boundary face counts in A_bnd (also walls without a pressure term),
@@ -749,7 +698,5 @@ int dg_laplace_diagonal(dg_ctx *c, double *diag, double tau_scale, void *stream)
 
 #include "pcg.inc"
 
-// ---------------------------------------------------------------------------
-// vector-valued operators (Helmholtz, projection, convective) live in
-// vecops.inc
-#include "vecops.inc"
+// The quadrature-point operators (Helmholtz, projection, convective, the
+// once-per-step right-hand sides, element-local PCG) are in vecops.cu.

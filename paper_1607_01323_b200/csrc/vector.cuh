@@ -25,7 +25,7 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
 }
 
 // partial[b] = sum over this block's strided slice of x*y (y == null -> sum x)
-__global__ void dot_partial_kernel(const double *__restrict__ x,
+static __global__ void dot_partial_kernel(const double *__restrict__ x,
                                    const double *__restrict__ y, int64_t n,
                                    double *__restrict__ partial) {
   __shared__ double sh[32];
@@ -38,7 +38,7 @@ __global__ void dot_partial_kernel(const double *__restrict__ x,
 }
 
 // out[0] = sum(partial[0..m)) in fixed order (one block)
-__global__ void sum_partials_kernel(const double *__restrict__ partial, int m,
+static __global__ void sum_partials_kernel(const double *__restrict__ partial, int m,
                                     double *__restrict__ out) {
   __shared__ double sh[32];
   double acc = 0.0;

@@ -9,6 +9,13 @@ Same names, arguments and error behaviour as the reference:
   apply_projection_operator(space, w, tau_d_e, tau_c_f)      operators.py:372
   eval_convective_rhs(space, bcs, history, betas, times, t_np1,
                       body_force=None)                       operators.py:533
+  eval_divergence_rhs(space, u, bcs, scale, form)            operators.py:265
+  eval_pressure_gradient_rhs(space, p, bcs, scale, form)     operators.py:322
+  compute_vorticity(space, u)                                operators.py:610
+  eval_pressure_neumann_rhs(space, bcs, history, vorticity_history, betas,
+                            nu, t_np1, body_force=None)      operators.py:621
+  gp_dirichlet_rhs(space, bcs, t, tau_scale=1.0)             operators.py:241
+  viscous_rhs_bc(space, bcs, t, nu)                          operators.py:494
 
 Inputs may be torch CUDA tensors (element-major device layout; the result
 is a new CUDA tensor) or numpy arrays (reference layout: the 2D kernel
@@ -237,22 +244,286 @@ def apply_projection_operator(space: DgSpace, w, tau_d_e, tau_c_f):
 
 def eval_convective_rhs(space: DgSpace, bcs: ResolvedBCs, history, betas, times,
                         t_np1: float, body_force: Optional[Callable] = None):
-    """sum_i beta_i [(grad v, u u) - (v, F*.n)] with the local Lax-Friedrichs
-    flux on the over-integration rule (operators.py:533-594).  The device
-    path covers homogeneous velocity data (zero Dirichlet g) and no body
-    force, the hot-path case of BASELINE config 3."""
+    """sum_i beta_i [(grad v, u u) - (v, F*.n)] + (v, f) with the local
+    Lax-Friedrichs flux on the over-integration rule (operators.py:533-594).
+    Dirichlet data g(x, times[i]) enters the mirror state 2g - u (a None
+    callable means homogeneous data, as for every boundary callable here); the data and
+    the body force are sampled on the host (they are the caller's Python
+    callables) and integrated on the device."""
     import ctypes
-    torch = _torch()
-    if body_force is not None:
-        raise NotImplementedError("body forces are assembled on the host path "
-                                  "(not part of the device hot path)")
-    for _, bc in bcs.dirichlet:
-        pass  # homogeneous data assumed: g = 0 on the hot path
+    if len(times) < len(history) or len(betas) < len(history):
+        raise ValueError("need one beta and one time per history level")
     args = [_Arg(space, u, space.dim) for u in history]
     out = args[0].new_out()
     ptrs = (ctypes.c_void_p * len(args))(*[a.t.data_ptr() for a in args])
     b = (ctypes.c_double * len(betas))(*[float(x) for x in betas])
+    keep = []
+    gd = None
+    if bcs.dirichlet:
+        pts = _rule_points(space, space.n_q_over)
+        flat = []
+        for t_i in times[:len(args)]:
+            sides = _side_data(space, pts, [(tag, lambda x, bc=bc, t=t_i: bc.g(x, t))
+                                            for tag, bc in bcs.dirichlet
+                                            if bc.g is not None], keep)
+            flat += sides
+        gd = (ctypes.c_void_p * len(flat))(*flat)
+    body = ctypes_ptr(0)
+    if body_force is not None:
+        fq = body_force(_volume_points(space, space.n_q_over), t_np1)
+        fq = np.ascontiguousarray(np.asarray(fq, dtype=np.float64).reshape(space.dim, -1))
+        keep.append(_dev(fq))
+        body = ctypes_ptr(keep[-1].data_ptr())
     ctx = space.ctx(bcs.kinds)
-    _lib.call("dg_convective_rhs", ctx.handle, len(args), ctypes.cast(ptrs, ctypes.c_void_p),
-              ctypes.cast(b, ctypes.c_void_p), ctypes_ptr(out.data_ptr()), _stream())
+    _lib.call("dg_convective_rhs_ex", ctx.handle, len(args), ctypes.cast(ptrs, ctypes.c_void_p),
+              ctypes.cast(b, ctypes.c_void_p),
+              ctypes.cast(gd, ctypes.c_void_p) if gd is not None else ctypes_ptr(0),
+              body, ctypes_ptr(out.data_ptr()), _stream())
     return args[0].result(out)
+
+
+# ---------------------------------------------------------------------------
+# once-per-step right-hand sides (operators.py:241-366, 494-527, 610-672)
+
+_FORMS = {"standard": 0, "weak": 1, "strong": 2}
+
+
+def _dev(a):
+    torch = _torch()
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to("cuda")
+
+
+def _rule_points(space, n_q):
+    from .basis import get_basis
+    return np.asarray(get_basis(space.k, n_q).points)
+
+
+def _volume_points(space, n_q):
+    """Physical coordinates of the tensor Gauss points of every cell,
+    (dim, ne, [z,] y, x) in element-major order."""
+    pts = _rule_points(space, n_q)
+    dim, mesh = space.dim, space.mesh
+    idx = np.indices(mesh.counts[::-1]).reshape(dim, -1)[::-1]      # ix, iy, iz
+    out = []
+    for d in range(dim):
+        v = mesh.axis_vertices[d]
+        c = v[idx[d]][:, None] + 0.5 * (pts[None, :] + 1.0) * np.diff(v)[idx[d]][:, None]
+        shape = [mesh.n_elements] + [1] * dim
+        shape[dim - d] = len(pts)
+        out.append(np.broadcast_to(c.reshape(shape), (mesh.n_elements,) + (len(pts),) * dim))
+    return np.stack(out)
+
+
+def side_face_points(space, side, pts):
+    """Physical coordinates of the face Gauss points of the boundary cells of
+    one side (side = 2*d + s, TAG_NAMES order) in the device boundary-data
+    layout of include/dgmf.h: (dim, ntan, [slow,] fast), tangential cells
+    (slow, fast) and points [slow][fast] in decreasing axis order."""
+    dim, mesh = space.dim, space.mesh
+    d, s = divmod(side, 2)
+    tang = [a for a in range(dim - 1, -1, -1) if a != d]
+    counts = [mesh.counts[a] for a in tang]
+    q = len(pts)
+    nt = len(tang)
+    X = np.empty((dim,) + tuple(counts) + (q,) * nt)
+    for a in range(dim):
+        v = mesh.axis_vertices[a]
+        if a == d:
+            X[a] = v[-1] if s else v[0]
+            continue
+        j = tang.index(a)
+        c = v[:-1, None] + 0.5 * (pts[None, :] + 1.0) * np.diff(v)[:, None]
+        shape = [1] * (2 * nt)
+        shape[j] = counts[j]
+        shape[nt + j] = q
+        X[a] = c.reshape(shape)
+    return X.reshape((dim, int(np.prod(counts))) + (q,) * nt)
+
+
+def _side_data(space, pts, entries, keep):
+    """Evaluate per-tag data callables fn(x) at the face points of their
+    sides; returns 6 device pointers (0 where no data) in the layout
+    [ntan][ncomp][n_f]."""
+    ptrs = [0] * 6
+    for tag, fn in entries:
+        side = TAG_NAMES.index(tag)
+        X = side_face_points(space, side, pts)
+        val = np.asarray(fn(X), dtype=np.float64)
+        if val.ndim == X.ndim - 1:          # scalar data
+            val = val[None]
+        nt = X.shape[1]
+        val = np.ascontiguousarray(np.moveaxis(val.reshape(val.shape[0], nt, -1), 1, 0))
+        t = _dev(val)
+        keep.append(t)
+        ptrs[side] = t.data_ptr()
+    return ptrs
+
+
+def _out_result(space, out, ncomp, like):
+    """Result for calls whose only inputs are callables: a CUDA tensor if
+    ``like`` is a tensor (or the string 'device'), else numpy in the layout
+    of ``like`` (default: the 2D reference kernel layout / 3D element-major)."""
+    torch = _torch()
+    if isinstance(like, torch.Tensor) or (isinstance(like, str) and like == "device"):
+        return out
+    if like is None:
+        m, ne = space.k + 1, space.mesh.n_elements
+        if space.dim == 2:
+            like_shape = (m, ne, m) if ncomp == 1 else (ncomp, m, ne, m)
+        else:
+            like_shape = space.field_shape(None if ncomp == 1 else ncomp)
+    else:
+        like_shape = np.shape(like)
+    return space.from_element_major(out.cpu().numpy(), ncomp, like_shape)
+
+
+def _bnd_call(name, space, bcs, entries, ncomp_out, like, *scalars):
+    import ctypes
+    torch = _torch()
+    keep = []
+    ptrs = _side_data(space, _rule_points(space, space.k + 1), entries, keep)
+    arr = (ctypes.c_void_p * 6)(*ptrs)
+    out = torch.empty(space.n_dofs * ncomp_out, dtype=torch.float64, device="cuda")
+    ctx = space.ctx(bcs.kinds)
+    _lib.call(name, ctx.handle, ctypes.cast(arr, ctypes.c_void_p),
+              *[ctypes.c_double(v) for v in scalars], ctypes_ptr(out.data_ptr()), _stream())
+    return _out_result(space, out, ncomp_out, like)
+
+
+def gp_dirichlet_rhs(space: DgSpace, bcs: ResolvedBCs, t: float, tau_scale: float = 1.0,
+                     like=None):
+    """Pressure-Dirichlet data g_p on velocity-Neumann faces for the Poisson
+    right side (operators.py:241-259)."""
+    entries = [(tag, lambda x, bc=bc: bc.g_p(x, t)) for tag, bc in bcs.neumann
+               if bc.g_p is not None]
+    return _bnd_call("dg_gp_dirichlet_rhs", space, bcs, entries, 1, like, float(tau_scale))
+
+
+def viscous_rhs_bc(space: DgSpace, bcs: ResolvedBCs, t: float, nu: float, like=None):
+    """Boundary-data terms of the viscous solve (operators.py:494-527):
+    Dirichlet g with 2 tau nu and the symmetric-gradient test, Neumann
+    h + g_p n."""
+    entries = [(tag, lambda x, bc=bc: bc.g(x, t)) for tag, bc in bcs.dirichlet
+               if bc.g is not None]
+
+    def neu(bc):
+        def f(x):
+            h = (np.asarray(bc.h(x, t), dtype=np.float64) if bc.h is not None
+                 else np.zeros((space.dim,) + x.shape[1:]))
+            gp = (np.asarray(bc.g_p(x, t), dtype=np.float64) if bc.g_p is not None
+                  else np.zeros(x.shape[1:]))
+            return np.concatenate([h, np.broadcast_to(gp, h.shape[1:])[None]])
+        return f
+    entries += [(tag, neu(bc)) for tag, bc in bcs.neumann
+                if bc.h is not None or bc.g_p is not None]
+    return _bnd_call("dg_viscous_rhs_bc", space, bcs, entries, space.dim, like, float(nu))
+
+
+def eval_divergence_rhs(space: DgSpace, u, bcs: ResolvedBCs, scale: float,
+                        form: str = "standard"):
+    """a(q, u) scaled: 'standard' volume form, 'weak' with central flux or
+    its 'strong' rewrite (operators.py:265-316)."""
+    if form not in _FORMS:
+        raise ValueError(f"unknown divergence form {form!r}")
+    torch = _torch()
+    a = _Arg(space, u, space.dim)
+    out = torch.empty(space.n_dofs, dtype=torch.float64, device="cuda")
+    ctx = space.ctx(bcs.kinds)
+    _lib.call("dg_divergence_rhs", ctx.handle, a.ptr(), ctypes_ptr(out.data_ptr()),
+              float(scale), _FORMS[form], _stream())
+    return _scalar_like(space, a, out)
+
+
+def _scalar_like(space, a, out):
+    """Scalar result of a vector-input call, in the input's type/layout."""
+    if a.is_torch:
+        return out.view(a.shape[1:]) if len(a.shape) > 1 and a.shape[0] == space.dim \
+            and int(np.prod(a.shape[1:])) == space.n_dofs else out
+    like = a.shape[1:] if len(a.shape) > 1 else (space.n_dofs,)
+    return space.from_element_major(out.cpu().numpy(), 1, like)
+
+
+def _vector_like(space, a, out):
+    """Vector result of a scalar-input call, in the input's type/layout."""
+    ncomp = space.dim
+    if a.is_torch:
+        return out.view((ncomp,) + tuple(a.shape)) if len(a.shape) > 1 else out
+    return space.from_element_major(out.cpu().numpy(), ncomp, (ncomp,) + tuple(a.shape))
+
+
+def eval_pressure_gradient_rhs(space: DgSpace, p, bcs: ResolvedBCs, scale: float,
+                               form: str = "standard"):
+    """b(v, p) scaled: standard -(v, scale grad p) or weak with central flux
+    (operators.py:322-366)."""
+    if form not in ("standard", "weak"):
+        raise ValueError(f"unknown pressure-gradient form {form!r}")
+    torch = _torch()
+    a = _Arg(space, p, 1)
+    out = torch.empty(space.n_dofs * space.dim, dtype=torch.float64, device="cuda")
+    ctx = space.ctx(bcs.kinds)
+    _lib.call("dg_pressure_gradient_rhs", ctx.handle, a.ptr(), ctypes_ptr(out.data_ptr()),
+              float(scale), _FORMS[form], _stream())
+    return _vector_like(space, a, out)
+
+
+def compute_vorticity(space: DgSpace, u):
+    """Element-local L2 projection of curl u (operators.py:610-618): a scalar
+    field in 2D (the reference), the three curl components in 3D."""
+    torch = _torch()
+    a = _Arg(space, u, space.dim)
+    nw = 1 if space.dim == 2 else 3
+    out = torch.empty(space.n_dofs * nw, dtype=torch.float64, device="cuda")
+    ctx = space.ctx(space.default_kinds())
+    _lib.call("dg_vorticity", ctx.handle, a.ptr(), ctypes_ptr(out.data_ptr()), _stream())
+    if nw == 1:
+        return _scalar_like(space, a, out)
+    return a.result(out)
+
+
+def eval_pressure_neumann_rhs(space: DgSpace, bcs: ResolvedBCs, history, vorticity_history,
+                              betas, nu: float, t_np1: float,
+                              body_force: Optional[Callable] = None, like=None):
+    """Consistent pressure Neumann data on velocity-Dirichlet faces:
+    -(dg/dt + sum_i beta_i (div(u u) + nu curl w) - f) . n
+    (operators.py:621-672).  dg/dt and f are sampled on the host at the face
+    points (caller's callables); the traces run on the device."""
+    import ctypes
+    torch = _torch()
+    nw = 1 if space.dim == 2 else 3
+    hist = [_Arg(space, u, space.dim) for u in history]
+    if not bcs.dirichlet:
+        out = torch.zeros(space.n_dofs, dtype=torch.float64, device="cuda")
+        return _out_result(space, out, 1, like) if like is not None else \
+            _scalar_like(space, hist[0], out)
+    vort = [_Arg(space, w, nw) for w in vorticity_history]
+    if len(vort) < len(hist) or len(betas) < len(hist):
+        raise ValueError("need one vorticity field and one beta per history level")
+    keep = []
+    entries = []
+    for tag, bc in bcs.dirichlet:
+        if bc.dg_dt is None and body_force is None:
+            continue
+
+        def f(x, bc=bc):
+            h = (np.asarray(bc.dg_dt(x, t_np1), dtype=np.float64) if bc.dg_dt is not None
+                 else np.zeros((space.dim,) + x.shape[1:]))
+            if body_force is not None:
+                h = h - np.asarray(body_force(x, t_np1), dtype=np.float64)
+            return h
+        entries.append((tag, f))
+    ptrs = _side_data(space, _rule_points(space, space.k + 1), entries, keep)
+    bnd = (ctypes.c_void_p * 6)(*ptrs)
+    hp = (ctypes.c_void_p * len(hist))(*[a.t.data_ptr() for a in hist])
+    wp = (ctypes.c_void_p * len(hist))(*[w.t.data_ptr() for w in vort[:len(hist)]])
+    bt = (ctypes.c_double * len(hist))(*[float(x) for x in betas[:len(hist)]])
+    out = torch.empty(space.n_dofs, dtype=torch.float64, device="cuda")
+    ctx = space.ctx(bcs.kinds)
+    _lib.call("dg_pressure_neumann_rhs", ctx.handle, len(hist), ctypes.cast(hp, ctypes.c_void_p),
+              ctypes.cast(wp, ctypes.c_void_p), ctypes.cast(bt, ctypes.c_void_p), float(nu),
+              ctypes.cast(bnd, ctypes.c_void_p), ctypes_ptr(out.data_ptr()), _stream())
+    if like is not None:
+        return _out_result(space, out, 1, like)
+    return _scalar_like(space, hist[0], out)
+
+
+

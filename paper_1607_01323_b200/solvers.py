@@ -259,3 +259,94 @@ def laplace_pcg(space, bcs, b, tau_scale: float = 1.0, project_dual: bool = Fals
     if is_np:
         return space.from_element_major(x.cpu().numpy(), 1, np.shape(b)), stats
     return x.view(shape), stats
+
+
+def element_local_pcg(op_local: Callable, prec_local: Callable, b, rel_tol: float = 1e-12,
+                      max_iter: int = 200, floor_factor: float = 8.0):
+    """Batched per-cell CG on block-diagonal SPD systems with the reference
+    semantics (solvers.py:201-256): every cell iterates with its own alpha,
+    beta and stops individually; the tolerance is clipped at
+    floor_factor * eps * lambda_max (running Lanczos diagonal).
+
+    Device vectors: b is a CUDA tensor (or numpy array moved to the device)
+    in element-major layout (ncomp, ne, ...), cell axis 1; the callables take
+    and return tensors of that layout.  Returns (x, iterations per cell,
+    converged per cell) as (tensor, numpy int array, numpy bool array).
+    For the V3 projection (op = projection with tau_C = None, prec = inverse
+    mass) use ``projection_element_pcg``, which runs all cells' iterations in
+    one kernel."""
+    torch = _torch()
+    b = _to_dev(b)
+    ne = b.shape[1]
+    red = (0,) + tuple(range(2, b.dim()))
+    bshape = (1, ne) + (1,) * (b.dim() - 2)
+
+    def edot(u, v):
+        return (u * v).sum(dim=red)
+
+    x = torch.zeros_like(b)
+    r = b.clone()
+    z = prec_local(r)
+    rz = edot(r, z)
+    norm0 = torch.sqrt(torch.clamp(rz, min=0.0))
+    active = norm0 > rel_tol * norm0
+    iters = torch.zeros(ne, dtype=torch.int64, device=b.device)
+    p = z.clone()
+    eps = float(np.finfo(float).eps)
+    lan_max = torch.ones(ne, dtype=b.dtype, device=b.device)
+    alpha_prev = torch.ones_like(lan_max)
+    beta_prev = torch.zeros_like(lan_max)
+    one = torch.ones_like(lan_max)
+    for it in range(1, max_iter + 1):
+        if not bool(active.any()):
+            break
+        Ap = op_local(p)
+        pAp = edot(p, Ap)
+        safe = torch.where(active & (pAp > 0), pAp, one)
+        alpha = torch.where(active, rz / safe, one)
+        lan_max = torch.maximum(lan_max, 1.0 / alpha + beta_prev / alpha_prev)
+        am = torch.where(active, alpha, torch.zeros_like(alpha)).view(bshape)
+        x += am * p
+        r -= am * Ap
+        z = prec_local(r)
+        rz_new = edot(r, z)
+        norm = torch.sqrt(torch.clamp(rz_new, min=0.0))
+        iters[active] = it
+        tol = torch.clamp(floor_factor * eps * lan_max, min=rel_tol) * norm0
+        active = active & (norm > tol)
+        beta = torch.where(active, rz_new / torch.where(rz > 0, rz, one),
+                           torch.zeros_like(rz))
+        alpha_prev, beta_prev = alpha, beta
+        p = z + beta.view(bshape) * p
+        rz = rz_new
+    return x, iters.cpu().numpy(), (~active).cpu().numpy()
+
+
+def projection_element_pcg(space, b, tau_d, rel_tol: float = 1e-12, max_iter: int = 200,
+                           floor_factor: float = 8.0):
+    """Fused ``element_local_pcg`` for the V3 projection (solvers.py:201-256
+    with op_local = apply_projection_operator(space, ., tau_d, None) and
+    prec_local = inverse_mass_apply): one CTA per cell runs its whole CG in
+    shared memory (dg_element_local_pcg).  b: velocity (dim components) as a
+    CUDA tensor (element-major) or numpy in the reference layout; tau_d: per
+    cell or None.  Returns (x, iterations per cell, converged per cell)."""
+    torch = _torch()
+    from .operators import _Arg
+    a = _Arg(space, b, space.dim)
+    x = a.new_out()
+    ne = space.mesh.n_elements
+    iters = torch.zeros(ne, dtype=torch.int32, device="cuda")
+    conv = torch.zeros(ne, dtype=torch.int32, device="cuda")
+    keep = None
+    td = ctypes_ptr(0)
+    if tau_d is not None:
+        keep = _to_dev(tau_d).contiguous().reshape(-1)
+        if keep.numel() != ne:
+            raise ValueError(f"tau_d needs one entry per cell ({ne})")
+        td = ctypes_ptr(keep.data_ptr())
+    ctx = space.ctx(space.default_kinds())
+    _lib.call("dg_element_local_pcg", ctx.handle, a.ptr(), ctypes_ptr(x.data_ptr()), td,
+              float(rel_tol), int(max_iter), float(floor_factor),
+              ctypes_ptr(iters.data_ptr()), ctypes_ptr(conv.data_ptr()), _stream())
+    del keep
+    return a.result(x), iters.cpu().numpy().astype(int), conv.cpu().numpy().astype(bool)

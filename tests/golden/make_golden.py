@@ -64,10 +64,33 @@ SETUPS = {
 }
 
 
-def make(name, k):
+# non-zero boundary data for the once-per-step right-hand sides
+# (operators.py:241-259, 494-527, 621-672); the same formulas live in
+# tests/golden_setups.py for the consumers of the fixture.
+def g_data(x, t):
+    return np.stack([np.sin(x[0] + t) * x[1], np.cos(2 * x[1]) - t * x[0]])
+
+
+def dgdt_data(x, t):
+    return np.stack([np.cos(x[0] + t) * x[1], -x[0] + 0 * x[1]])
+
+
+def h_data(x, t):
+    return np.stack([x[0] * x[1] + t, np.sin(3 * x[0]) - x[1]])
+
+
+def gp_data(x, t):
+    return np.cos(x[0] - 2 * x[1]) + t
+
+
+def make(name, k, data=False):
     ext, counts, grading, per, kinds = SETUPS[name]
     mesh = build_box_mesh(ext, counts, grading=grading, periodic=per)
-    spec = ops.BoundarySpec({t: (dirichlet_zero() if v == "D" else neumann_zero())
+    if data:
+        dbc, nbc = ops.DirichletBC(g_data, dgdt_data), ops.NeumannBC(h_data, gp_data)
+    else:
+        dbc, nbc = dirichlet_zero(), neumann_zero()
+    spec = ops.BoundarySpec({t: (dbc if v == "D" else nbc)
                              for t, v in kinds.items()})
     space = DgSpace(mesh, k)
     return space, spec.resolve(space)
@@ -152,6 +175,49 @@ def main():
                 space, bcs, [ur], (1.0,), (0.0,), 0.0))
             out[key + "_zm"] = em(space, sol.zero_mean_project(space, pr))
             out[key + "_zmd"] = em(space, sol.zero_mean_project_dual(space, pr))
+            # once-per-step right-hand sides (operators.py:241-366, 494-527,
+            # 610-672) with non-zero boundary data
+            _, bcd = make(name, k, data=True)
+            out[key + "_convd"] = em(space, ops.eval_convective_rhs(
+                space, bcd, [ur, u2r], (2.0, -1.0), (0.3, 0.2), 0.4,
+                body_force=body_force))
+            for form in ("standard", "weak", "strong"):
+                out[f"{key}_div_{form}"] = em(space, ops.eval_divergence_rhs(
+                    space, ur, bcd, 2.5, form))
+            for form in ("standard", "weak"):
+                out[f"{key}_grad_{form}"] = em(space, ops.eval_pressure_gradient_rhs(
+                    space, pr, bcd, 1.7, form))
+            w1 = ops.compute_vorticity(space, ur)
+            w2 = ops.compute_vorticity(space, u2r)
+            out[key + "_vort"] = em(space, w1)
+            out[key + "_pn"] = em(space, ops.eval_pressure_neumann_rhs(
+                space, bcd, [ur, u2r], [w1, w2], (2.0, -1.0), 0.025, 0.4,
+                body_force=body_force))
+            out[key + "_pn0"] = em(space, ops.eval_pressure_neumann_rhs(
+                space, bcs, [ur], [w1], (1.0,), 0.025, 0.4))
+            out[key + "_gp"] = em(space, ops.gp_dirichlet_rhs(space, bcd, 0.3))
+            out[key + "_gp75"] = em(space, ops.gp_dirichlet_rhs(space, bcd, 0.3, 7.5))
+            out[key + "_vrb"] = em(space, ops.viscous_rhs_bc(space, bcd, 0.3, 0.025))
+            # element-local PCG on the block-diagonal projection operator
+            # with inverse-mass preconditioning (solvers.py:201-256; the
+            # configuration of pkg/tests/test_solvers_multigrid.py:155-195)
+            # Per-cell counts of long local solves (k=5: ~40 iterations on
+            # 72 unknowns, well past the loss of orthogonality) move by +-2
+            # under a change of summation order (measured against a permuted
+            # restatement), so the fixture also holds a fixed 5-iteration
+            # run ("el5") whose iterate is compared exactly.
+            for tag, zeta, rtol, mit in (("el", None, 1e-8, 200), ("elx", 1e6, 1e-8, 200),
+                                         ("el12", None, 1e-12, 200),
+                                         ("el5", None, 1e-14, 5)):
+                td = np.full(ne, zeta) if zeta else tau_d * 10.0
+                x, iters, conv = sol.element_local_pcg(
+                    lambda w: ops.apply_projection_operator(space, w, td, None),
+                    lambda r: ops.inverse_mass_apply(space, r), ur, rel_tol=rtol,
+                    max_iter=mit)
+                out[f"{key}_{tag}_tau"] = td
+                out[f"{key}_{tag}_x"] = em(space, x)
+                out[f"{key}_{tag}_iters"] = iters
+                out[f"{key}_{tag}_conv"] = conv
 
     # solver histories (2D analogue of config 2): pure-Neumann periodic-x,
     # wall-y Poisson, Chebyshev(5, 20) over Jacobi with the MG level's

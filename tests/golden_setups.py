@@ -32,12 +32,59 @@ def relerr(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
 
 
-def oracle_setup(name, k):
+# non-zero boundary data of tests/golden/make_golden.py (2D)
+def g_data(x, t):
+    return np.stack([np.sin(x[0] + t) * x[1], np.cos(2 * x[1]) - t * x[0]])
+
+
+def dgdt_data(x, t):
+    return np.stack([np.cos(x[0] + t) * x[1], -x[0] + 0 * x[1]])
+
+
+def h_data(x, t):
+    return np.stack([x[0] * x[1] + t, np.sin(3 * x[0]) - x[1]])
+
+
+def gp_data(x, t):
+    return np.cos(x[0] - 2 * x[1]) + t
+
+
+# 3D analogues (no reference exists in 3D; used against the 3D oracle)
+def g_data3(x, t):
+    return np.stack([np.sin(x[0] + t) * x[1], np.cos(2 * x[1]) - t * x[2],
+                     x[0] * x[2] + 0.5])
+
+
+def dgdt_data3(x, t):
+    return np.stack([np.cos(x[0] + t) * x[1], -x[2] + 0 * x[1], np.sin(x[1] * x[2])])
+
+
+def h_data3(x, t):
+    return np.stack([x[0] * x[1] + t, np.sin(3 * x[0]) - x[2], x[1] - x[2] ** 2])
+
+
+def gp_data3(x, t):
+    return np.cos(x[0] - 2 * x[1] + x[2]) + t
+
+
+def body_force3(x, t):
+    return np.stack([np.sin(x[0]) + t, x[1] ** 2, np.cos(x[2]) * x[0]])
+
+
+def oracle_bcs(O, dim, data):
+    if not data:
+        return O.zero_dirichlet(dim), O.zero_neumann(dim)
+    if dim == 2:
+        return O.DirichletBC(g_data, dgdt_data), O.NeumannBC(h_data, gp_data)
+    return O.DirichletBC(g_data3, dgdt_data3), O.NeumannBC(h_data3, gp_data3)
+
+
+def oracle_setup(name, k, data=False):
     from oracle import dg_oracle as O
     ext, counts, grading, per, kinds = SETUPS[name]
     mesh = O.build_box_mesh(ext, counts, grading=grading, periodic=per)
-    spec = O.BoundarySpec({t: (O.zero_dirichlet(2) if v == "D" else O.zero_neumann(2))
-                           for t, v in kinds.items()})
+    dbc, nbc = oracle_bcs(O, 2, data)
+    spec = O.BoundarySpec({t: (dbc if v == "D" else nbc) for t, v in kinds.items()})
     space = O.DgSpace(mesh, k)
     return space, spec.resolve(space)
 

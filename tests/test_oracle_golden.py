@@ -103,3 +103,64 @@ def test_solver_histories_match_reference(k, nx):
         n = len(ref_hist) if pname == "cheb" else 60
         np.testing.assert_allclose(got[:n], ref_hist[:n], rtol=1e-9)
         assert relerr(flat(x), Z[f"{key}_{pname}_x"]) < 1e-9
+
+
+@pytest.mark.parametrize("name", list(SETUPS))
+@pytest.mark.parametrize("k", KS)
+def test_step_rhs_match_reference(name, k):
+    """Once-per-step right-hand sides (operators.py:241-366, 494-527,
+    610-672) with non-zero boundary data."""
+    space, bcs = oracle_setup(name, k)
+    _, bcd = oracle_setup(name, k, data=True)
+    key = f"{name}_k{k}"
+    p = Z[key + "_p"].reshape(space.field_shape())
+    u = Z[key + "_u"].reshape(space.field_shape(2))
+    u2 = Z[key + "_u2"].reshape(space.field_shape(2))
+    w1 = O.compute_vorticity(space, u)
+    w2 = O.compute_vorticity(space, u2)
+    checks = {"_vort": w1,
+              "_convd": O.eval_convective_rhs(space, bcd, [u, u2], (2.0, -1.0), (0.3, 0.2),
+                                              0.4, body_force=body_force)}
+    for form in ("standard", "weak", "strong"):
+        checks[f"_div_{form}"] = O.eval_divergence_rhs(space, u, bcd, 2.5, form)
+    for form in ("standard", "weak"):
+        checks[f"_grad_{form}"] = O.eval_pressure_gradient_rhs(space, p, bcd, 1.7, form)
+    checks["_pn"] = O.eval_pressure_neumann_rhs(space, bcd, [u, u2], [w1, w2],
+                                                (2.0, -1.0), 0.025, 0.4,
+                                                body_force=body_force)
+    checks["_pn0"] = O.eval_pressure_neumann_rhs(space, bcs, [u], [w1], (1.0,),
+                                                 0.025, 0.4)
+    checks["_gp"] = O.gp_dirichlet_rhs(space, bcd, 0.3)
+    checks["_gp75"] = O.gp_dirichlet_rhs(space, bcd, 0.3, 7.5)
+    checks["_vrb"] = O.viscous_rhs_bc(space, bcd, 0.3, 0.025)
+    for suffix, got in checks.items():
+        want = Z[key + suffix]
+        if np.linalg.norm(want) == 0.0:
+            assert np.linalg.norm(flat(got)) == 0.0, suffix
+            continue
+        err = relerr(flat(got), want)
+        assert err < TOL, (suffix, err)
+
+
+@pytest.mark.parametrize("name", list(SETUPS))
+@pytest.mark.parametrize("k", KS)
+def test_element_local_pcg_matches_reference(name, k):
+    """Per-cell CG on M + tau_D div-div with inverse-mass preconditioning:
+    identical per-cell iteration counts (solvers.py:201-256)."""
+    space, _ = oracle_setup(name, k)
+    key = f"{name}_k{k}"
+    u = Z[key + "_u"].reshape(space.field_shape(2))
+    for tag, rtol, mit in (("el", 1e-8, 200), ("elx", 1e-8, 200),
+                           ("el12", 1e-12, 200), ("el5", 1e-14, 5)):
+        td = Z[f"{key}_{tag}_tau"]
+        x, iters, conv = O.element_local_pcg(
+            lambda w: O.apply_projection_operator(space, w, td, None),
+            lambda r: O.inverse_mass_apply(space, r), u, rel_tol=rtol, max_iter=mit)
+        want = Z[f"{key}_{tag}_iters"]
+        np.testing.assert_array_equal(conv, Z[f"{key}_{tag}_conv"])
+        if tag == "el5":    # fixed iteration count: the iterate itself agrees
+            np.testing.assert_array_equal(iters, want)
+            assert relerr(flat(x), Z[f"{key}_{tag}_x"]) < 1e-12
+        else:               # converged solves: counts to +-2 (see make_golden)
+            assert np.abs(iters - want).max() <= 2, (tag, iters, want)
+            assert relerr(flat(x), Z[f"{key}_{tag}_x"]) < (1e-10 if tag == "el12" else 1e-6)
