@@ -113,15 +113,15 @@ def hbm_peak():
         return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(k):
-    """DRAM bytes per launch of laplace_vmult_kernel from the committed ncu
-    --set full summary (profiles/ncu_laplace.json), or None."""
+def ncu_summary(k):
+    """Committed ncu --set full summary of the headline vmult kernel at degree
+    k (profiles/ncu_laplace.json): kernel name, DRAM bytes per launch, fp64
+    instruction counts per DoF; {} if absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_laplace.json")) as f:
-            d = json.load(f)
-        return d.get(f"k{k}", {}).get("dram_bytes_per_launch")
+            return json.load(f).get(f"k{k}", {})
     except Exception:
-        return None
+        return {}
 
 
 def oracle_sample(k, cells, threads_all):
@@ -327,10 +327,12 @@ def main():
         per_rank_dofs = nd
         achieved = per_rank_dofs * BYTES_PER_DOF / (ms_step * 1e-3) / 1e9
         clocks = clk.summary()
+        prof = ncu_summary(k)
         fma = FMA_PER_DOF.get(k + 1)
+        flop = prof.get("flop_per_dof") or (2 * fma if fma else None)
         sm_mhz = clocks["sm_mhz"] or 1965.0
         fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
-        fp64_ach = per_rank_dofs * 2 * fma / (ms_step * 1e-3) / 1e12 if fma else None
+        fp64_ach = per_rank_dofs * flop / (ms_step * 1e-3) / 1e12 if flop else None
         line = {
             "metric": "SIP Laplace vmult DoF/s (fp64)",
             "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
@@ -343,13 +345,17 @@ def main():
                        "cells": n, "k": k, "dofs": total, "parallelism": f"x-slabs{world}",
                        "l2": "inputs (8 B/DoF x dofs) larger than L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(k),
+                         "frac": achieved / peak,
+                         "traffic": prof.get("dram_bytes_per_launch") if n == 128 else None,
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_dof": BYTES_PER_DOF,
-                         "kernel": "laplace_vmult_kernel"},
-            "fp64": {"fma_per_dof": fma, "achieved_tflops": fp64_ach,
+                         "kernel": prof.get("kernel", "laplace_vmult_kernel")},
+            "fp64": {"flop_per_dof": flop,
+                     "flop_source": ("ncu sass dfma/dadd/dmul counts (profiles/ncu_laplace.json)"
+                                     if prof.get("flop_per_dof") else "model 2 x (7n + 18)"),
+                     "achieved_tflops": fp64_ach,
                      "peak_tflops_at_clock": fp64_peak,
-                     "frac": (fp64_ach / fp64_peak) if fma else None,
+                     "frac": (fp64_ach / fp64_peak) if flop else None,
                      "peak_kind": "nominal 64 DFMA/clk/SM x 148 SMs x median SM clock"},
             "gpu_launches": args.steps * (1 if world == 1 else 2),
             "clocks": clocks,

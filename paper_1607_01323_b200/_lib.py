@@ -28,6 +28,17 @@ def sources():
     return [os.path.join(CSRC, f) for f in names]
 
 
+def _up_to_date(obj):
+    """Object newer than its source and every header nvcc listed for it."""
+    dep = obj + ".d"
+    if not (os.path.exists(obj) and os.path.exists(dep)):
+        return False
+    text = open(dep).read().replace("\\\n", " ")
+    files = text.split(":", 1)[1].split() if ":" in text else []
+    t = os.path.getmtime(obj)
+    return all(os.path.exists(f) and os.path.getmtime(f) <= t for f in files)
+
+
 def build(verbose=False, force=False):
     """Compile libdgmf.so for sm_100a with nvcc (in-tree, travels with the repo).
     One nvcc per translation unit, run in parallel, then one link."""
@@ -43,11 +54,13 @@ def build(verbose=False, force=False):
     procs, objs = [], []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc] + compile_flags + ["-c", "-o", obj, src]
+        objs.append(obj)
+        if not force and _up_to_date(obj):
+            continue
+        cmd = [nvcc] + compile_flags + ["-MD", "-MF", obj + ".d", "-c", "-o", obj, src]
         if verbose:
             print(" ".join(cmd))
         procs.append((subprocess.Popen(cmd, cwd=HERE), src))
-        objs.append(obj)
     failed = [src for p, src in procs if p.wait() != 0]
     if failed:
         raise subprocess.CalledProcessError(1, f"nvcc {failed}")

@@ -38,11 +38,13 @@ enum SideMode : int {
 struct Geo {
   int nx, ny, nz;            // owned cells per axis (nz = 1 in 2D)
   const double *hx, *hy, *hz;  // cell sizes per axis index (owned)
+  const double *hxi, *hyi, *hzi;  // their inverses (host-computed: no divisions in kernels)
   const double *tau;         // tau_e per owned cell (Eq. 18)
   int mode[6];
   const double *ghost[2];    // x-ghost layers (ny*nz cells each) or null
   const double *ghost_tau[2];
   double ghost_h[2];
+  double ghost_hi[2];
   int exp_flags;             // timing experiments (DG_EXP env); 0 in production
 };
 

@@ -28,6 +28,7 @@ struct dg_ctx {
   double ghost_h[2] = {1.0, 1.0};
   std::vector<double> ghost_tau_h[2];
   double *d_hx = nullptr, *d_hy = nullptr, *d_hz = nullptr, *d_tau = nullptr;
+  double *d_hinv = nullptr;  // [1/hx | 1/hy | 1/hz]
   double *d_ghost_tau[2] = {nullptr, nullptr};
   const double *d_recv[2] = {nullptr, nullptr};  // caller-owned ghost layers
   int64_t halo_count = 0;
@@ -50,11 +51,15 @@ struct dg_ctx {
     g.hy = d_hy;
     g.hz = d_hz;
     g.tau = d_tau;
+    g.hxi = d_hinv;
+    g.hyi = d_hinv ? d_hinv + counts[0] : nullptr;
+    g.hzi = d_hinv ? d_hinv + counts[0] + counts[1] : nullptr;
     for (int i = 0; i < 6; ++i) g.mode[i] = mode[i];
     for (int s = 0; s < 2; ++s) {
       g.ghost[s] = d_recv[s];
       g.ghost_tau[s] = d_ghost_tau[s];
       g.ghost_h[s] = ghost_h[s];
+      g.ghost_hi[s] = 1.0 / ghost_h[s];
     }
     static const int exp_flags = [] {
       const char *v = getenv("DG_EXP");

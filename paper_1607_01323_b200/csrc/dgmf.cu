@@ -9,6 +9,7 @@
 #include "common.cuh"
 #include "ctx.h"
 #include "laplace.cuh"
+#include "laplace6.cuh"
 #include "laplace_persist.cuh"
 #include "laplace_warp.cuh"
 #include "tables.h"
@@ -194,6 +195,13 @@ int dg_ctx_create(const dg_mesh_desc *desc, dg_ctx **out) {
   if ((rc = upload(&c->d_hx, c->hx))) goto fail;
   if ((rc = upload(&c->d_hy, c->hy))) goto fail;
   if ((rc = upload(&c->d_hz, c->hz))) goto fail;
+  {
+    std::vector<double> hinv;
+    for (double h : c->hx) hinv.push_back(1.0 / h);
+    for (double h : c->hy) hinv.push_back(1.0 / h);
+    for (double h : c->hz) hinv.push_back(1.0 / h);
+    if ((rc = upload(&c->d_hinv, hinv))) goto fail;
+  }
   if ((rc = upload(&c->d_tau, c->tau))) goto fail;
   if (cudaMalloc((void **)&c->d_red, sizeof(double) * (kRedBlocks + 64)) != cudaSuccess) goto cfail;
   if (cudaMalloc((void **)&c->d_scal, sizeof(double) * 32) != cudaSuccess) goto cfail;
@@ -213,6 +221,7 @@ int dg_ctx_destroy(dg_ctx *c) {
   cudaFree(c->d_hx);
   cudaFree(c->d_hy);
   cudaFree(c->d_hz);
+  cudaFree(c->d_hinv);
   cudaFree(c->d_tau);
   for (int s = 0; s < 2; ++s) {
     cudaFree(c->d_ghost_tau[s]);
@@ -308,6 +317,10 @@ static int64_t laplace_bricks(const dg_ctx *c) {
          ((c->counts[2] + bz - 1) / bz);
 }
 
+template <int N, int BX, int BY, int BZ, int EPI = kEpiStore>
+static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
+                           cudaStream_t st, const EpiArgs &ea = EpiArgs{});
+
 // fused-epilogue vmults for the CG / Chebyshev loop (default bricks, k = 2..5)
 static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, double tau_scale,
                                 int epi, const EpiArgs &ea, cudaStream_t st) {
@@ -316,6 +329,8 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
     if (epi == kEpiCheb) return launch_laplace<D, NN, X, Y, Z, kEpiCheb>(c, src, dst, tau_scale, 0, st, ea); \
     if (epi == kEpiDot) return launch_laplace<D, NN, X, Y, Z, kEpiDot>(c, src, dst, tau_scale, 0, st, ea);   \
   }
+  // v4 bricks here also for k = 4: its 416-thread CTAs stream the CG vectors of
+  // the epilogue faster than the 96-thread register-plane CTAs
   DG_E(3, 3, 4, 4, 4) DG_E(3, 4, 4, 4, 2) DG_E(3, 5, 4, 2, 2) DG_E(3, 6, 2, 2, 2)
   DG_E(2, 3, 16, 8, 1) DG_E(2, 4, 16, 8, 1) DG_E(2, 5, 8, 8, 1) DG_E(2, 6, 8, 8, 1)
 #undef DG_E
@@ -361,12 +376,51 @@ static int launch_laplace_warp(dg_ctx *c, const double *src, double *dst, double
   return DG_OK;
 }
 
+template <int N, int BX, int BY, int BZ, int EPI>
+static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
+                           cudaStream_t st, const EpiArgs &ea) {
+  using C = Lap6Cfg<N, BX, BY, BZ>;
+  auto kern = laplace6_kernel<N, BX, BY, BZ, EPI>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  const Geo g = c->geo();
+  const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, (g.nz + BZ - 1) / BZ);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part, ea);
+  DG_LAUNCH_CHECK("laplace6_kernel");
+  return DG_OK;
+}
+
 static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                             cudaStream_t st) {
   static const int variant = [] {
     const char *v = getenv("DG_LAP_VARIANT");  // brick-shape experiments
     return v ? atoi(v) : 0;
   }();
+  static const int brick6 = [] {
+    const char *v = getenv("DG_LAP6_BRICK");
+    return v ? atoi(v) : 0;
+  }();
+  if (c->dim == 3 && variant == 6) {  // register-plane kernel (laplace6.cuh)
+    if (c->n == 5) {
+      if (brick6 == 1) return launch_laplace6<5, 2, 2, 2>(c, src, dst, tau_scale, part, st);
+      if (brick6 == 2) return launch_laplace6<5, 4, 4, 2>(c, src, dst, tau_scale, part, st);
+      if (brick6 == 3) return launch_laplace6<5, 8, 2, 2>(c, src, dst, tau_scale, part, st);
+      return launch_laplace6<5, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+    }
+    if (c->n == 4) {
+      if (brick6 == 1) return launch_laplace6<4, 2, 2, 2>(c, src, dst, tau_scale, part, st);
+      if (brick6 == 2) return launch_laplace6<4, 4, 4, 2>(c, src, dst, tau_scale, part, st);
+      return launch_laplace6<4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+    }
+    if (c->n == 3) {
+      if (brick6 == 1) return launch_laplace6<3, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+      if (brick6 == 2) return launch_laplace6<3, 4, 4, 4>(c, src, dst, tau_scale, part, st);
+      return launch_laplace6<3, 4, 4, 2>(c, src, dst, tau_scale, part, st);
+    }
+  }
   if (c->dim == 3 && part == 0 && variant == 30) {  // persistent pipelined
     if (c->n == 5) return launch_laplace_persist<5, 4, 2, 2>(c, src, dst, tau_scale, st);
     if (c->n == 3) return launch_laplace_persist<3, 4, 4, 4>(c, src, dst, tau_scale, st);
@@ -387,7 +441,9 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
       case 2: return launch_laplace<3, 2, 8, 4, 4>(c, src, dst, tau_scale, part, st);
       case 3: return launch_laplace<3, 3, 4, 4, 4>(c, src, dst, tau_scale, part, st);
       case 4: return launch_laplace<3, 4, 4, 4, 2>(c, src, dst, tau_scale, part, st);
-      case 5: return launch_laplace<3, 5, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+      case 5:
+        if (variant == 4) return launch_laplace<3, 5, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+        return launch_laplace6<5, 4, 2, 2>(c, src, dst, tau_scale, part, st);
       case 6: return launch_laplace<3, 6, 2, 2, 2>(c, src, dst, tau_scale, part, st);
       case 7: return launch_laplace<3, 7, 2, 2, 2>(c, src, dst, tau_scale, part, st);
       case 8: return launch_laplace<3, 8, 2, 2, 2>(c, src, dst, tau_scale, part, st);

@@ -46,6 +46,7 @@ struct NbrInfo {
   int kind;           // 0 in-brick, 1 halo, 2 boundary none, 3 boundary neumann
   int cb;             // in-brick cell index
   double h;           // neighbour size in the face-normal direction
+  double hi;          // its inverse
   double tau;         // neighbour tau_e
   const double *src;  // halo: neighbour cell data (global)
 };
@@ -60,6 +61,7 @@ __device__ __forceinline__ NbrInfo resolve_nbr(const Geo &g, const double *u, in
   r.cb = 0;
   r.src = nullptr;
   r.h = 1.0;
+  r.hi = 1.0;
   r.tau = 0.0;
   const int nd = D == 0 ? g.nx : D == 1 ? g.ny : g.nz;
   const int cd = D == 0 ? ix : D == 1 ? iy : iz;
@@ -73,6 +75,7 @@ __device__ __forceinline__ NbrInfo resolve_nbr(const Geo &g, const double *u, in
       r.kind = 1;
       r.src = g.ghost[S] + (size_t)t * NP;
       r.h = g.ghost_h[S];
+      r.hi = g.ghost_hi[S];
       r.tau = g.ghost_tau[S][t];
       return r;
     } else {
@@ -83,6 +86,7 @@ __device__ __forceinline__ NbrInfo resolve_nbr(const Geo &g, const double *u, in
   const int cx = D == 0 ? nc : ix, cy = D == 1 ? nc : iy, cz = D == 2 ? nc : iz;
   const size_t e = (size_t)cx + (size_t)g.nx * (cy + (size_t)g.ny * cz);
   r.h = (D == 0) ? g.hx[cx] : (D == 1) ? g.hy[cy] : g.hz[cz];
+  r.hi = (D == 0) ? g.hxi[cx] : (D == 1) ? g.hyi[cy] : g.hzi[cz];
   r.tau = g.tau[e];
   const int lo = D == 0 ? x0 : D == 1 ? y0 : z0;
   const int ext = D == 0 ? ex : D == 1 ? ey : ez;
