@@ -200,6 +200,34 @@ int dg_laplace_pcg(dg_ctx *ctx, const double *b, double *x,
                    const double *diag, const dg_pcg_params *prm,
                    dg_pcg_stats *stats, double *hist_host, void *stream);
 
+/* ---- geometric multigrid (multigrid.py:33-151, mesh.py:354-374) ---------
+ * Levels are contexts of nested boxes (counts doubling per axis, same dim,
+ * degree, periodicity and boundary kinds), coarse (0) to fine. */
+typedef struct dg_mg dg_mg;
+/* Transfer.prolong (multigrid.py:49-58): xf (+)= E xc (add != 0 accumulates);
+ * Transfer.restrict (multigrid.py:60-69): xc = E^T xf */
+int dg_mg_prolong(dg_ctx *coarse, dg_ctx *fine, const double *xc, double *xf,
+                  int add, void *stream);
+int dg_mg_restrict(dg_ctx *fine, dg_ctx *coarse, const double *xf, double *xc,
+                   void *stream);
+/* MultigridHierarchy (multigrid.py:76-128): per-level Jacobi diagonals
+ * (device, caller-owned, kept alive) and Chebyshev lambda_max (the
+ * reference's safety * Lanczos estimate, computed by the caller from its
+ * seeded start vectors); smoother Chebyshev(degree, smoothing_range) over
+ * Jacobi; coarsest level Chebyshev(coarse_iters, coarse_range). */
+int dg_mg_create(dg_ctx *const *levels, int n_levels, const double *const *diag,
+                 const double *lambda_max, int degree, double smoothing_range,
+                 int coarse_iters, double coarse_range, double tau_scale,
+                 dg_mg **out);
+int dg_mg_destroy(dg_mg *mg);
+/* MultigridHierarchy.vcycle (multigrid.py:133-151): x = V(b), finest level */
+int dg_mg_vcycle(dg_mg *mg, const double *b, double *x, void *stream);
+/* dg_laplace_pcg with the V-cycle as preconditioner (prm->cheb_* unused);
+ * ctx must be the hierarchy's finest level */
+int dg_laplace_pcg_mg(dg_ctx *ctx, dg_mg *mg, const double *b, double *x,
+                      const dg_pcg_params *prm, dg_pcg_stats *stats,
+                      double *hist_host, void *stream);
+
 /* ---- multi-GPU x-slabs (ghost cell layers) ------------------------------ */
 /* doubles in one ghost layer: ny*nz cells of one component (n^dim each),
  * ordered by (iz, iy) -- the size of every send/recv buffer below */

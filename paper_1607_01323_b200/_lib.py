@@ -124,6 +124,13 @@ PROTOTYPES = {
     "dg_zero_mean": [_P, _P, _P],
     "dg_laplace_pcg": [_P, _P, _P, _P, ctypes.POINTER(PcgParams),
                        ctypes.POINTER(PcgStats), _DP, _P],
+    "dg_laplace_pcg_mg": [_P, _P, _P, _P, ctypes.POINTER(PcgParams),
+                          ctypes.POINTER(PcgStats), _DP, _P],
+    "dg_mg_prolong": [_P, _P, _P, _P, _I, _P],
+    "dg_mg_restrict": [_P, _P, _P, _P, _P],
+    "dg_mg_create": [_P, _I, _P, _P, _I, _D, _I, _D, _D, ctypes.POINTER(_P)],
+    "dg_mg_destroy": [_P],
+    "dg_mg_vcycle": [_P, _P, _P, _P],
     "dg_halo_count": [_P, ctypes.POINTER(_L)],
     "dg_halo_pack": [_P, _P, _P, _P, _P],
     "dg_halo_attach": [_P, _P, _P],

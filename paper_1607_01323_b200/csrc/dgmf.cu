@@ -12,6 +12,7 @@
 #include "laplace6.cuh"
 #include "laplace_persist.cuh"
 #include "laplace_warp.cuh"
+#include "mg.cuh"
 #include "tables.h"
 #include "tensor.cuh"
 #include "tensor_fast.cuh"

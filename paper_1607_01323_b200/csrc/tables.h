@@ -15,5 +15,8 @@ struct Basis1D {
 void gauss_rule(int n, std::vector<double> &pts, std::vector<double> &wts);
 void gll_nodes(int k, std::vector<double> &nodes);
 void basis_tables(int k, int nq, Basis1D &b);
+// V[q][i] = l_i(x_q), Dv[q][i] = l_i'(x_q) for the Lagrange basis on nodes
+void lagrange_tables(const std::vector<double> &nodes, const std::vector<double> &x,
+                     std::vector<double> &V, std::vector<double> &Dv);
 
 }  // namespace dg
