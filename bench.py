@@ -221,11 +221,31 @@ def run_cg(dist_on):
                             rel_tol=1e-10, max_iter=5000)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    return {"config": "C2: 32^3 Q4 periodic x,z / walls y, Chebyshev(5,20)-Jacobi PCG, rel_tol 1e-10",
-            "dofs": space.n_dofs, "iterations": st.iterations, "converged": st.converged,
-            "solve_ms": 1e3 * dt, "ms_per_iteration": 1e3 * dt / max(st.iterations, 1),
-            "dof_per_s_per_iteration": space.n_dofs * st.iterations / dt,
-            "lambda_max": lmax}
+    out = {"config": "C2: 32^3 Q4 periodic x,z / walls y, Chebyshev(5,20)-Jacobi PCG, rel_tol 1e-10",
+           "dofs": space.n_dofs, "iterations": st.iterations, "converged": st.converged,
+           "solve_ms": 1e3 * dt, "ms_per_iteration": 1e3 * dt / max(st.iterations, 1),
+           "dof_per_s_per_iteration": space.n_dofs * st.iterations / dt,
+           "lambda_max": lmax}
+    # the reference's actual Poisson preconditioner: geometric multigrid
+    # V-cycle (multigrid.py), levels 4^3 .. 32^3, same right-hand side
+    from paper_1607_01323_b200 import multigrid as MG
+    meshes = MG.box_mesh_hierarchy(((0, 1),) * 3, (4, 4, 4), 3, periodic=(True, False, True))
+    spaces = [DgSpace(m, 4) for m in meshes]
+    spec = ops.BoundarySpec({"ymin": ops.DirichletBC(None), "ymax": ops.DirichletBC(None)})
+    mg = MG.MultigridHierarchy(spaces, spec, project=sol.zero_mean_project)
+    bb = b.reshape(-1)
+    MG.laplace_pcg_mg(mg, bb, project_dual=True, rel_tol=1e-10, max_iter=3)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    xm, stm = MG.laplace_pcg_mg(mg, bb, project_dual=True, rel_tol=1e-10, max_iter=200)
+    torch.cuda.synchronize()
+    dtm = time.perf_counter() - t0
+    out["multigrid"] = {"levels": mg.n_levels, "coarse_iters": mg.levels[0].coarse_iters,
+                        "iterations": stm.iterations, "converged": stm.converged,
+                        "solve_ms": 1e3 * dtm,
+                        "rel_diff_vs_chebyshev": float((xm.reshape(-1) - x.reshape(-1)).norm()
+                                                       / x.reshape(-1).norm())}
+    return out
 
 
 def main():
