@@ -138,7 +138,7 @@ __device__ __forceinline__ int face_node(int d, int sl, int fa, int k) {
 // over the FQ face points [slow][fast] (kernels.py:119-156).
 template <int DIM, int N, int NQ>
 __device__ void face_traces(const double *cell, int ncomp, int d, int s, const double h[3],
-                            double *dst, const FaceScratch &F) {
+                            double *dst, const FaceScratch &F, bool need_grad = true) {
   constexpr int NP = DIM == 3 ? N * N * N : N * N;
   constexpr int FQ = DIM == 3 ? NQ * NQ : NQ;
   constexpr int FN = DIM == 3 ? N * N : N;
@@ -157,6 +157,15 @@ __device__ void face_traces(const double *cell, int ncomp, int d, int s, const d
     }
     __syncthreads();
     double *dv = dst + (c * (1 + DIM)) * FQ;
+    if (!need_grad) {  // values only (convective, projection, divergence, gradient)
+      if (DIM == 3) {
+        contract(F.ft, F.t0, F.S, NQ, N, 0, N, N, 1);
+        contract(F.t0, dv, F.S, NQ, N, 1, NQ, N, 1);
+      } else {
+        contract(F.ft, dv, F.S, NQ, N, 0, N, 1, 1);
+      }
+      continue;
+    }
     if (DIM == 3) {
       contract(F.ft, F.t0, F.S, NQ, N, 0, N, N, 1);
       contract(F.t0, dv, F.S, NQ, N, 1, NQ, N, 1);                          // value
@@ -554,12 +563,13 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
           load(src, NCI, en, snb);
         }
         __syncthreads();
-        face_traces<DIM, N, NQ>(su, NCI, d, s, h, fo, F);
+        const bool tgrad = op == kOpHelmholtz;  // only the viscous flux needs face gradients
+        face_traces<DIM, N, NQ>(su, NCI, d, s, h, fo, F, tgrad);
         if (kind == 0) {
           // traces scale by 2/h[b]; the neighbour differs only along d
           const double hsave = h[d];
           h[d] = hn;
-          face_traces<DIM, N, NQ>(snb, NCI, d, 1 - s, h, fb, F);
+          face_traces<DIM, N, NQ>(snb, NCI, d, 1 - s, h, fb, F, tgrad);
           h[d] = hsave;
         }
         const double fdet = face_det(d);
