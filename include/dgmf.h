@@ -166,6 +166,15 @@ int dg_element_local_pcg(dg_ctx *ctx, const double *b, double *x,
                          double floor_factor, int *iters, int *converged,
                          void *stream);
 
+/* compute_penalty_parameters(space, u, dt, cfl, cfg)  operators.py:736-755:
+ * tau_D per cell = zeta_d_star/cfl |u_mean| V^(1/dim) dt (tau_d NULL: skip);
+ * tau_C per face = average of zeta_c_star/cfl |u_mean| dt of the two cells,
+ * in the face layout of dg_projection_vmult (tau_c NULL: skip).  u: dim
+ * components. */
+int dg_penalty_parameters(dg_ctx *ctx, const double *u, double dt, double cfl,
+                          double zeta_d_star, double zeta_c_star, double *tau_d,
+                          double *tau_c, void *stream);
+
 /* ---- vector kernels for the solvers (solvers.py) ------------------------ */
 /* deterministic fixed-order dot product; result written to device *out */
 int dg_dot(dg_ctx *ctx, const double *x, const double *y, int64_t n,

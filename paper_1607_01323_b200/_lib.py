@@ -119,6 +119,7 @@ PROTOTYPES = {
     "dg_gp_dirichlet_rhs": [_P, _P, _D, _P, _P],
     "dg_viscous_rhs_bc": [_P, _P, _D, _P, _P],
     "dg_element_local_pcg": [_P, _P, _P, _P, _D, _I, _D, _P, _P, _P],
+    "dg_penalty_parameters": [_P, _P, _D, _D, _D, _D, _P, _P, _P],
     "dg_dot": [_P, _P, _P, _L, _P, _P],
     "dg_zero_mean_dual": [_P, _P, _P],
     "dg_zero_mean": [_P, _P, _P],

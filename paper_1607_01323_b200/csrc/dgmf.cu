@@ -757,3 +757,85 @@ int dg_laplace_diagonal(dg_ctx *c, double *diag, double tau_scale, void *stream)
 
 // The quadrature-point operators (Helmholtz, projection, convective, the
 // once-per-step right-hand sides, element-local PCG) are in vecops.cu.
+
+// compute_penalty_parameters (operators.py:736-755): one warp per cell forms
+// the cell integrals of the velocity components (sum_i u_i w_i with the
+// dual weights), |u_mean| = |integral| / V, tau_D = zd |u_mean| V^(1/dim) dt,
+// tau_C,e = zc |u_mean| dt; pass 2 averages tau_C,e onto faces.
+__global__ void penalty_cell_kernel(const double *__restrict__ u, Geo g, int dim, int nn, WInt wi,
+                                    int64_t ncells, double dt, double zd, double zc,
+                                    double *__restrict__ tau_d, double *__restrict__ tau_ce) {
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= ncells) return;
+  const int64_t np = (dim == 3) ? (int64_t)nn * nn * nn : (int64_t)nn * nn;
+  double m[3] = {0.0, 0.0, 0.0};
+  for (int c = 0; c < dim; ++c) {
+    double acc = 0.0;
+    for (int64_t o = lane; o < np; o += 32) {
+      const int64_t i = e * np + o;
+      acc += u[(int64_t)c * ncells * np + i] * dual_weight(g, dim, nn, wi, i);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    m[c] = acc;
+  }
+  if (lane != 0) return;
+  const int ix = (int)(e % g.nx), iy = (int)((e / g.nx) % g.ny), iz = (int)(e / ((int64_t)g.nx * g.ny));
+  double vol = g.hx[ix] * g.hy[iy];
+  if (dim == 3) vol *= g.hz[iz];
+  const double norm = sqrt(m[0] * m[0] + m[1] * m[1] + m[2] * m[2]) / vol;
+  if (tau_d) tau_d[e] = zd * norm * pow(vol, 1.0 / dim) * dt;
+  if (tau_ce) tau_ce[e] = zc * norm * dt;
+}
+
+// tau_C face layout [d*ncells + e]: face between cell e and its +d neighbour
+// (periodic wrap included; 0 where there is no face)
+__global__ void penalty_face_kernel(const double *__restrict__ tau_ce, Geo g, int dim,
+                                    int64_t ncells, double *__restrict__ tau_c) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= dim * ncells) return;
+  const int d = (int)(i / ncells);
+  const int64_t e = i - (int64_t)d * ncells;
+  int idx[3];
+  idx[0] = (int)(e % g.nx);
+  idx[1] = (int)((e / g.nx) % g.ny);
+  idx[2] = (int)(e / ((int64_t)g.nx * g.ny));
+  const int nd = d == 0 ? g.nx : (d == 1 ? g.ny : g.nz);
+  int nb = idx[d] + 1;
+  if (nb >= nd) {
+    if (g.mode[2 * d + 1] != kWrap) {
+      tau_c[i] = 0.0;
+      return;
+    }
+    nb = 0;
+  }
+  idx[d] = nb;
+  const int64_t en = idx[0] + (int64_t)g.nx * (idx[1] + (int64_t)g.ny * idx[2]);
+  tau_c[i] = 0.5 * (tau_ce[e] + tau_ce[en]);
+}
+
+extern "C" int dg_penalty_parameters(dg_ctx *c, const double *u, double dt, double cfl, double zeta_d_star,
+                          double zeta_c_star, double *tau_d, double *tau_c, void *stream) {
+  if (!c || !u) return inval("null argument");
+  if (!(cfl > 0.0)) return inval("CFL must be positive, got " + std::to_string(cfl));
+  if (c->mode[0] == kGhost || c->mode[1] == kGhost)
+    return inval("penalty parameters run on whole-mesh contexts");
+  const cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_work(c, 1);
+  if (rc) return rc;
+  double *tce = tau_c ? c->work[0] : nullptr;  // per-cell tau_C (n_cells <= n_dofs)
+  const int64_t nc = c->n_cells;
+  if (nc == 0) return DG_OK;
+  penalty_cell_kernel<<<(unsigned)((nc * 32 + 255) / 256), 256, 0, st>>>(
+      u, c->geo(), c->dim, c->n, wint_of(c), nc, dt, zeta_d_star / cfl, zeta_c_star / cfl, tau_d,
+      tce);
+  DG_LAUNCH_CHECK("penalty_cell_kernel");
+  if (tau_c) {
+    penalty_face_kernel<<<(unsigned)((c->dim * nc + 255) / 256), 256, 0, st>>>(tce, c->geo(),
+                                                                               c->dim, nc, tau_c);
+    DG_LAUNCH_CHECK("penalty_face_kernel");
+  }
+  return DG_OK;
+}
+

@@ -527,3 +527,66 @@ def eval_pressure_neumann_rhs(space: DgSpace, bcs: ResolvedBCs, history, vortici
 
 
 
+
+
+# ---------------------------------------------------------------------------
+# stabilisation variants and penalty parameters (operators.py:28-75, 736-755)
+
+VARIANTS = ("VHW", "V1", "V2", "V3a", "V3b", "V3c", "V4")
+
+
+@dataclass
+class VariantConfig:
+    """Stabilisation variant selector and penalty factors (operators.py:31-75)."""
+    variant: str = "V3c"
+    zeta_d_star: float = 1.0
+    zeta_c_star: float = 1.0
+    dt_ref: Optional[float] = None
+
+    def __post_init__(self):
+        if self.variant not in VARIANTS:
+            raise ValueError(f"unknown variant {self.variant!r}")
+        if self.zeta_d_star < 0 or self.zeta_c_star < 0:
+            raise ValueError("penalty factors must be >= 0")
+        if self.variant == "V1" and not (self.dt_ref and self.dt_ref > 0):
+            raise ValueError("V1 needs a positive reference time step dt_ref")
+
+    @property
+    def uses_divdiv(self) -> bool:
+        return self.variant in ("V3a", "V3b", "V3c", "V4")
+
+    @property
+    def uses_jump(self) -> bool:
+        return self.variant == "V4"
+
+    @property
+    def a_form(self) -> str:
+        return "weak" if self.variant in ("V3b", "V3c") else "standard"
+
+    @property
+    def b_form(self) -> str:
+        return "weak" if self.variant == "V3c" else "standard"
+
+    @property
+    def local_projection(self) -> bool:
+        return not self.uses_jump
+
+
+def compute_penalty_parameters(space: DgSpace, u, dt: float, cfl: float, cfg: VariantConfig):
+    """tau_D per cell and tau_C per face from the cell-mean velocity
+    (operators.py:736-755; h = V^(1/dim)).  Returns device tensors (tau_c in
+    the face layout apply_projection_operator accepts) or None where the
+    variant has no such term."""
+    if cfl <= 0:
+        raise ValueError(f"CFL must be positive, got {cfl}")
+    torch = _torch()
+    a = _Arg(space, u, space.dim)
+    ne = space.mesh.n_elements
+    td = torch.empty(ne, dtype=torch.float64, device="cuda") if cfg.uses_divdiv else None
+    tc = torch.empty(space.dim * ne, dtype=torch.float64, device="cuda") if cfg.uses_jump else None
+    ctx = space.ctx(space.default_kinds())
+    _lib.call("dg_penalty_parameters", ctx.handle, a.ptr(), float(dt), float(cfl),
+              float(cfg.zeta_d_star), float(cfg.zeta_c_star),
+              ctypes_ptr(td.data_ptr() if td is not None else 0),
+              ctypes_ptr(tc.data_ptr() if tc is not None else 0), _stream())
+    return td, tc
