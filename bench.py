@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--cells", type=int, default=128, help="cells per axis (C5: 128)")
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--no-cg", action="store_true")
+    ap.add_argument("--no-step", action="store_true", help="skip the config-4 time-step timing")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true",
@@ -191,6 +192,42 @@ def cpu_baseline(k):
     dt = time.perf_counter() - t0
     return {"value": p.size * reps / dt, "unit": "DoF/s", "cores": 1, "kind": "port",
             "sample": f"{cells}^3 cells Q{k} walls vmult x {reps} (numpy port, 1 thread)"}
+
+
+def run_c4_step(nsteps=3):
+    """BASELINE config 4: dual-splitting steps on the 64 x 32 x 32 Q3 channel
+    (y graded 1.8, periodic x/z, walls), nu = 1/180, dt = 1e-3, BDF2, V4,
+    u0 = (1 - y^2, 0, 0) + 0.1 U(-1,1) (seed 3), history [u0, u0]."""
+    import numpy as np
+    import torch
+    from paper_1607_01323_b200 import multigrid as MG, operators as ops, stepper as S
+    from paper_1607_01323_b200.spaces import DgSpace
+    meshes = MG.box_mesh_hierarchy(((0, 2 * np.pi), (-1, 1), (0, np.pi)), (2, 1, 1), 5,
+                                   grading=(0.0, 1.8, 0.0), periodic=(True, False, True))
+    spaces = [DgSpace(m, 3) for m in meshes]
+    spec = ops.BoundarySpec({"ymin": ops.DirichletBC(None), "ymax": ops.DirichletBC(None)})
+    cfg = S.StepConfig(dt=1e-3, nu=1 / 180, J=2, variant=ops.VariantConfig("V4"))
+    vc = S.VelocityCorrection(spaces, spec, cfg)
+    x, y, z = spaces[-1].node_coords()
+    rng = np.random.default_rng(3)
+    u0 = np.stack([1 - y ** 2, 0 * y, 0 * y]) + 0.1 * rng.uniform(-1, 1, (3,) + y.shape)
+    u0 = torch.as_tensor(u0.ravel(), device="cuda")
+    w0 = ops.compute_vorticity(spaces[-1], u0)
+    hu, hp, hw = [u0, u0], [], [w0, w0]
+    steps = []
+    for n in range(nsteps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = vc.step(hu, hp, hw, n * 1e-3)
+        torch.cuda.synchronize()
+        steps.append({"ms": 1e3 * (time.perf_counter() - t0), "substep_ms": r.times_ms,
+                      "iterations": r.iters})
+        hu, hp, hw = [r.u, hu[0]], [r.p] + hp[:1], [r.w, hw[0]]
+    return {"config": "C4: 64x32x32 Q3 channel, y graded 1.8, nu 1/180, dt 1e-3, BDF2, V4 "
+                      "(zeta* = 1, CFL = 1), MG-PCG pressure, M^-1-PCG projection/viscous",
+            "velocity_dofs": 3 * spaces[-1].n_dofs, "ms_per_step_after_first": float(
+                np.median([s["ms"] for s in steps[1:]])) if nsteps > 1 else steps[0]["ms"],
+            "steps": steps}
 
 
 def run_cg(dist_on):
@@ -335,6 +372,9 @@ def main():
     cg = None
     if rank == 0 and world == 1 and not args.no_cg:
         cg = run_cg(False)
+    step = None
+    if rank == 0 and world == 1 and not args.no_step:
+        step = run_c4_step()
     sweep = []
     if rank == 0 and world == 1 and args.sweep:
         sweep = run_sweep()
@@ -384,6 +424,8 @@ def main():
             line["e2e"] = e2e
         if cg:
             line["cg"] = cg
+        if step:
+            line["c4_step"] = step
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

@@ -74,7 +74,7 @@ struct VecCfg {
   static constexpr int FN = DIM == 3 ? N * N : N;     // face nodes
   static constexpr int MX = (N > NQ ? N : NQ);
   static constexpr int BIG = DIM == 3 ? MX * MX * MX : MX * MX;
-  static constexpr int THREADS = QP >= 256 ? 256 : 128;
+  static constexpr int THREADS = QP >= 256 ? 256 : (QP > 64 ? 128 : 64);
   static constexpr int NCM = NCI > NCO ? NCI : NCO;
   // shared layout (doubles)
   static constexpr int U = 0;                       // own cell, NCI * NP
@@ -95,21 +95,23 @@ struct VecCfg {
   static constexpr size_t SMEM = sizeof(double) * NDBL;
 };
 
-// Generic contraction along axis A of a [e2][e1][e0] array (x = axis 0
-// fastest): out[..r..] = sum_c T[r*ldc + c] in[..c..].  T is R x Cc.
-__device__ __forceinline__ void contract(const double *in, double *out, const double *T, int R,
-                                         int Cc, int A, int e0, int e1, int e2) {
-  int o0 = e0, o1 = e1, o2 = e2;
-  if (A == 0) o0 = R; else if (A == 1) o1 = R; else o2 = R;
-  const int tot = o0 * o1 * o2;
-  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-    const int x = i % o0, y = (i / o0) % o1, z = i / (o0 * o1);
-    int r, base, stride;
-    if (A == 0) { r = x; base = (z * e1 + y) * e0; stride = 1; }
-    else if (A == 1) { r = y; base = z * e1 * e0 + x; stride = e0; }
-    else { r = z; base = y * e0 + x; stride = e0 * e1; }
+// Contraction along axis A of a [E2][E1][E0] array (x = axis 0 fastest):
+// out[..r..] = sum_c T[r*Cc + c] in[..c..], T is R x Cc.  All extents are
+// compile-time constants (no integer divisions in the index math).
+template <int R, int Cc, int A, int E0, int E1, int E2>
+__device__ __forceinline__ void contract(const double *in, double *out, const double *T) {
+  constexpr int O0 = A == 0 ? R : E0, O1 = A == 1 ? R : E1, O2 = A == 2 ? R : E2;
+  constexpr int TOT = O0 * O1 * O2;
+  constexpr int STRIDE = A == 0 ? 1 : (A == 1 ? E0 : E0 * E1);
+  for (int i = threadIdx.x; i < TOT; i += blockDim.x) {
+    const int x = i % O0, y = (i / O0) % O1, z = i / (O0 * O1);
+    int r, base;
+    if (A == 0) { r = x; base = (z * E1 + y) * E0; }
+    else if (A == 1) { r = y; base = z * E1 * E0 + x; }
+    else { r = z; base = y * E0 + x; }
     double acc = 0.0;
-    for (int c = 0; c < Cc; ++c) acc += T[r * Cc + c] * in[base + c * stride];
+#pragma unroll
+    for (int c = 0; c < Cc; ++c) acc += T[r * Cc + c] * in[base + c * STRIDE];
     out[i] = acc;
   }
   __syncthreads();
@@ -159,26 +161,26 @@ __device__ void face_traces(const double *cell, int ncomp, int d, int s, const d
     double *dv = dst + (c * (1 + DIM)) * FQ;
     if (!need_grad) {  // values only (convective, projection, divergence, gradient)
       if (DIM == 3) {
-        contract(F.ft, F.t0, F.S, NQ, N, 0, N, N, 1);
-        contract(F.t0, dv, F.S, NQ, N, 1, NQ, N, 1);
+        contract<NQ, N, 0, N, N, 1>(F.ft, F.t0, F.S);
+        contract<NQ, N, 1, NQ, N, 1>(F.t0, dv, F.S);
       } else {
-        contract(F.ft, dv, F.S, NQ, N, 0, N, 1, 1);
+        contract<NQ, N, 0, N, 1, 1>(F.ft, dv, F.S);
       }
       continue;
     }
     if (DIM == 3) {
-      contract(F.ft, F.t0, F.S, NQ, N, 0, N, N, 1);
-      contract(F.t0, dv, F.S, NQ, N, 1, NQ, N, 1);                          // value
-      contract(F.ft + F.big, F.t1, F.S, NQ, N, 0, N, N, 1);
-      contract(F.t1, dv + (1 + d) * FQ, F.S, NQ, N, 1, NQ, N, 1);           // normal
+      contract<NQ, N, 0, N, N, 1>(F.ft, F.t0, F.S);
+      contract<NQ, N, 1, NQ, N, 1>(F.t0, dv, F.S);                          // value
+      contract<NQ, N, 0, N, N, 1>(F.ft + F.big, F.t1, F.S);
+      contract<NQ, N, 1, NQ, N, 1>(F.t1, dv + (1 + d) * FQ, F.S);           // normal
       const int tfa = d == 0 ? 1 : 0, tsl = d == 2 ? 1 : 2;
-      contract(F.ft, F.t2, F.D, NQ, N, 0, N, N, 1);
-      contract(F.t2, dv + (1 + tfa) * FQ, F.S, NQ, N, 1, NQ, N, 1);         // d/d fast
-      contract(F.t0, dv + (1 + tsl) * FQ, F.D, NQ, N, 1, NQ, N, 1);         // d/d slow
+      contract<NQ, N, 0, N, N, 1>(F.ft, F.t2, F.D);
+      contract<NQ, N, 1, NQ, N, 1>(F.t2, dv + (1 + tfa) * FQ, F.S);         // d/d fast
+      contract<NQ, N, 1, NQ, N, 1>(F.t0, dv + (1 + tsl) * FQ, F.D);         // d/d slow
     } else {
-      contract(F.ft, dv, F.S, NQ, N, 0, N, 1, 1);
-      contract(F.ft + F.big, dv + (1 + d) * FQ, F.S, NQ, N, 0, N, 1, 1);
-      contract(F.ft, dv + (1 + (1 - d)) * FQ, F.D, NQ, N, 0, N, 1, 1);
+      contract<NQ, N, 0, N, 1, 1>(F.ft, dv, F.S);
+      contract<NQ, N, 0, N, 1, 1>(F.ft + F.big, dv + (1 + d) * FQ, F.S);
+      contract<NQ, N, 0, N, 1, 1>(F.ft, dv + (1 + (1 - d)) * FQ, F.D);
     }
     for (int i = threadIdx.x; i < DIM * FQ; i += blockDim.x) {
       const int b = i / FQ;
@@ -201,28 +203,28 @@ __device__ void face_lift(const double *fv, int ncomp, int d, int s, const doubl
     const double *dv = fv + (c * (1 + DIM)) * FQ;
     if (DIM == 3) {
       const int tfa = d == 0 ? 1 : 0, tsl = d == 2 ? 1 : 2;
-      contract(dv, F.t0, F.ST, N, NQ, 0, NQ, NQ, 1);
-      contract(F.t0, F.t1, F.ST, N, NQ, 1, N, NQ, 1);           // value part [sl][fa]
+      contract<N, NQ, 0, NQ, NQ, 1>(dv, F.t0, F.ST);
+      contract<N, NQ, 1, N, NQ, 1>(F.t0, F.t1, F.ST);           // value part [sl][fa]
       if (grad_terms) {
-        contract(dv + (1 + tfa) * FQ, F.t0, F.DT, N, NQ, 0, NQ, NQ, 1);
-        contract(F.t0, F.t2, F.ST, N, NQ, 1, N, NQ, 1);
+        contract<N, NQ, 0, NQ, NQ, 1>(dv + (1 + tfa) * FQ, F.t0, F.DT);
+        contract<N, NQ, 1, N, NQ, 1>(F.t0, F.t2, F.ST);
         for (int i = threadIdx.x; i < FN; i += blockDim.x) F.t1[i] += (2.0 / h[tfa]) * F.t2[i];
         __syncthreads();
-        contract(dv + (1 + tsl) * FQ, F.t0, F.ST, N, NQ, 0, NQ, NQ, 1);
-        contract(F.t0, F.t2, F.DT, N, NQ, 1, N, NQ, 1);
+        contract<N, NQ, 0, NQ, NQ, 1>(dv + (1 + tsl) * FQ, F.t0, F.ST);
+        contract<N, NQ, 1, N, NQ, 1>(F.t0, F.t2, F.DT);
         for (int i = threadIdx.x; i < FN; i += blockDim.x) F.t1[i] += (2.0 / h[tsl]) * F.t2[i];
         __syncthreads();
-        contract(dv + (1 + d) * FQ, F.t0, F.ST, N, NQ, 0, NQ, NQ, 1);
-        contract(F.t0, F.t2, F.ST, N, NQ, 1, N, NQ, 1);          // normal-gradient part
+        contract<N, NQ, 0, NQ, NQ, 1>(dv + (1 + d) * FQ, F.t0, F.ST);
+        contract<N, NQ, 1, N, NQ, 1>(F.t0, F.t2, F.ST);          // normal-gradient part
       }
     } else {
       const int tt = 1 - d;
-      contract(dv, F.t1, F.ST, N, NQ, 0, NQ, 1, 1);
+      contract<N, NQ, 0, NQ, 1, 1>(dv, F.t1, F.ST);
       if (grad_terms) {
-        contract(dv + (1 + tt) * FQ, F.t2, F.DT, N, NQ, 0, NQ, 1, 1);
+        contract<N, NQ, 0, NQ, 1, 1>(dv + (1 + tt) * FQ, F.t2, F.DT);
         for (int i = threadIdx.x; i < FN; i += blockDim.x) F.t1[i] += (2.0 / h[tt]) * F.t2[i];
         __syncthreads();
-        contract(dv + (1 + d) * FQ, F.t2, F.ST, N, NQ, 0, NQ, 1, 1);
+        contract<N, NQ, 0, NQ, 1, 1>(dv + (1 + d) * FQ, F.t2, F.ST);
       }
     }
     double *oc = out + c * NP;
@@ -278,8 +280,8 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
   __syncthreads();
 
   const int op = prm.op;
-  const int e0 = N, e1 = N, e2 = DIM == 3 ? N : 1;
-  const int q0 = NQ, q1 = NQ, q2 = DIM == 3 ? NQ : 1;
+  constexpr int e0 = N, e1 = N, e2 = DIM == 3 ? N : 1;
+  constexpr int q0 = NQ, q1 = NQ, q2 = DIM == 3 ? NQ : 1;
   auto wq = [&](int i) {  // tensor weight * det at q point i
     const int x = i % NQ, y = (i / NQ) % NQ, z = DIM == 3 ? i / (NQ * NQ) : 0;
     return det * W[x] * W[y] * (DIM == 3 ? W[z] : 1.0);
@@ -438,24 +440,24 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
         const double *uc = su + c * NP;
         double *val = qv + c * QP;
         if (DIM == 3) {
-          contract(uc, t0, S, NQ, N, 0, e0, e1, e2);                 // [z][y][qx]
-          contract(t0, t1, S, NQ, N, 1, q0, e1, e2);                 // [z][qy][qx]
-          if (need_qv) contract(t1, val, S, NQ, N, 2, q0, q1, e2);   // values
+          contract<NQ, N, 0, e0, e1, e2>(uc, t0, S);                 // [z][y][qx]
+          contract<NQ, N, 1, q0, e1, e2>(t0, t1, S);                 // [z][qy][qx]
+          if (need_qv) contract<NQ, N, 2, q0, q1, e2>(t1, val, S);   // values
           if (need_qg) {
-            contract(t1, qg + (c * DIM + 2) * QP, D, NQ, N, 2, q0, q1, e2);  // d/dz
-            contract(t0, t2, D, NQ, N, 1, q0, e1, e2);
-            contract(t2, qg + (c * DIM + 1) * QP, S, NQ, N, 2, q0, q1, e2);  // d/dy
-            contract(uc, t0, D, NQ, N, 0, e0, e1, e2);
-            contract(t0, t1, S, NQ, N, 1, q0, e1, e2);
-            contract(t1, qg + (c * DIM + 0) * QP, S, NQ, N, 2, q0, q1, e2);  // d/dx
+            contract<NQ, N, 2, q0, q1, e2>(t1, qg + (c * DIM + 2) * QP, D);  // d/dz
+            contract<NQ, N, 1, q0, e1, e2>(t0, t2, D);
+            contract<NQ, N, 2, q0, q1, e2>(t2, qg + (c * DIM + 1) * QP, S);  // d/dy
+            contract<NQ, N, 0, e0, e1, e2>(uc, t0, D);
+            contract<NQ, N, 1, q0, e1, e2>(t0, t1, S);
+            contract<NQ, N, 2, q0, q1, e2>(t1, qg + (c * DIM + 0) * QP, S);  // d/dx
           }
         } else {
-          contract(uc, t0, S, NQ, N, 0, e0, e1, 1);
-          if (need_qv) contract(t0, val, S, NQ, N, 1, q0, e1, 1);
+          contract<NQ, N, 0, e0, e1, 1>(uc, t0, S);
+          if (need_qv) contract<NQ, N, 1, q0, e1, 1>(t0, val, S);
           if (need_qg) {
-            contract(t0, qg + (c * DIM + 1) * QP, D, NQ, N, 1, q0, e1, 1);
-            contract(uc, t0, D, NQ, N, 0, e0, e1, 1);
-            contract(t0, qg + (c * DIM + 0) * QP, S, NQ, N, 1, q0, e1, 1);
+            contract<NQ, N, 1, q0, e1, 1>(t0, qg + (c * DIM + 1) * QP, D);
+            contract<NQ, N, 0, e0, e1, 1>(uc, t0, D);
+            contract<NQ, N, 1, q0, e1, 1>(t0, qg + (c * DIM + 0) * QP, S);
           }
         }
       }
@@ -511,12 +513,12 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
         double *oa = sout + a * NP;
         if (need_val) {
           if (DIM == 3) {
-            contract(t2, t0, ST, N, NQ, 0, q0, q1, q2);
-            contract(t0, t1, ST, N, NQ, 1, e0, q1, q2);
-            contract(t1, t0, ST, N, NQ, 2, e0, e1, q2);
+            contract<N, NQ, 0, q0, q1, q2>(t2, t0, ST);
+            contract<N, NQ, 1, e0, q1, q2>(t0, t1, ST);
+            contract<N, NQ, 2, e0, e1, q2>(t1, t0, ST);
           } else {
-            contract(t2, t1, ST, N, NQ, 0, q0, q1, 1);
-            contract(t1, t0, ST, N, NQ, 1, e0, q1, 1);
+            contract<N, NQ, 0, q0, q1, 1>(t2, t1, ST);
+            contract<N, NQ, 1, e0, q1, 1>(t1, t0, ST);
           }
           for (int i = tid; i < NP; i += blockDim.x) oa[i] += t0[i];
           __syncthreads();
@@ -527,12 +529,12 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
           const double sc = 2.0 / h[b];
           const double *gb = tg + b * QP;
           if (DIM == 3) {
-            contract(gb, t0, b == 0 ? DT : ST, N, NQ, 0, q0, q1, q2);
-            contract(t0, t1, b == 1 ? DT : ST, N, NQ, 1, e0, q1, q2);
-            contract(t1, t0, b == 2 ? DT : ST, N, NQ, 2, e0, e1, q2);
+            contract<N, NQ, 0, q0, q1, q2>(gb, t0, b == 0 ? DT : ST);
+            contract<N, NQ, 1, e0, q1, q2>(t0, t1, b == 1 ? DT : ST);
+            contract<N, NQ, 2, e0, e1, q2>(t1, t0, b == 2 ? DT : ST);
           } else {
-            contract(gb, t1, b == 0 ? DT : ST, N, NQ, 0, q0, q1, 1);
-            contract(t1, t0, b == 1 ? DT : ST, N, NQ, 1, e0, q1, 1);
+            contract<N, NQ, 0, q0, q1, 1>(gb, t1, b == 0 ? DT : ST);
+            contract<N, NQ, 1, e0, q1, 1>(t1, t0, b == 1 ? DT : ST);
           }
           for (int i = tid; i < NP; i += blockDim.x) oa[i] += sc * t0[i];
           __syncthreads();
@@ -666,12 +668,12 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
           t2[i] = prm.vol_data[((int64_t)a * ncells + e) * QP + i] * wq(i);
         __syncthreads();
         if (DIM == 3) {
-          contract(t2, t0, ST, N, NQ, 0, q0, q1, q2);
-          contract(t0, t1, ST, N, NQ, 1, e0, q1, q2);
-          contract(t1, t0, ST, N, NQ, 2, e0, e1, q2);
+          contract<N, NQ, 0, q0, q1, q2>(t2, t0, ST);
+          contract<N, NQ, 1, e0, q1, q2>(t0, t1, ST);
+          contract<N, NQ, 2, e0, e1, q2>(t1, t0, ST);
         } else {
-          contract(t2, t1, ST, N, NQ, 0, q0, q1, 1);
-          contract(t1, t0, ST, N, NQ, 1, e0, q1, 1);
+          contract<N, NQ, 0, q0, q1, 1>(t2, t1, ST);
+          contract<N, NQ, 1, e0, q1, 1>(t1, t0, ST);
         }
         for (int i = tid; i < NP; i += blockDim.x) sout[a * NP + i] += t0[i];
         __syncthreads();
