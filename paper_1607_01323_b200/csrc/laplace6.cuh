@@ -60,8 +60,10 @@ struct Lap6Cfg {
   static constexpr size_t SMEM = sizeof(double) * (size_t)NDBL + sizeof(int) * NC * 6;
 };
 
+// 4 CTAs per SM need <= 168 registers at 96 threads: one more register drops
+// the occupancy to 3 CTAs and costs ~30 % (measured)
 template <int N, int BX, int BY, int BZ, int EPI = kEpiStore>
-__global__ void __launch_bounds__(Lap6Cfg<N, BX, BY, BZ>::THREADS)
+__global__ void __launch_bounds__(Lap6Cfg<N, BX, BY, BZ>::THREADS, 4)
 laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g,
                 const LapTab<N> T, const double tau_scale, const int part,
                 const EpiArgs ea = EpiArgs{}) {
