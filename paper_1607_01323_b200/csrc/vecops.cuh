@@ -17,6 +17,8 @@
 // One CTA per cell.  Neighbour cells are read from global memory (L2) into
 // shared memory one face at a time.  NCI input / NCO output components.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace dg {
@@ -76,22 +78,29 @@ struct VecCfg {
   static constexpr int BIG = DIM == 3 ? MX * MX * MX : MX * MX;
   static constexpr int THREADS = QP >= 256 ? 256 : (QP > 64 ? 128 : 64);
   static constexpr int NCM = NCI > NCO ? NCI : NCO;
-  // shared layout (doubles)
+  // shared layout (doubles).  The volume buffers (QV, QG, TG) and the face
+  // buffers (NB, FO, FB, FV, FT) are alive in different phases and share one
+  // region: fewer doubles per cell, more cells resident per SM.
   static constexpr int U = 0;                       // own cell, NCI * NP
-  static constexpr int NB = U + NCI * NP;           // neighbour cell, NCI * NP
-  static constexpr int OUT = NB + NCI * NP;         // accumulator, NCO * NP
-  static constexpr int QV = OUT + NCO * NP;         // values at q points, NCM * QP
-  static constexpr int QG = QV + NCM * QP;          // phys gradients, NCI * DIM * QP
-  static constexpr int T0 = QG + NCI * DIM * QP;    // temporaries, 3 * BIG
+  static constexpr int OUT = U + NCI * NP;          // accumulator, NCO * NP
+  static constexpr int T0 = OUT + NCO * NP;         // temporaries, 3 * BIG
   static constexpr int T1 = T0 + BIG;
   static constexpr int T2 = T1 + BIG;
-  static constexpr int TG = T2 + BIG;               // test data, DIM * QP
-  static constexpr int FO = TG + DIM * QP;          // own face traces NCI*(1+DIM)*FQ
+  static constexpr int ACC = T2 + BIG;              // pressure Neumann data, DIM * FQ
+  static constexpr int SHARED = ACC + DIM * FQ;     // volume | face region
+  static constexpr int QV = SHARED;                 // values at q points, NCM * QP
+  static constexpr int QG = QV + NCM * QP;          // phys gradients, NCI * DIM * QP
+  static constexpr int TG = QG + NCI * DIM * QP;    // test data, DIM * QP
+  static constexpr int VOL_END = TG + DIM * QP;
+  static constexpr int NB = SHARED;                 // neighbour cell, NCI * NP
+  static constexpr int FO = NB + NCI * NP;          // own face traces NCI*(1+DIM)*FQ
   static constexpr int FB = FO + NCI * (1 + DIM) * FQ;  // neighbour traces
   static constexpr int FV = FB + NCI * (1 + DIM) * FQ;  // face test data NCO*(1+DIM)*FQ
   static constexpr int FT = FV + NCO * (1 + DIM) * FQ;  // face temporaries 2*BIG
-  static constexpr int TAB = FT + 2 * BIG;              // tables S, D, ST(N x NQ), DT
-  static constexpr int NDBL = TAB + 4 * NQ * N + NQ + 2 * N;
+  static constexpr int FACE_END = FT + 2 * BIG;
+  static constexpr int TAB = VOL_END > FACE_END ? VOL_END : FACE_END;  // tables S, D, ST, DT
+  static constexpr int HSM = TAB + 4 * NQ * N + NQ + 2 * N;  // cell sizes: own[3], neighbour[3]
+  static constexpr int NDBL = HSM + 6;
   static constexpr size_t SMEM = sizeof(double) * NDBL;
 };
 
@@ -255,11 +264,17 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
   double *fo = sm + C::FO, *fb = sm + C::FB, *fv = sm + C::FV, *ft = sm + C::FT;
   double *S = sm + C::TAB, *D = S + NQ * N, *ST = D + NQ * N, *DT = ST + NQ * N;
   double *W = DT + NQ * N, *dL = W + NQ, *dR = dL + N;
+  double *hs = sm + C::HSM, *hsn = hs + 3;  // cell sizes for the face helpers (shared:
+                                            // no local-memory copy of an indexed array)
+  // kernel-parameter arrays indexed by runtime level / side, staged in shared
+  // memory (a dynamically indexed parameter array would be copied to local)
+  __shared__ const double *p_hist[kMaxHist], *p_vort[kMaxHist], *p_bnd[6], *p_gh[kMaxHist][6];
+  __shared__ double p_beta[kMaxHist];
   const int tid = threadIdx.x;
   const int64_t e = blockIdx.x;
   const int ix = (int)(e % g.nx), iy = (int)((e / g.nx) % g.ny), iz = (int)(e / ((int64_t)g.nx * g.ny));
-  const int cidx[3] = {ix, iy, iz};
-  double h[3] = {g.hx[ix], g.hy[iy], DIM == 3 ? g.hz[iz] : 2.0};
+  const double h[3] = {g.hx[ix], g.hy[iy], DIM == 3 ? g.hz[iz] : 2.0};
+  if (tid < 3) hs[tid] = tid == 0 ? h[0] : (tid == 1 ? h[1] : h[2]);
   double det = 0.125 * h[0] * h[1] * h[2];
   if (DIM == 2) det = 0.25 * h[0] * h[1];
   const FaceScratch F{t0, t1, t2, ft, S, D, ST, DT, dL, dR, C::BIG};
@@ -277,6 +292,18 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
     dR[i] = tab.dR[i];
   }
   for (int i = tid; i < NCO * NP; i += blockDim.x) sout[i] = 0.0;
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j < kMaxHist; ++j) {
+      p_hist[j] = prm.hist[j];
+      p_vort[j] = prm.vort[j];
+      p_beta[j] = prm.beta[j];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) p_gh[j][q] = prm.gh[j][q];
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) p_bnd[q] = prm.bnd[q];
+  }
   __syncthreads();
 
   const int op = prm.op;
@@ -313,7 +340,7 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
   };
   auto side_kind = [&](int d, int s) {
     const int nd = d == 0 ? g.nx : (d == 1 ? g.ny : g.nz);
-    const int nidx = cidx[d] + (s ? 1 : -1);
+    const int nidx = (d == 0 ? ix : (d == 1 ? iy : iz)) + (s ? 1 : -1);
     if (nidx >= 0 && nidx < nd) return 0;
     const int m = g.mode[2 * d + s];
     return (m == kBndNone || m == kBndNeumann) ? m : 0;
@@ -328,29 +355,32 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
       if (op == kOpPressureNeumann && kind != kBndNone) continue;
       if (op == kOpGpDirichlet && kind != kBndNeumann) continue;
       const int64_t it = tan_index(d);
-      const double *bd = prm.bnd[side];
+      const double *bd = p_bnd[side];
       const double fdet = face_det(d);
       const double nsgn = s ? 1.0 : -1.0;
       bool grad_terms = false;
       if (op == kOpPressureNeumann) {
         // h_a = sum_i beta_i (div(u u) + nu curl w)_a (+ dg/dt - f data)
-        double *acc = qv;  // DIM * FQ accumulators
+        double *acc = sm + C::ACC;  // DIM * FQ accumulators (the face buffers alias qv)
         for (int i = tid; i < DIM * FQ; i += blockDim.x) acc[i] = 0.0;
         for (int lev = 0; lev < prm.n_hist; ++lev) {
-          load(prm.hist[lev], DIM, e, su);
-          load(prm.vort[lev], prm.n_vort, e, snb);
+          load(p_hist[lev], DIM, e, su);
+          load(p_vort[lev], prm.n_vort, e, snb);
           __syncthreads();
-          face_traces<DIM, N, NQ>(su, DIM, d, s, h, fo, F);
-          face_traces<DIM, N, NQ>(snb, prm.n_vort, d, s, h, fb, F);
-          const double beta = prm.beta[lev];
+          face_traces<DIM, N, NQ>(su, DIM, d, s, hs, fo, F);
+          face_traces<DIM, N, NQ>(snb, prm.n_vort, d, s, hs, fb, F);
+          const double beta = p_beta[lev];
           for (int i = tid; i < FQ; i += blockDim.x) {
             double uu[DIM], gr[DIM][DIM], gw[3][DIM];
             for (int c = 0; c < DIM; ++c) {
               uu[c] = fo[(c * (1 + DIM)) * FQ + i];
               for (int b = 0; b < DIM; ++b) gr[c][b] = fo[(c * (1 + DIM) + 1 + b) * FQ + i];
             }
-            for (int c = 0; c < prm.n_vort && c < 3; ++c)
-              for (int b = 0; b < DIM; ++b) gw[c][b] = fb[(c * (1 + DIM) + 1 + b) * FQ + i];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+              for (int b = 0; b < DIM; ++b)
+                gw[c][b] = c < prm.n_vort ? fb[(c * (1 + DIM) + 1 + b) * FQ + i] : 0.0;
             double div = 0.0;
             for (int c = 0; c < DIM; ++c) div += gr[c][c];
             double curl[DIM];
@@ -412,7 +442,7 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
         }
       }
       __syncthreads();
-      face_lift<DIM, N, NQ>(fv, NCO, d, s, h, grad_terms, sout, F);
+      face_lift<DIM, N, NQ>(fv, NCO, d, s, hs, grad_terms, sout, F);
     }
   } else {
     // ---- volume + face operators ---------------------------------------------
@@ -431,8 +461,8 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
                              (op == kOpGradient && weak)) ? 1 : 0;
     const int nlev = op == kOpConvective ? prm.n_hist : 1;
     for (int lev = 0; lev < nlev; ++lev) {
-      const double *src = op == kOpConvective ? prm.hist[lev] : u;
-      const double beta = op == kOpConvective ? prm.beta[lev] : 1.0;
+      const double *src = op == kOpConvective ? p_hist[lev] : u;
+      const double beta = op == kOpConvective ? p_beta[lev] : 1.0;
       load(src, NCI, e, su);
       __syncthreads();
       // ---- values and physical gradients at q points ------------------------
@@ -464,7 +494,7 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
       if (need_qg) {
         for (int i = tid; i < NCI * DIM * QP; i += blockDim.x) {
           const int d = (i / QP) % DIM;
-          qg[i] *= 2.0 / h[d];
+          qg[i] *= 2.0 / hs[d];
         }
         __syncthreads();
       }
@@ -545,19 +575,22 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
                          (op == kOpProjection && prm.tau_c != nullptr) || op == kOpConvective ||
                          ((op == kOpDivergence || op == kOpGradient) && prm.form != kFormStandard);
       if (!faces) continue;
-      for (int side = 0; side < 2 * DIM; ++side) {
-        const int d = side >> 1, s = side & 1;
+      // the face physics indexes gradients by the face direction: make it a
+      // compile-time constant (no local-memory arrays)
+      auto do_side = [&](auto dconst, const int s) {
+        constexpr int d = decltype(dconst)::value;
+        const int side = 2 * d + s;
         const int kind = side_kind(d, s);
         // projection / strong divergence: interior faces only; Helmholtz:
         // nothing on velocity-Neumann faces; others: all faces
         if ((op == kOpProjection || (op == kOpDivergence && prm.form == kFormStrong)) && kind != 0)
-          continue;
-        if (op == kOpHelmholtz && kind == kBndNeumann) continue;
+          return;
+        if (op == kOpHelmholtz && kind == kBndNeumann) return;
         int64_t en = e;
         double hn = h[d];
         if (kind == 0) {
           const int nd = d == 0 ? g.nx : (d == 1 ? g.ny : g.nz);
-          int nidx = cidx[d] + (s ? 1 : -1);
+          int nidx = (d == 0 ? ix : (d == 1 ? iy : iz)) + (s ? 1 : -1);
           if (nidx < 0 || nidx >= nd) nidx = s ? 0 : nd - 1;  // periodic wrap
           const int cx = d == 0 ? nidx : ix, cy = d == 1 ? nidx : iy, cz = d == 2 ? nidx : iz;
           en = cx + (int64_t)g.nx * (cy + (int64_t)g.ny * cz);
@@ -566,14 +599,10 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
         }
         __syncthreads();
         const bool tgrad = op == kOpHelmholtz;  // only the viscous flux needs face gradients
-        face_traces<DIM, N, NQ>(su, NCI, d, s, h, fo, F, tgrad);
-        if (kind == 0) {
-          // traces scale by 2/h[b]; the neighbour differs only along d
-          const double hsave = h[d];
-          h[d] = hn;
-          face_traces<DIM, N, NQ>(snb, NCI, d, 1 - s, h, fb, F, tgrad);
-          h[d] = hsave;
-        }
+        if (tid < 3) hsn[tid] = tid == d ? hn : hs[tid];  // the neighbour differs along d only
+        __syncthreads();
+        face_traces<DIM, N, NQ>(su, NCI, d, s, hs, fo, F, tgrad);
+        if (kind == 0) face_traces<DIM, N, NQ>(snb, NCI, d, 1 - s, hsn, fb, F, tgrad);
         const double fdet = face_det(d);
         const double nsgn = s ? 1.0 : -1.0;  // own outward normal = nsgn e_d
         double tau = 0.0;
@@ -627,7 +656,7 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
             if (kind == 0) {
               for (int c = 0; c < NCI; ++c) up[c] = un[c];
             } else {  // mirror state 2 g - u with the level's Dirichlet data
-              const double *gd = prm.gh[lev][side];
+              const double *gd = p_gh[lev][side];
               for (int c = 0; c < NCI; ++c)
                 up[c] = (gd ? 2.0 * gd[(tan_index(d) * NCI + c) * FQ + i] : 0.0) - uo[c];
             }
@@ -658,7 +687,17 @@ vecop_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g
           }
         }
         __syncthreads();
-        face_lift<DIM, N, NQ>(fv, NCO, d, s, h, op == kOpHelmholtz, sout, F);
+        face_lift<DIM, N, NQ>(fv, NCO, d, s, hs, op == kOpHelmholtz, sout, F);
+      };
+      for (int side = 0; side < 2 * DIM; ++side) {
+        const int sd = side & 1;
+        switch (side >> 1) {
+          case 0: do_side(std::integral_constant<int, 0>(), sd); break;
+          case 1: do_side(std::integral_constant<int, 1>(), sd); break;
+          default:
+            if (DIM == 3) do_side(std::integral_constant<int, DIM - 1>(), sd);
+            break;
+        }
       }
     }
     if (op == kOpConvective && prm.vol_data != nullptr) {
