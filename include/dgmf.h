@@ -81,6 +81,14 @@ int dg_basis_tables(int k, int n_q, double *S, double *D, double *nodes,
 /* apply_pressure_laplace(space, p, bcs, tau_scale)  operators.py:187-238 */
 int dg_laplace_vmult(dg_ctx *ctx, const double *src, double *dst,
                      double tau_scale, void *stream);
+/* apply_pressure_laplace with HOST buffers (the numpy call form of the
+ * reference): src_host -> device -> vmult -> dst_host, pipelined in
+ * n_chunks z-chunks of whole x-y layers on three streams (H2D, kernel, D2H
+ * overlap when the host buffers are pinned).  Whole-mesh contexts; results
+ * identical to dg_laplace_vmult.  dst_host is complete once `stream` has
+ * reached this call's end (e.g. after cudaStreamSynchronize). */
+int dg_laplace_vmult_host(dg_ctx *ctx, const double *src_host, double *dst_host,
+                          double tau_scale, int n_chunks, void *stream);
 /* laplace_diagonal(space, bcs, tau_scale)  operators.py:717-730 */
 int dg_laplace_diagonal(dg_ctx *ctx, double *diag, double tau_scale,
                         void *stream);

@@ -46,6 +46,7 @@ struct Geo {
   double ghost_h[2];
   double ghost_hi[2];
   int exp_flags;             // timing experiments (DG_EXP env); 0 in production
+  int bz0;                   // first brick z index of a chunked (z-range) launch, else 0
 };
 
 // 1D reference matrices on [-1,1] for n = k+1 GLL nodes, Gauss rule n_q = n:

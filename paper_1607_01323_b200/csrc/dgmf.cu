@@ -223,6 +223,10 @@ int dg_ctx_destroy(dg_ctx *c) {
   cudaFree(c->d_hy);
   cudaFree(c->d_hz);
   cudaFree(c->d_hinv);
+  cudaFree(c->d_hin);
+  cudaFree(c->d_hout);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   cudaFree(c->d_tau);
   for (int s = 0; s < 2; ++s) {
     cudaFree(c->d_ghost_tau[s]);
@@ -285,6 +289,17 @@ static LapTab<N> lap_tab(const Basis1D &b) {
   return t;
 }
 
+// z-bricks of a launch: the ctx's chunk (cell layers [zc0, zc1), zc0 a
+// multiple of 4 >= BZ) for the pipelined host-buffer vmult, else all
+static unsigned chunk_bricks_z(const dg_ctx *c, int BZ, Geo &g) {
+  if (c->zc1 > 0) {
+    g.bz0 = c->zc0 / BZ;
+    return (unsigned)((c->zc1 - c->zc0 + BZ - 1) / BZ);
+  }
+  g.bz0 = 0;
+  return (unsigned)((g.nz + BZ - 1) / BZ);
+}
+
 template <int DIM, int N, int BX, int BY, int BZ, int EPI = kEpiStore>
 static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                           cudaStream_t st, const EpiArgs &ea = EpiArgs{}) {
@@ -295,8 +310,8 @@ static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
-  const Geo g = c->geo();
-  const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, (g.nz + BZ - 1) / BZ);
+  Geo g = c->geo();
+  const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, chunk_bricks_z(c, BZ, g));
   kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part, ea);
   DG_LAUNCH_CHECK("laplace_vmult_kernel");
   return DG_OK;
@@ -387,8 +402,8 @@ static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
-  const Geo g = c->geo();
-  const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, (g.nz + BZ - 1) / BZ);
+  Geo g = c->geo();
+  const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, chunk_bricks_z(c, BZ, g));
   kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part, ea);
   DG_LAUNCH_CHECK("laplace6_kernel");
   return DG_OK;
@@ -538,6 +553,79 @@ int dg_laplace_vmult(dg_ctx *c, const double *src, double *dst, double tau_scale
   if ((c->mode[0] == kGhost && !c->d_recv[0]) || (c->mode[1] == kGhost && !c->d_recv[1]))
     return inval("x-slab context: attach ghost layers (dg_halo_attach) first");
   return laplace_dispatch(c, src, dst, tau_scale, 0, (cudaStream_t)stream);
+}
+
+// apply_pressure_laplace on HOST buffers (pinned for overlap): the mesh is
+// cut into z-chunks of whole x-y layers (contiguous in the element-major
+// layout); host->device copies of chunk i+1, the vmult of chunk i and the
+// device->host copy of chunk i-1 run on three streams, so the two PCIe
+// directions and the kernel overlap.  A chunk's vmult waits for the copies of
+// its z-neighbour chunks (its halo).
+int dg_laplace_vmult_host(dg_ctx *c, const double *src_host, double *dst_host, double tau_scale,
+                          int n_chunks, void *stream) {
+  if (!c || !src_host || !dst_host) return inval("null argument");
+  if (c->mode[0] == kGhost || c->mode[1] == kGhost)
+    return inval("host-buffer vmult runs on whole-mesh contexts");
+  std::lock_guard<std::mutex> lock(c->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = c->n_dofs;
+  if (!c->d_hin) {
+    DG_CUDA_CHECK(cudaMalloc((void **)&c->d_hin, sizeof(double) * (n > 0 ? n : 1)));
+    DG_CUDA_CHECK(cudaMalloc((void **)&c->d_hout, sizeof(double) * (n > 0 ? n : 1)));
+    DG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    DG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+  }
+  static const bool variant = getenv("DG_LAP_VARIANT") && atoi(getenv("DG_LAP_VARIANT")) != 0;
+  const int nz = c->counts[2];
+  int nch = (c->dim == 3 && !variant) ? n_chunks : 1;
+  if (nch < 1) nch = 1;
+  int layers = (nz + nch - 1) / nch;
+  layers = ((layers + 3) / 4) * 4;  // chunk boundaries on multiples of 4 (brick heights)
+  nch = (nz + layers - 1) / layers;
+  const int64_t per_layer = (int64_t)c->counts[0] * c->counts[1] * c->np;
+  std::vector<cudaEvent_t> eh(nch), ec(nch);
+  for (int i = 0; i < nch; ++i) {
+    DG_CUDA_CHECK(cudaEventCreateWithFlags(&eh[i], cudaEventDisableTiming));
+    DG_CUDA_CHECK(cudaEventCreateWithFlags(&ec[i], cudaEventDisableTiming));
+  }
+  cudaEvent_t start, done;
+  DG_CUDA_CHECK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  DG_CUDA_CHECK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  DG_CUDA_CHECK(cudaEventRecord(start, st));  // order after prior work on the caller's stream
+  DG_CUDA_CHECK(cudaStreamWaitEvent(c->s_h2d, start, 0));
+  int rc = DG_OK;
+  for (int i = 0; i < nch; ++i) {
+    const int z0 = i * layers, z1 = std::min(nz, z0 + layers);
+    const int64_t off = z0 * per_layer, cnt = (int64_t)(z1 - z0) * per_layer;
+    DG_CUDA_CHECK(cudaMemcpyAsync(c->d_hin + off, src_host + off, sizeof(double) * cnt,
+                                  cudaMemcpyHostToDevice, c->s_h2d));
+    DG_CUDA_CHECK(cudaEventRecord(eh[i], c->s_h2d));
+  }
+  const bool zper = c->mode[4] == kWrap;
+  for (int i = 0; i < nch && rc == DG_OK; ++i) {
+    DG_CUDA_CHECK(cudaStreamWaitEvent(st, eh[std::min(i + 1, nch - 1)], 0));
+    if (zper && i == 0) DG_CUDA_CHECK(cudaStreamWaitEvent(st, eh[nch - 1], 0));
+    c->zc0 = i * layers;
+    c->zc1 = nch > 1 ? std::min(nz, c->zc0 + layers) : 0;
+    rc = laplace_dispatch(c, c->d_hin, c->d_hout, tau_scale, 0, st);
+    c->zc0 = c->zc1 = 0;
+    if (rc) break;
+    DG_CUDA_CHECK(cudaEventRecord(ec[i], st));
+    DG_CUDA_CHECK(cudaStreamWaitEvent(c->s_d2h, ec[i], 0));
+    const int z0 = i * layers, z1 = std::min(nz, z0 + layers);
+    const int64_t off = z0 * per_layer, cnt = (int64_t)(z1 - z0) * per_layer;
+    DG_CUDA_CHECK(cudaMemcpyAsync(dst_host + off, c->d_hout + off, sizeof(double) * cnt,
+                                  cudaMemcpyDeviceToHost, c->s_d2h));
+  }
+  DG_CUDA_CHECK(cudaEventRecord(done, c->s_d2h));
+  DG_CUDA_CHECK(cudaStreamWaitEvent(st, done, 0));  // the caller's stream sees the result
+  for (int i = 0; i < nch; ++i) {
+    cudaEventDestroy(eh[i]);
+    cudaEventDestroy(ec[i]);
+  }
+  cudaEventDestroy(start);
+  cudaEventDestroy(done);
+  return rc;
 }
 
 int dg_laplace_vmult_part(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,

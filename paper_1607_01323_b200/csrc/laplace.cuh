@@ -291,7 +291,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   const double **hsrc = reinterpret_cast<const double **>(smem + C::OFF_PTR);
   int *soff = reinterpret_cast<int *>(smem + C::NDBL);
 
-  const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
+  const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z + g.bz0;
   const int x0 = bx * BX, y0 = by * BY, z0 = bz * BZ;
   const int ex = min(BX, g.nx - x0), ey = min(BY, g.ny - y0);
   const int ez = (DIM == 3) ? min(BZ, g.nz - z0) : 1;
