@@ -10,8 +10,6 @@
 #include "ctx.h"
 #include "laplace.cuh"
 #include "laplace6.cuh"
-#include "laplace_persist.cuh"
-#include "laplace_warp.cuh"
 #include "mg.cuh"
 #include "tables.h"
 #include "tensor.cuh"
@@ -353,45 +351,6 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
   return DG_ENOTSUP;
 }
 
-template <int N, int BX, int BY, int BZ>
-static int launch_laplace_persist(dg_ctx *c, const double *src, double *dst, double tau_scale,
-                                  cudaStream_t st) {
-  using C = PersistCfg<N, BX, BY, BZ>;
-  using L = LapCfg<3, N, BX, BY, BZ>;
-  auto kern = laplace_persist_kernel<N, BX, BY, BZ>;
-  static int nsm = 0;
-  if (!nsm) {
-    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    int dev = 0;
-    DG_CUDA_CHECK(cudaGetDevice(&dev));
-    DG_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  }
-  const Geo g = c->geo();
-  const int nbx = (g.nx + BX - 1) / BX, nby = (g.ny + BY - 1) / BY, nbz = (g.nz + BZ - 1) / BZ;
-  const int nb = nbx * nby * nbz;
-  const int grid = nb < 2 * nsm ? nb : 2 * nsm;
-  kern<<<grid, L::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, nbx, nby, nb);
-  DG_LAUNCH_CHECK("laplace_persist_kernel");
-  return DG_OK;
-}
-
-template <int N, int BX, int BY, int BZ, int NW>
-static int launch_laplace_warp(dg_ctx *c, const double *src, double *dst, double tau_scale,
-                               int part, cudaStream_t st) {
-  using C = WarpLapCfg<N, BX, BY, BZ, NW>;
-  auto kern = laplace_warp_kernel<N, BX, BY, BZ, NW>;
-  static bool attr = false;
-  if (!attr) {
-    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
-  }
-  const Geo g = c->geo();
-  const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, (g.nz + BZ - 1) / BZ);
-  kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part);
-  DG_LAUNCH_CHECK("laplace_warp_kernel");
-  return DG_OK;
-}
-
 template <int N, int BX, int BY, int BZ, int EPI>
 static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea) {
@@ -415,44 +374,11 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
     const char *v = getenv("DG_LAP_VARIANT");  // brick-shape experiments
     return v ? atoi(v) : 0;
   }();
-  static const int brick6 = [] {
-    const char *v = getenv("DG_LAP6_BRICK");
-    return v ? atoi(v) : 0;
-  }();
-  if (c->dim == 3 && variant == 6) {  // register-plane kernel (laplace6.cuh)
-    if (c->n == 5) {
-      if (brick6 == 1) return launch_laplace6<5, 2, 2, 2>(c, src, dst, tau_scale, part, st);
-      if (brick6 == 2) return launch_laplace6<5, 4, 4, 2>(c, src, dst, tau_scale, part, st);
-      if (brick6 == 3) return launch_laplace6<5, 8, 2, 2>(c, src, dst, tau_scale, part, st);
-      return launch_laplace6<5, 4, 2, 2>(c, src, dst, tau_scale, part, st);
-    }
-    if (c->n == 4) {
-      if (brick6 == 1) return launch_laplace6<4, 2, 2, 2>(c, src, dst, tau_scale, part, st);
-      if (brick6 == 2) return launch_laplace6<4, 4, 4, 2>(c, src, dst, tau_scale, part, st);
-      return launch_laplace6<4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
-    }
-    if (c->n == 3) {
-      if (brick6 == 1) return launch_laplace6<3, 4, 2, 2>(c, src, dst, tau_scale, part, st);
-      if (brick6 == 2) return launch_laplace6<3, 4, 4, 4>(c, src, dst, tau_scale, part, st);
-      return launch_laplace6<3, 4, 4, 2>(c, src, dst, tau_scale, part, st);
-    }
-  }
-  if (c->dim == 3 && part == 0 && variant == 30) {  // persistent pipelined
-    if (c->n == 5) return launch_laplace_persist<5, 4, 2, 2>(c, src, dst, tau_scale, st);
-    if (c->n == 3) return launch_laplace_persist<3, 4, 4, 4>(c, src, dst, tau_scale, st);
-  }
-  if (c->dim == 3 && variant == 20) {  // barrier-free warp-per-cell kernel
-    if (c->n == 3) return launch_laplace_warp<3, 4, 4, 4, 8>(c, src, dst, tau_scale, part, st);
-    if (c->n == 4) return launch_laplace_warp<4, 4, 4, 4, 8>(c, src, dst, tau_scale, part, st);
-    if (c->n == 5) return launch_laplace_warp<5, 4, 4, 2, 8>(c, src, dst, tau_scale, part, st);
+  if (c->dim == 3 && variant == 6) {  // register-plane kernel at k = 2, 3 (experiment)
+    if (c->n == 4) return launch_laplace6<4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+    if (c->n == 3) return launch_laplace6<3, 4, 4, 2>(c, src, dst, tau_scale, part, st);
   }
   if (c->dim == 3) {
-    if (c->n == 5 && variant == 1) return launch_laplace<3, 5, 2, 2, 2>(c, src, dst, tau_scale, part, st);
-    if (c->n == 5 && variant == 2) return launch_laplace<3, 5, 4, 4, 1>(c, src, dst, tau_scale, part, st);
-    if (c->n == 5 && variant == 3) return launch_laplace<3, 5, 2, 2, 1>(c, src, dst, tau_scale, part, st);
-    if (c->n == 4 && variant == 1) return launch_laplace<3, 4, 2, 2, 2>(c, src, dst, tau_scale, part, st);
-    if (c->n == 4 && variant == 2) return launch_laplace<3, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
-    if (c->n == 4 && variant == 3) return launch_laplace<3, 4, 4, 4, 1>(c, src, dst, tau_scale, part, st);
     switch (c->n) {
       case 2: return launch_laplace<3, 2, 8, 4, 4>(c, src, dst, tau_scale, part, st);
       case 3: return launch_laplace<3, 3, 4, 4, 4>(c, src, dst, tau_scale, part, st);
