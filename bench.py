@@ -235,6 +235,51 @@ def run_c4_step(nsteps=3):
             "steps": steps}
 
 
+def run_small_configs():
+    """BASELINE configs 1 and 3 (latency / fp64-heavy cases, not roofline
+    configs): C1 8^3 Q3 walls Laplace vmult with both wall kinds; C3
+    convective term 32^3 Q5 periodic [0, 2pi]^3 Taylor-Green + 1e-2 noise
+    (seed 2), n_q = 8 (reference rule) and 9 (BASELINE literal)."""
+    import numpy as np
+    import torch
+    from paper_1607_01323_b200 import mesh as M, operators as ops
+    from paper_1607_01323_b200.spaces import DgSpace
+
+    def timeit(f, reps=50):
+        f()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    out = {}
+    mesh = M.build_box_mesh(((0, 1),) * 3, (8, 8, 8))
+    space = DgSpace(mesh, 3)
+    p = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, space.n_dofs), device="cuda")
+    for kind, bc in (("dirichlet", ops.DirichletBC(None)), ("neumann", ops.NeumannBC(None, None))):
+        bcs = ops.BoundarySpec({t: bc for t in mesh.boundary_tags()}).resolve(space)
+        ms = timeit(lambda: ops.apply_pressure_laplace(space, p, bcs))
+        out[f"C1_{kind}_walls"] = {"dofs": space.n_dofs, "ms": ms, "dof_per_s": space.n_dofs / ms * 1e3}
+    mesh = M.build_box_mesh(((0, 2 * np.pi),) * 3, (32, 32, 32), periodic=(True, True, True))
+    for nq in (8, 9):
+        space = DgSpace(mesh, 5, n_q_over=nq)
+        x, y, z = space.node_coords()
+        rng = np.random.default_rng(2)
+        u = np.stack([np.sin(x) * np.cos(y) * np.cos(z), -np.cos(x) * np.sin(y) * np.cos(z), 0 * z])
+        u = u + 1e-2 * rng.uniform(-1, 1, u.shape)
+        ud = torch.as_tensor(u.ravel(), device="cuda")
+        bcs = ops.BoundarySpec({}).resolve(space)
+        ms = timeit(lambda: ops.eval_convective_rhs(space, bcs, [ud], (1.0,), (0.0,), 0.0), 10)
+        out[f"C3_convective_nq{nq}"] = {"velocity_dofs": 3 * space.n_dofs, "ms": ms,
+                                       "dof_per_s": 3 * space.n_dofs / ms * 1e3,
+                                       "bytes_per_dof": 16.0}
+    return out
+
+
 def run_cg(dist_on):
     """BASELINE config 2: 32^3, Q4, periodic x,z, walls y, pure Neumann,
     rhs = zero_mean_project_dual(M (sin 2pi x cos pi y sin 2pi z + 1e-3 N(0,1),
@@ -408,6 +453,9 @@ def main():
     step = None
     if rank == 0 and world == 1 and not args.no_step:
         step = run_c4_step()
+    small = None
+    if rank == 0 and world == 1 and not args.no_step:
+        small = run_small_configs()
     sweep = []
     if rank == 0 and world == 1 and args.sweep:
         sweep = run_sweep()
@@ -459,6 +507,8 @@ def main():
             line["cg"] = cg
         if step:
             line["c4_step"] = step
+        if small:
+            line["configs"] = small
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

@@ -217,6 +217,13 @@ int dg_laplace_pcg(dg_ctx *ctx, const double *b, double *x,
                    const double *diag, const dg_pcg_params *prm,
                    dg_pcg_stats *stats, double *hist_host, void *stream);
 
+/* One Chebyshev step (solvers.py:121-128) fused into the vmult epilogue:
+ * rc -= L d_old ; d_new = a d_old + b rc/diag ; x += d_new.  The vector
+ * update rounds like the reference's numpy expression (no FMA contraction). */
+int dg_cheb_step(dg_ctx *ctx, const double *d_old, double *d_new, double *rc,
+                 double *x, const double *diag, double a, double b,
+                 double tau_scale, void *stream);
+
 /* ---- geometric multigrid (multigrid.py:33-151, mesh.py:354-374) ---------
  * Levels are contexts of nested boxes (counts doubling per axis, same dim,
  * degree, periodicity and boundary kinds), coarse (0) to fine. */

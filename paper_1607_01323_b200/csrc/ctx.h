@@ -40,9 +40,6 @@ struct dg_ctx {
   std::vector<double *> work;  // solver work vectors (n_dofs each)
   double *d_partials = nullptr;  // per-brick partial sums of the fused vmult epilogue
   int64_t partials_n = 0;
-  // chunked vmult (z-range of cell layers, multiple of 4) for the pipelined
-  // host-buffer path; zc1 <= 0: whole mesh
-  int zc0 = 0, zc1 = 0;
   double *d_hin = nullptr, *d_hout = nullptr;   // device staging of dg_laplace_vmult_host
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   std::mutex mu;

@@ -287,12 +287,20 @@ static LapTab<N> lap_tab(const Basis1D &b) {
   return t;
 }
 
-// z-bricks of a launch: the ctx's chunk (cell layers [zc0, zc1), zc0 a
-// multiple of 4 >= BZ) for the pipelined host-buffer vmult, else all
+// z-range of cell layers [z0, z1) of the vmult being launched by this host
+// thread (the pipelined host-buffer path; z1 <= 0: whole mesh).  Thread-local,
+// so concurrent calls on other threads are unaffected.
+struct ZChunk {
+  int z0 = 0, z1 = 0;
+};
+static thread_local ZChunk t_chunk;
+
+// z-bricks of a launch: the current chunk (z0 a multiple of 4 >= BZ), else all
 static unsigned chunk_bricks_z(const dg_ctx *c, int BZ, Geo &g) {
-  if (c->zc1 > 0) {
-    g.bz0 = c->zc0 / BZ;
-    return (unsigned)((c->zc1 - c->zc0 + BZ - 1) / BZ);
+  (void)c;
+  if (t_chunk.z1 > 0) {
+    g.bz0 = t_chunk.z0 / BZ;
+    return (unsigned)((t_chunk.z1 - t_chunk.z0 + BZ - 1) / BZ);
   }
   g.bz0 = 0;
   return (unsigned)((g.nz + BZ - 1) / BZ);
@@ -531,10 +539,10 @@ int dg_laplace_vmult_host(dg_ctx *c, const double *src_host, double *dst_host, d
   for (int i = 0; i < nch && rc == DG_OK; ++i) {
     DG_CUDA_CHECK(cudaStreamWaitEvent(st, eh[std::min(i + 1, nch - 1)], 0));
     if (zper && i == 0) DG_CUDA_CHECK(cudaStreamWaitEvent(st, eh[nch - 1], 0));
-    c->zc0 = i * layers;
-    c->zc1 = nch > 1 ? std::min(nz, c->zc0 + layers) : 0;
+    t_chunk.z0 = i * layers;
+    t_chunk.z1 = nch > 1 ? std::min(nz, t_chunk.z0 + layers) : 0;
     rc = laplace_dispatch(c, c->d_hin, c->d_hout, tau_scale, 0, st);
-    c->zc0 = c->zc1 = 0;
+    t_chunk = ZChunk{};
     if (rc) break;
     DG_CUDA_CHECK(cudaEventRecord(ec[i], st));
     DG_CUDA_CHECK(cudaStreamWaitEvent(c->s_d2h, ec[i], 0));

@@ -350,3 +350,41 @@ def projection_element_pcg(space, b, tau_d, rel_tol: float = 1e-12, max_iter: in
               ctypes_ptr(iters.data_ptr()), ctypes_ptr(conv.data_ptr()), _stream())
     del keep
     return a.result(x), iters.cpu().numpy().astype(int), conv.cpu().numpy().astype(bool)
+
+
+def laplace_chebyshev_smooth(space, bcs, diag, cfg: ChebyshevConfig, rhs, x=None,
+                             degree: Optional[int] = None, tau_scale: float = 1.0):
+    """chebyshev_smooth(L, diag, cfg, rhs, x) (solvers.py:93-129) for the SIP
+    Laplacian with every step one fused kernel (dg_cheb_step: vmult +
+    Chebyshev update in the epilogue).  Device tensors (element-major)."""
+    torch = _torch()
+    deg = cfg.degree if degree is None else degree
+    rhs = _to_dev(rhs).reshape(-1)
+    diag = _to_dev(diag).reshape(-1)
+    if x is None:
+        x = torch.zeros_like(rhs)
+        r = rhs.clone()
+    else:
+        x = _to_dev(x).reshape(-1).clone()
+        if deg == 0:
+            return x
+        r = rhs - apply_pressure_laplace(space, x, bcs, tau_scale)
+    if deg == 0:
+        return x
+    lmax = cfg.lambda_max
+    lmin = lmax / cfg.smoothing_range
+    theta, delta = 0.5 * (lmax + lmin), 0.5 * (lmax - lmin)
+    sigma1 = theta / delta
+    rho = 1.0 / sigma1
+    d = (r / diag) / theta
+    x += d
+    d2 = torch.empty_like(d)
+    ctx = space.ctx(bcs.kinds)
+    for _ in range(deg - 1):
+        rho_new = 1.0 / (2.0 * sigma1 - rho)
+        _lib.call("dg_cheb_step", ctx.handle, ctypes_ptr(d.data_ptr()), ctypes_ptr(d2.data_ptr()),
+                  ctypes_ptr(r.data_ptr()), ctypes_ptr(x.data_ptr()), ctypes_ptr(diag.data_ptr()),
+                  float(rho_new * rho), float(2.0 * rho_new / delta), float(tau_scale), _stream())
+        d, d2 = d2, d
+        rho = rho_new
+    return x

@@ -293,3 +293,23 @@ def test_host_buffer_vmult_matches_device(per, k):
         got = ops.apply_pressure_laplace(space, h, bcs)
         assert got.device.type == "cpu" and torch.equal(got, want), chunks
     ops.HOST_CHUNKS = 32
+
+
+@pytest.mark.parametrize("k", [1, 3, 4, 6])
+def test_fused_chebyshev_smooth_matches_generic(k):
+    """dg_cheb_step (vmult + Chebyshev update in one kernel) == the
+    reference-form chebyshev_smooth with the Laplace callable."""
+    from paper_1607_01323_b200 import operators as ops
+    mesh = M.build_box_mesh(((0, 1), (0, 2), (0, 1)), (4, 3, 4), periodic=(True, False, True))
+    space = DgSpace(mesh, k)
+    bcs = ops.BoundarySpec({"ymin": ops.DirichletBC(None), "ymax": ops.NeumannBC(None, None)}
+                           ).resolve(space)
+    diag = ops.laplace_diagonal(space, bcs)
+    cfg = sol.ChebyshevConfig(5, 20.0, 2.7)
+    b = torch.rand(space.n_dofs, dtype=torch.float64, device="cuda")
+    x0 = torch.rand(space.n_dofs, dtype=torch.float64, device="cuda")
+    L = lambda v: ops.apply_pressure_laplace(space, v, bcs)
+    for xin in (None, x0):
+        want = sol.chebyshev_smooth(L, diag, cfg, b, xin)
+        got = sol.laplace_chebyshev_smooth(space, bcs, diag, cfg, b, xin)
+        assert relerr(got.cpu().numpy(), want.cpu().numpy()) < 1e-13
