@@ -23,7 +23,7 @@ BC_NONE, BC_VELOCITY_DIRICHLET, BC_VELOCITY_NEUMANN = 0, 1, 2
 
 
 def sources():
-    names = ["dgmf.cu", "vecops.cu", "vec_over.cu", "tables.cpp"]
+    names = ["dgmf.cu", "vecops.cu", "vec_over.cu", "vcart.cu", "tables.cpp"]
     names += [f"vec_lin{d}_{p}.cu" for d in (2, 3) for p in ("00", "01", "10", "11")]
     return [os.path.join(CSRC, f) for f in names]
 

@@ -42,6 +42,8 @@ struct dg_ctx {
   int64_t partials_n = 0;
   double *d_hin = nullptr, *d_hout = nullptr;   // device staging of dg_laplace_vmult_host
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  double *d_trc = nullptr;  // face traces of the Cartesian vector operators (vcart.cu)
+  int64_t trc_n = 0;
   std::mutex mu;
 
   dg::Geo geo() const {

@@ -234,6 +234,7 @@ int dg_ctx_destroy(dg_ctx *c) {
   if (c->h_scal) cudaFreeHost(c->h_scal);
   for (double *w : c->work) cudaFree(w);
   cudaFree(c->d_partials);
+  cudaFree(c->d_trc);
   delete c;
   return DG_OK;
 }

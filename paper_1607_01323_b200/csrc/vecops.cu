@@ -10,6 +10,12 @@
 
 using namespace dg;
 
+namespace dg {
+// Cartesian fast path of the Helmholtz / projection operators (vcart.cu)
+int vcart_apply(dg_ctx *c, int op, const double *src, double *dst, double gamma0_dt, double nu,
+                const double *tau_d, const double *tau_c, cudaStream_t st);
+}  // namespace dg
+
 // operators on the linear rule (n_q = k+1); CI / CO: 0 = dim components,
 // 1 = scalar (instantiated in vec_lin<dim>_<CI><CO>.cu)
 template <int CI, int CO>
@@ -43,6 +49,8 @@ extern "C" int dg_helmholtz_vmult(dg_ctx *c, const double *src, double *dst, dou
   prm.op = kOpHelmholtz;
   prm.gamma0_dt = gamma0_dt;
   prm.nu = nu;
+  const int rc = vcart_apply(c, 0, src, dst, gamma0_dt, nu, nullptr, nullptr, (cudaStream_t)stream);
+  if (rc != DG_ENOTSUP) return rc;
   return vecop_linear<0, 0>(c, src, dst, prm, (cudaStream_t)stream);
 }
 
@@ -54,6 +62,8 @@ extern "C" int dg_projection_vmult(dg_ctx *c, const double *src, double *dst,
   prm.op = kOpProjection;
   prm.tau_d = tau_d;
   prm.tau_c = tau_c;
+  const int rc = vcart_apply(c, 1, src, dst, 0.0, 0.0, tau_d, tau_c, (cudaStream_t)stream);
+  if (rc != DG_ENOTSUP) return rc;
   return vecop_linear<0, 0>(c, src, dst, prm, (cudaStream_t)stream);
 }
 
