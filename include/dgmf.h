@@ -217,6 +217,18 @@ int dg_laplace_pcg(dg_ctx *ctx, const double *b, double *x,
                    const double *diag, const dg_pcg_params *prm,
                    dg_pcg_stats *stats, double *hist_host, void *stream);
 
+/* PCG of the velocity solves (solvers.py:30-73 with prec = inverse_mass_apply,
+ * operators.py:176-181): op 0 = viscous Helmholtz (gamma0_dt, nu; the
+ * context's boundary kinds), op 1 = projection (tau_d per cell, tau_c in the
+ * layout of dg_projection_vmult; either NULL to skip).  3D, 3 components.
+ * x: initial guess in, solution out (reference x0 semantics; zeros = None).
+ * Reference stopping rule sqrt(r.z) <= max(rel_tol sqrt(r0.z0), abs_tol),
+ * breakdown flags, residual history as dg_laplace_pcg.  Blocking. */
+int dg_vector_pcg(dg_ctx *ctx, int op, double gamma0_dt, double nu,
+                  const double *tau_d, const double *tau_c, const double *b,
+                  double *x, double rel_tol, double abs_tol, int max_iter,
+                  dg_pcg_stats *stats, double *hist_host, void *stream);
+
 /* One Chebyshev step (solvers.py:121-128) fused into the vmult epilogue:
  * rc -= L d_old ; d_new = a d_old + b rc/diag ; x += d_new.  The vector
  * update rounds like the reference's numpy expression (no FMA contraction). */

@@ -127,6 +127,8 @@ PROTOTYPES = {
     "dg_laplace_pcg": [_P, _P, _P, _P, ctypes.POINTER(PcgParams),
                        ctypes.POINTER(PcgStats), _DP, _P],
     "dg_cheb_step": [_P, _P, _P, _P, _P, _P, _D, _D, _D, _P],
+    "dg_vector_pcg": [_P, ctypes.c_int, _D, _D, _P, _P, _P, _P, _D, _D, ctypes.c_int,
+                      ctypes.POINTER(PcgStats), _DP, _P],
     "dg_laplace_pcg_mg": [_P, _P, _P, _P, ctypes.POINTER(PcgParams),
                           ctypes.POINTER(PcgStats), _DP, _P],
     "dg_mg_prolong": [_P, _P, _P, _P, _I, _P],

@@ -44,6 +44,10 @@ struct dg_ctx {
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   double *d_trc = nullptr;  // face traces of the Cartesian vector operators (vcart.cu)
   int64_t trc_n = 0;
+  std::vector<double *> vwork;  // vector-PCG work vectors (vwork_n doubles each)
+  int64_t vwork_n = 0;
+  double *d_vpart = nullptr;    // per-CTA partial sums of the vector-PCG update
+  int64_t vpart_n = 0;
   std::mutex mu;
 
   dg::Geo geo() const {

@@ -235,6 +235,8 @@ int dg_ctx_destroy(dg_ctx *c) {
   for (double *w : c->work) cudaFree(w);
   cudaFree(c->d_partials);
   cudaFree(c->d_trc);
+  for (double *w : c->vwork) cudaFree(w);
+  cudaFree(c->d_vpart);
   delete c;
   return DG_OK;
 }

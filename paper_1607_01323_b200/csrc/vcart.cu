@@ -1,9 +1,12 @@
 // Host side of the Cartesian vector-operator fast path (vcart.cuh): tables,
 // the per-context trace buffer, launches.  Own translation unit of libdgmf.
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "ctx.h"
 #include "vcart.cuh"
+#include "vector.cuh"
 
 namespace dg {
 
@@ -88,3 +91,174 @@ int vcart_apply(dg_ctx *c, int op, const double *src, double *dst, double gamma0
 }
 
 }  // namespace dg
+
+// ---------------------------------------------------------------------------
+// M^-1-preconditioned CG of the velocity solves (viscous Helmholtz,
+// projection), the reference pcg (solvers.py:30-73) with
+// prec = inverse_mass_apply, run on the device: the operator is the fast
+// path above, the x / r update, the exact inverse mass and the r.z partial
+// sums are one kernel (vpcg_update_kernel), reductions are deterministic,
+// the host reads two scalars per iteration.
+
+namespace dg {
+
+__global__ void vpcg_sub_kernel(double *__restrict__ r, const double *__restrict__ b,
+                                const double *__restrict__ y, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    r[i] = __dsub_rn(b[i], y[i]);
+}
+
+// p = z + beta p ; scal[0] = rz_new
+__global__ void vpcg_p_kernel(double *__restrict__ p, const double *__restrict__ z, double beta,
+                              double rz_new, double *__restrict__ scal, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+  if (blockIdx.x == 0 && threadIdx.x == 0) scal[0] = rz_new;
+}
+
+static int vgrid(int64_t n) {
+  const int64_t b = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
+}
+
+static int ensure_vwork(dg_ctx *c, int nvec, int64_t per) {
+  if (c->vwork_n < per) {
+    for (double *w : c->vwork) cudaFree(w);
+    c->vwork.clear();
+    c->vwork_n = per;
+  }
+  while ((int)c->vwork.size() < nvec) {
+    double *p = nullptr;
+    DG_CUDA_CHECK(cudaMalloc((void **)&p, sizeof(double) * (size_t)std::max<int64_t>(per, 1)));
+    c->vwork.push_back(p);
+  }
+  return DG_OK;
+}
+
+template <int N>
+static int launch_vpcg_update(dg_ctx *c, double *x, double *r, const double *p, const double *Ap,
+                              double *z, const double *scal, cudaStream_t st, int *nblocks) {
+  using C = VcCfg<N>;
+  MinvTab<N> mi;
+  for (int i = 0; i < N * N; ++i) mi.A[i] = c->basis.Minv[i];
+  const int64_t nb = (c->n_cells + C::CPB - 1) / C::CPB;
+  if (c->vpart_n < nb) {
+    cudaFree(c->d_vpart);
+    c->d_vpart = nullptr;
+    c->vpart_n = 0;
+    DG_CUDA_CHECK(cudaMalloc((void **)&c->d_vpart, sizeof(double) * (size_t)nb));
+    c->vpart_n = nb;
+  }
+  *nblocks = (int)nb;
+  if (nb == 0) return DG_OK;
+  vpcg_update_kernel<N><<<(unsigned)nb, ((C::THREADS + 31) / 32) * 32, 0, st>>>(
+      x, r, p, Ap, z, scal, mi, c->geo(), c->n_cells, c->d_vpart);
+  DG_LAUNCH_CHECK("vpcg_update_kernel");
+  return DG_OK;
+}
+
+static int vpcg_update(dg_ctx *c, double *x, double *r, const double *p, const double *Ap, double *z,
+                       const double *scal, cudaStream_t st, int *nblocks) {
+#define DG_U(NN) \
+  case NN: return launch_vpcg_update<NN>(c, x, r, p, Ap, z, scal, st, nblocks);
+  switch (c->n) { DG_U(2) DG_U(3) DG_U(4) DG_U(5) DG_U(6) DG_U(7) DG_U(8) }
+#undef DG_U
+  return inval("unsupported degree");
+}
+
+}  // namespace dg
+
+using namespace dg;
+
+extern "C" int dg_vector_pcg(dg_ctx *c, int op, double gamma0_dt, double nu, const double *tau_d,
+                             const double *tau_c, const double *b, double *x, double rel_tol,
+                             double abs_tol, int max_iter, dg_pcg_stats *stats, double *hist,
+                             void *stream) {
+  if (!c || !b || !x || !stats) return inval("null argument");
+  if (op != 0 && op != 1) return inval("vector PCG: op 0 (viscous Helmholtz) or 1 (projection)");
+  if (c->dim != 3) return inval("vector PCG: 3D contexts");
+  if (c->mode[0] == kGhost || c->mode[1] == kGhost)
+    return inval("vector PCG runs on whole-mesh contexts");
+  if (max_iter < 0) return inval("max_iter must be >= 0");
+  std::lock_guard<std::mutex> lock(c->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = 3 * c->n_dofs;
+  int rc = ensure_vwork(c, 4, n);
+  if (rc) return rc;
+  double *r = c->vwork[0], *z = c->vwork[1], *p = c->vwork[2], *Ap = c->vwork[3];
+  double *scal = c->d_scal + 10;  // [rz, pAp, rz_new]
+  double *hs = c->h_scal + 10;
+  auto apply = [&](const double *src, double *dst) {
+    return op == 0 ? dg_helmholtz_vmult(c, src, dst, gamma0_dt, nu, stream)
+                   : dg_projection_vmult(c, src, dst, tau_d, tau_c, stream);
+  };
+  const int gb = vgrid(n);
+  // r = b - A x0 ; z = M^-1 r ; rz
+  if ((rc = apply(x, Ap))) return rc;
+  vpcg_sub_kernel<<<gb, 256, 0, st>>>(r, b, Ap, n);
+  DG_LAUNCH_CHECK("vpcg_sub_kernel");
+  if ((rc = dg_inverse_mass(c, r, z, 3, stream))) return rc;
+  dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(r, z, n, c->d_red);
+  sum_partials_kernel<<<1, 1024, 0, st>>>(c->d_red, kRedBlocks, scal + 0);
+  DG_LAUNCH_CHECK("dot");
+  DG_CUDA_CHECK(cudaMemcpyAsync(hs, scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+  DG_CUDA_CHECK(cudaStreamSynchronize(st));
+  double rz = hs[0];
+  stats->iterations = 0;
+  stats->converged = 0;
+  stats->breakdown = 0;
+  if (rz < 0) {
+    stats->residual = std::sqrt(std::fabs(rz));
+    stats->breakdown = 1;
+    return DG_OK;
+  }
+  const double norm0 = std::sqrt(rz);
+  const double tol = std::max(rel_tol * norm0, abs_tol);
+  if (hist) hist[0] = norm0;
+  double norm = norm0;
+  stats->residual = norm0;
+  if (norm0 <= tol) {
+    stats->converged = 1;
+    return DG_OK;
+  }
+  DG_CUDA_CHECK(cudaMemcpyAsync(p, z, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  for (int it = 1; it <= max_iter; ++it) {
+    if ((rc = apply(p, Ap))) return rc;
+    dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(p, Ap, n, c->d_red);
+    sum_partials_kernel<<<1, 1024, 0, st>>>(c->d_red, kRedBlocks, scal + 1);
+    DG_LAUNCH_CHECK("dot");
+    int nb = 0;
+    if ((rc = vpcg_update(c, x, r, p, Ap, z, scal, st, &nb))) return rc;
+    sum_partials_kernel<<<1, 1024, 0, st>>>(c->d_vpart, nb, scal + 2);
+    DG_LAUNCH_CHECK("sum_partials_kernel");
+    DG_CUDA_CHECK(cudaMemcpyAsync(hs + 1, scal + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    DG_CUDA_CHECK(cudaStreamSynchronize(st));
+    const double pAp = hs[1];
+    if (pAp <= 0.0) {  // the update kernel left x, r untouched
+      stats->iterations = it;
+      stats->residual = norm;
+      stats->breakdown = 1;
+      return DG_OK;
+    }
+    const double rz_new = hs[2];
+    norm = std::sqrt(std::max(rz_new, 0.0));
+    if (hist) hist[it] = norm;
+    stats->iterations = it;
+    stats->residual = norm;
+    if (norm <= tol) {
+      stats->converged = 1;
+      return DG_OK;
+    }
+    if (rz_new <= 0.0) {
+      stats->breakdown = 1;
+      return DG_OK;
+    }
+    vpcg_p_kernel<<<gb, 256, 0, st>>>(p, z, rz_new / rz, rz_new, scal, n);
+    DG_LAUNCH_CHECK("vpcg_p_kernel");
+    rz = rz_new;
+  }
+  return DG_OK;
+}
+

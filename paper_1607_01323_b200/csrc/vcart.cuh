@@ -414,4 +414,88 @@ vc_apply_kernel(const double *__restrict__ u, const double *__restrict__ trc,
   }
 }
 
+// One M^-1-preconditioned CG update of the velocity solves (solvers.py:56-67
+// with prec = inverse_mass_apply), fused per cell:
+//   alpha = rz / pAp;  x += alpha p;  r -= alpha Ap;  z = M^-1 r;  partial r.z
+// M^-1 = (Minv x Minv x Minv) / det with the same sweep order (x, y, z) and
+// scale as dg_inverse_mass (tensor.cuh).  One thread per node, CPB cells per
+// CTA; per-CTA partial sums are added in fixed order by a second kernel.
+template <int N>
+struct MinvTab {
+  double A[N * N];
+};
+
+template <int N>
+__global__ void __launch_bounds__(((VcCfg<N>::THREADS + 31) / 32) * 32)
+vpcg_update_kernel(double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
+                   const double *__restrict__ Ap, double *__restrict__ z,
+                   const double *__restrict__ scal, const __grid_constant__ MinvTab<N> mi,
+                   const Geo g, const int64_t ncells, double *__restrict__ partials) {
+  using C = VcCfg<N>;
+  constexpr int P = C::P;
+  __shared__ double buf[2][C::CPB * 3 * P];
+  __shared__ double red[32];
+  if (!(scal[1] > 0.0)) return;  // breakdown: the host stops, x and r stay
+  const double alpha = __ddiv_rn(scal[0], scal[1]);
+  // blockDim = THREADS rounded up to whole warps (full-mask shuffles below);
+  // the padding threads own no node
+  const bool in = threadIdx.x < C::THREADS;
+  const int cs = in ? threadIdx.x / P : 0, q = in ? threadIdx.x % P : 0;
+  const int x0 = q % N, y0 = (q / N) % N, z0 = q / (N * N);
+  const int64_t e = (int64_t)blockIdx.x * C::CPB + cs;
+  const bool valid = in && e < ncells;
+  double *b0 = buf[0] + cs * 3 * P, *b1 = buf[1] + cs * 3 * P;
+  double rv[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int64_t i = ((int64_t)c * ncells + e) * P + q;
+    double v = 0.0;
+    if (valid) {
+      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+      v = __dsub_rn(r[i], __dmul_rn(alpha, Ap[i]));
+      r[i] = v;
+    }
+    rv[c] = v;
+    if (in) b0[c * P + q] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double t = vc_dot<N, 0>(mi.A + x0 * N, 1, b0 + c * P, x0, y0, z0);
+    if (in) b1[c * P + q] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double t = vc_dot<N, 1>(mi.A + y0 * N, 1, b1 + c * P, x0, y0, z0);
+    if (in) b0[c * P + q] = t;
+  }
+  __syncthreads();
+  double acc = 0.0;
+  if (valid) {
+    const int ix = (int)(e % g.nx), iy = (int)((e / g.nx) % g.ny), iz = (int)(e / ((int64_t)g.nx * g.ny));
+    double s = 0.5 * g.hx[ix] * 0.5 * g.hy[iy];
+    s *= 0.5 * g.hz[iz];
+    s = 1.0 / s;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double zv = s * vc_dot<N, 2>(mi.A + z0 * N, 1, b0 + c * P, x0, y0, z0);
+      z[((int64_t)c * ncells + e) * P + q] = zv;
+      acc += rv[c] * zv;
+    }
+  }
+  // deterministic block sum
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[w] = acc;
+  __syncthreads();
+  if (w == 0) {
+    acc = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) partials[blockIdx.x] = acc;
+  }
+}
+
 }  // namespace dg

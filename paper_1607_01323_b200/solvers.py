@@ -388,3 +388,50 @@ def laplace_chebyshev_smooth(space, bcs, diag, cfg: ChebyshevConfig, rhs, x=None
         d, d2 = d2, d
         rho = rho_new
     return x
+
+
+def _vector_pcg(space, op, kinds, gamma0_dt, nu, tau_d, tau_c, b, x0, rel_tol, abs_tol, max_iter):
+    torch = _torch()
+    bt = _to_dev(b).contiguous().reshape(-1)
+    if bt.numel() != 3 * space.n_dofs:
+        raise ValueError(f"expected {3 * space.n_dofs} values, got {bt.numel()}")
+    x = torch.zeros_like(bt) if x0 is None else _to_dev(x0).reshape(-1).clone()
+    st = _lib.PcgStats()
+    hist = np.zeros(max_iter + 1)
+    ctx = space.ctx(kinds)
+    keep = [t.contiguous() if t is not None else None for t in (tau_d, tau_c)]
+    ptr = lambda t: ctypes_ptr(t.data_ptr() if t is not None else 0)
+    _lib.call("dg_vector_pcg", ctx.handle, int(op), float(gamma0_dt), float(nu), ptr(keep[0]),
+              ptr(keep[1]), ctypes_ptr(bt.data_ptr()), ctypes_ptr(x.data_ptr()), float(rel_tol),
+              float(abs_tol), int(max_iter), ctypes.byref(st),
+              hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream())
+    stats = SolverStats(st.iterations, st.residual, bool(st.converged), bool(st.breakdown),
+                        list(hist[:st.iterations + 1]))
+    return x.view(b.shape) if hasattr(b, "shape") else x, stats
+
+
+def helmholtz_pcg(space, bcs, b, gamma0_dt: float, nu: float, x0=None, rel_tol: float = 1e-8,
+                  abs_tol: float = 0.0, max_iter: int = 1000):
+    """``pcg(lambda v: apply_viscous_helmholtz(space, v, gamma0_dt, nu, bcs),
+    lambda r: inverse_mass_apply(space, r), b, x0, ...)`` (solvers.py:30-73,
+    operators.py:418-491) as one device call (dg_vector_pcg): fast-path
+    operator, fused update / inverse mass / r.z kernel.  3D, device tensors."""
+    return _vector_pcg(space, 0, bcs.kinds, gamma0_dt, nu, None, None, b, x0, rel_tol, abs_tol,
+                       max_iter)
+
+
+def projection_pcg(space, b, tau_d=None, tau_c=None, x0=None, rel_tol: float = 1e-8,
+                   abs_tol: float = 0.0, max_iter: int = 1000):
+    """``pcg(lambda w: apply_projection_operator(space, w, tau_d, tau_c),
+    lambda r: inverse_mass_apply(space, r), b, x0, ...)`` (operators.py:372-412)
+    as one device call.  tau_d per cell, tau_c in the device face layout
+    [d*ne + e] (compute_penalty_parameters returns both)."""
+    torch = _torch()
+    td = None if tau_d is None else _to_dev(tau_d).reshape(-1)
+    tc = None
+    if tau_c is not None:
+        from .operators import face_penalty_layout
+        tc = tau_c if isinstance(tau_c, torch.Tensor) else face_penalty_layout(space, tau_c)
+        tc = _to_dev(tc).reshape(-1)
+    return _vector_pcg(space, 1, space.default_kinds(), 0.0, 0.0, td, tc, b, x0, rel_tol,
+                       abs_tol, max_iter)

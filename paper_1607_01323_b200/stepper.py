@@ -148,9 +148,13 @@ class VelocityCorrection:
                 uhh, its, _ = sol.projection_element_pcg(sp, rhs, tau_d, rel_tol=cfg.rel_tol_proj)
                 it["projection"] = int(its.max())
             else:
-                uhh, st = sol.pcg(lambda w: ops.apply_projection_operator(sp, w, tau_d, tau_c),
-                                  lambda r: ops.inverse_mass_apply(sp, r), rhs, x0=uhat,
-                                  rel_tol=cfg.rel_tol_proj, max_iter=cfg.max_iter)
+                if self.fused and sp.dim == 3:
+                    uhh, st = sol.projection_pcg(sp, rhs, tau_d, tau_c, x0=uhat,
+                                                 rel_tol=cfg.rel_tol_proj, max_iter=cfg.max_iter)
+                else:
+                    uhh, st = sol.pcg(lambda w: ops.apply_projection_operator(sp, w, tau_d, tau_c),
+                                      lambda r: ops.inverse_mass_apply(sp, r), rhs, x0=uhat,
+                                      rel_tol=cfg.rel_tol_proj, max_iter=cfg.max_iter)
                 it["projection"] = st.iterations
         t0 = mark("projection", t0)
         # (d) viscous step
@@ -158,9 +162,13 @@ class VelocityCorrection:
         if bcs.dirichlet or bcs.neumann:
             rhs = rhs + ops.viscous_rhs_bc(sp, bcs, t_np1, nu, like="device").view(rhs.shape)
         u0 = sum(be[i] * hist_u[i] for i in range(J))
-        u, st = sol.pcg(lambda v: ops.apply_viscous_helmholtz(sp, v, g0 / dt, nu, bcs),
-                        lambda r: ops.inverse_mass_apply(sp, r), rhs, x0=u0,
-                        rel_tol=cfg.rel_tol_v, max_iter=cfg.max_iter)
+        if self.fused and sp.dim == 3:
+            u, st = sol.helmholtz_pcg(sp, bcs, rhs, g0 / dt, nu, x0=u0, rel_tol=cfg.rel_tol_v,
+                                      max_iter=cfg.max_iter)
+        else:
+            u, st = sol.pcg(lambda v: ops.apply_viscous_helmholtz(sp, v, g0 / dt, nu, bcs),
+                            lambda r: ops.inverse_mass_apply(sp, r), rhs, x0=u0,
+                            rel_tol=cfg.rel_tol_v, max_iter=cfg.max_iter)
         it["viscous"] = st.iterations
         w = ops.compute_vorticity(sp, u)
         mark("viscous", t0)
