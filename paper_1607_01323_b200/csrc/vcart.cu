@@ -5,7 +5,7 @@
 #include <cstdlib>
 
 #include "ctx.h"
-#include "vcart.cuh"
+#include "vcart2.cuh"
 #include "vector.cuh"
 
 namespace dg {
@@ -43,30 +43,32 @@ static int ensure_trc(dg_ctx *c, int64_t n) {
 template <int N, int OP>
 static int launch_vc(dg_ctx *c, const double *src, double *dst, double gamma0_dt, double nu,
                      const double *tau_d, const double *tau_c, cudaStream_t st) {
-  using C = VcCfg<N>;
+  using C = VlCfg<N>;
   static const VcTab<N> tab = vc_tab<N>(c->basis);  // depends on k only
-  auto ktr = vc_trace_kernel<N, OP == kVcHelmholtz>;
-  auto kap = vc_apply_kernel<N, OP>;
+  auto ktr = vl_trace_kernel<N, OP == kVcHelmholtz>;
+  auto kap = vl_apply_kernel<N, OP>;
   static bool attr = false;
   if (!attr) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(ktr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     DG_CUDA_CHECK(cudaFuncSetAttribute(kap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    DG_CUDA_CHECK(cudaFuncSetAttribute(ktr, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    DG_CUDA_CHECK(cudaFuncSetAttribute(kap, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
   if (c->n_cells == 0) return DG_OK;
   const bool faces = OP == kVcHelmholtz ? nu != 0.0 : tau_c != nullptr;
   if (faces) {
-    if (int rc = ensure_trc(c, c->n_cells * C::TRC)) return rc;
+    if (int rc = ensure_trc(c, c->n_cells * 36 * N * N)) return rc;
   }
   const unsigned grid = (unsigned)((c->n_cells + C::CPB - 1) / C::CPB);
   const Geo g = c->geo();
   if (faces) {
     ktr<<<grid, C::THREADS, C::SMEM, st>>>(src, c->d_trc, g, tab, c->n_cells);
-    DG_LAUNCH_CHECK("vc_trace_kernel");
+    DG_LAUNCH_CHECK("vl_trace_kernel");
   }
   kap<<<grid, C::THREADS, C::SMEM, st>>>(src, c->d_trc, dst, g, tab, gamma0_dt, nu, tau_d, tau_c,
                                           c->n_cells);
-  DG_LAUNCH_CHECK("vc_apply_kernel");
+  DG_LAUNCH_CHECK("vl_apply_kernel");
   return DG_OK;
 }
 
