@@ -264,6 +264,40 @@ int dg_laplace_pcg_mg(dg_ctx *ctx, dg_mg *mg, const double *b, double *x,
                       const dg_pcg_params *prm, dg_pcg_stats *stats,
                       double *hist_host, void *stream);
 
+/* ---- general-geometry 2D path (reference geometry.py, operators.py) -----
+ * Quadrilateral meshes with iso-parametric (curved) mappings and arbitrary
+ * conforming connectivity, the reference's own 2D setting.  The caller
+ * computes the geometry at the quadrature points (geometry.py:29-87) and
+ * the per-(cell, slot) links (spaces.py:140-163) and passes DEVICE arrays in
+ * the element-major layouts below; the context keeps the pointers (not
+ * owned) and copies the 1D tables.
+ *   jxw  [e][q][q]        jit  [e][4][q][q] (J^-T entries 00 01 10 11)
+ *   fsj  [e][4][q]        fnrm [e][4][2][q]  fjit [e][4][4][q]
+ *   nbr  [e][4] int64 neighbour cell or -1, nslot / nflip [e][4] int32
+ *   tau  [e]   Eq. 18 per cell (compute_tau_ip, geometry.py:90-108)
+ * On interior faces both cells carry the minus side's sJxW and normal
+ * (negated on the plus side) as the reference's gather/scatter does. */
+typedef struct dg_g2 dg_g2;
+typedef struct {
+  int n, nq;            /* nodes per direction (k+1), Gauss points n_q */
+  int64_t ncells;
+  const double *jxw, *jit, *fsj, *fnrm, *fjit, *tau;   /* device */
+  const int64_t *nbr;                                  /* device */
+  const int *nslot, *nflip;                            /* device */
+  const double *S, *D, *Si, *ld, *rd;                  /* host 1D tables */
+} dg_g2_desc;
+int dg_g2_create(const dg_g2_desc *desc, dg_g2 **out);
+int dg_g2_destroy(dg_g2 *g);
+/* op 0 mass (operators.py:167-173), 1 exact inverse mass (:176-181,
+ * kernels.py:95-107), 2 SIP pressure Laplacian (:187-238) with kind[e][4]
+ * (device int32: 0 interior, DG_BC_VELOCITY_DIRICHLET, DG_BC_VELOCITY_NEUMANN)
+ * and tau_scale; ncomp fields of ncells*n*n values each (mass ops) */
+int dg_g2_apply(dg_g2 *g, int op, double tau_scale, const int *kind,
+                const double *src, double *dst, int ncomp, void *stream);
+/* exact Jacobi diagonal (operators.py:675-730) */
+int dg_g2_laplace_diagonal(dg_g2 *g, double tau_scale, const int *kind,
+                           double *diag, void *stream);
+
 /* ---- multi-GPU x-slabs (ghost cell layers) ------------------------------ */
 /* doubles in one ghost layer: ny*nz cells of one component (n^dim each),
  * ordered by (iz, iy) -- the size of every send/recv buffer below */

@@ -23,7 +23,7 @@ BC_NONE, BC_VELOCITY_DIRICHLET, BC_VELOCITY_NEUMANN = 0, 1, 2
 
 
 def sources():
-    names = ["dgmf.cu", "vecops.cu", "vec_over.cu", "vcart.cu", "tables.cpp"]
+    names = ["dgmf.cu", "vecops.cu", "vec_over.cu", "vcart.cu", "gen2d.cu", "tables.cpp"]
     names += [f"vec_lin{d}_{p}.cu" for d in (2, 3) for p in ("00", "01", "10", "11")]
     return [os.path.join(CSRC, f) for f in names]
 
@@ -90,6 +90,16 @@ class PcgStats(ctypes.Structure):
                 ("converged", ctypes.c_int), ("breakdown", ctypes.c_int)]
 
 
+class G2Desc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("nq", ctypes.c_int), ("ncells", ctypes.c_int64),
+                ("jxw", ctypes.c_void_p), ("jit", ctypes.c_void_p), ("fsj", ctypes.c_void_p),
+                ("fnrm", ctypes.c_void_p), ("fjit", ctypes.c_void_p), ("tau", ctypes.c_void_p),
+                ("nbr", ctypes.c_void_p), ("nslot", ctypes.c_void_p), ("nflip", ctypes.c_void_p),
+                ("S", ctypes.POINTER(ctypes.c_double)), ("D", ctypes.POINTER(ctypes.c_double)),
+                ("Si", ctypes.POINTER(ctypes.c_double)), ("ld", ctypes.POINTER(ctypes.c_double)),
+                ("rd", ctypes.POINTER(ctypes.c_double))]
+
+
 _P = ctypes.c_void_p
 _D = ctypes.c_double
 _I = ctypes.c_int
@@ -135,6 +145,10 @@ PROTOTYPES = {
     "dg_mg_restrict": [_P, _P, _P, _P, _P],
     "dg_mg_create": [_P, _I, _P, _P, _I, _D, _I, _D, _D, ctypes.POINTER(_P)],
     "dg_mg_destroy": [_P],
+    "dg_g2_create": [ctypes.POINTER(G2Desc), ctypes.POINTER(_P)],
+    "dg_g2_destroy": [_P],
+    "dg_g2_apply": [_P, _I, _D, _P, _P, _P, _I, _P],
+    "dg_g2_laplace_diagonal": [_P, _D, _P, _P, _P],
     "dg_mg_vcycle": [_P, _P, _P, _P],
     "dg_halo_count": [_P, ctypes.POINTER(_L)],
     "dg_halo_pack": [_P, _P, _P, _P, _P],

@@ -1,0 +1,88 @@
+// Host side of the general-geometry 2D operators (gen2d.cuh): the context
+// holds the caller's device geometry / connectivity arrays (not owned) and
+// the 1D tables; the C-ABI entry points are declared in include/dgmf.h.
+#include <string>
+
+#include "ctx.h"
+#include "gen2d.cuh"
+
+using namespace dg;
+
+struct dg_g2 {
+  G2Geo geo;
+  G2Tab tab;
+};
+
+namespace {
+
+int g2_launch(dg_g2 *g, const G2Params &prm, const double *src, double *dst, cudaStream_t st) {
+  constexpr int CPB = 2;
+  if (g->geo.ncells == 0) return DG_OK;
+  const unsigned grid = (unsigned)((g->geo.ncells + CPB - 1) / CPB);
+  g2_kernel<CPB><<<grid, 64 * CPB, 0, st>>>(src, dst, g->geo, g->tab, prm);
+  DG_LAUNCH_CHECK("g2_kernel");
+  return DG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dg_g2_create(const dg_g2_desc *d, dg_g2 **out) {
+  if (!d || !out) return inval("null argument");
+  *out = nullptr;
+  if (d->n < 2 || d->n > kG2MaxN) return inval("general 2D path: 1 <= k <= 7");
+  if (d->nq < 1 || d->nq > kG2MaxQ) return inval("general 2D path: n_q <= 11");
+  if (d->ncells < 0) return inval("negative cell count");
+  if (!d->jxw || !d->jit || !d->fsj || !d->fnrm || !d->fjit || !d->nbr || !d->nslot ||
+      !d->nflip || !d->tau || !d->S || !d->D || !d->ld || !d->rd)
+    return inval("null geometry / table array");
+  dg_g2 *g = new dg_g2();
+  g->geo = G2Geo{d->n, d->nq, d->ncells, d->jxw, d->jit, d->fsj, d->fnrm, d->fjit,
+                 d->nbr, d->nslot, d->nflip, d->tau};
+  for (int i = 0; i < d->nq * d->n; ++i) {
+    g->tab.S[i] = d->S[i];
+    g->tab.D[i] = d->D[i];
+  }
+  for (int i = 0; i < d->n * d->n; ++i) g->tab.Si[i] = d->Si ? d->Si[i] : 0.0;
+  for (int i = 0; i < d->n; ++i) {
+    g->tab.ld[i] = d->ld[i];
+    g->tab.rd[i] = d->rd[i];
+  }
+  *out = g;
+  return DG_OK;
+}
+
+int dg_g2_destroy(dg_g2 *g) {
+  delete g;
+  return DG_OK;
+}
+
+int dg_g2_apply(dg_g2 *g, int op, double tau_scale, const int *kind, const double *src,
+                double *dst, int ncomp, void *stream) {
+  if (!g || !src || !dst) return inval("null argument");
+  if (op < kG2Mass || op > kG2Laplace) return inval("general 2D: unknown operator");
+  if (op == kG2Laplace && !kind) return inval("general 2D Laplace needs the boundary kinds");
+  if (op == kG2InvMass && g->geo.nq != g->geo.n)
+    return inval("inverse mass requires the n_q = k + 1 Gauss rule");
+  if (op == kG2Laplace && ncomp != 1) return inval("the Laplacian acts on one scalar field");
+  if (src == dst) return inval("general 2D: src and dst must not alias");
+  G2Params prm{op, tau_scale, kind, -1};
+  const int64_t per = g->geo.ncells * g->geo.n * g->geo.n;
+  for (int c = 0; c < ncomp; ++c)
+    if (int rc = g2_launch(g, prm, src + c * per, dst + c * per, (cudaStream_t)stream)) return rc;
+  return DG_OK;
+}
+
+int dg_g2_laplace_diagonal(dg_g2 *g, double tau_scale, const int *kind, double *diag,
+                           void *stream) {
+  if (!g || !kind || !diag) return inval("null argument");
+  const int np = g->geo.n * g->geo.n;
+  for (int l = 0; l < np; ++l) {
+    G2Params prm{kG2LaplaceLocal, tau_scale, kind, l};
+    if (int rc = g2_launch(g, prm, nullptr, diag, (cudaStream_t)stream)) return rc;
+  }
+  return DG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,336 @@
+"""General-geometry 2D path: the reference's own 2D setting — quadrilateral
+meshes with iso-parametric (possibly curved, k_geo > 1) mappings, arbitrary
+conforming connectivity and face-orientation flips (reference mesh.py,
+geometry.py, spaces.py) — on the device (csrc/gen2d.cuh, dg_g2_*).
+
+``GeneralSpace2D(mesh, k)`` takes any object with the reference ``Mesh``
+fields (``geom_degree``, ``geom_nodes`` (2, mg, ne, mg), ``interior``
+(em, sm, ep, sp, flip), ``boundary`` (elem, slot, tag), ``tag_names``), so a
+reference user passes the meshes they already build (box, warped, cylinder).
+The geometry at the quadrature points is restated here from
+geometry.py:29-87 (host setup, numpy) and uploaded once; the operators
+mirror operators.py under the same names and take reference-layout numpy
+fields (m, ne, m) / (c, m, ne, m) or element-major CUDA tensors.
+"""
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .basis import get_basis
+from .spaces import _torch
+
+_REF_NORMALS = ((-1.0, 0.0), (1.0, 0.0), (0.0, -1.0), (0.0, 1.0))
+
+
+def _vol(F, S1, S2):
+    """out[a, e, b] = sum_j sum_i S1[a, j] S2[b, i] F[j, e, i] (kernel layout)."""
+    return np.einsum("aj,jei,bi->aeb", S1, F, S2, optimize=True)
+
+
+def _face_values(F, t):
+    S = t.S
+    return np.stack([(S @ F[:, :, 0]).T, (S @ F[:, :, -1]).T, F[0] @ S.T, F[-1] @ S.T])
+
+
+def _face_gradients(F, t):
+    S, D, ld, rd = t.S, t.D, t.left_deriv, t.right_deriv
+    m, ne, _ = F.shape
+    Fr = F.reshape(m * ne, m)
+    dxl = (Fr @ ld).reshape(m, ne)
+    dxr = (Fr @ rd).reshape(m, ne)
+    Fy = F.reshape(m, ne * m)
+    dyb = (ld @ Fy).reshape(ne, m)
+    dyt = (rd @ Fy).reshape(ne, m)
+    gx = np.stack([(S @ dxl).T, (S @ dxr).T, F[0] @ D.T, F[-1] @ D.T])
+    gy = np.stack([(D @ F[:, :, 0]).T, (D @ F[:, :, -1]).T, dyb @ S.T, dyt @ S.T])
+    return gx, gy
+
+
+class Geometry2D:
+    """Mapped geometry at the Gauss points (restates geometry.py:29-87):
+    xq, jxw, jinvT (volume) and xf, jinvT_f, normal, sjxw (faces), in the
+    reference kernel layouts."""
+
+    def __init__(self, mesh, n_q: int):
+        gb = get_basis(mesh.geom_degree, n_q)
+        w = gb.weights
+        X, Y = mesh.geom_nodes[0], mesh.geom_nodes[1]
+        xs, ys = _vol(X, gb.S, gb.S), _vol(Y, gb.S, gb.S)
+        dxdxi, dydxi = _vol(X, gb.S, gb.D), _vol(Y, gb.S, gb.D)
+        dxdeta, dydeta = _vol(X, gb.D, gb.S), _vol(Y, gb.D, gb.S)
+        det = dxdxi * dydeta - dxdeta * dydxi
+        if not (det > 0).all():
+            bad = int(np.argwhere((det <= 0).any(axis=(0, 2)))[0, 0])
+            raise ValueError(f"non-positive mapping Jacobian in element {bad}")
+        self.xq = np.stack([xs, ys])
+        self.jxw = det * np.multiply.outer(w, w)[:, None, :]
+        self.jinvT = np.stack([np.stack([dydeta / det, -dydxi / det]),
+                               np.stack([-dxdeta / det, dxdxi / det])])
+        self.volumes = self.jxw.sum(axis=(0, 2))
+        fx, fy = _face_values(X, gb), _face_values(Y, gb)
+        gxx, gxy = _face_gradients(X, gb)
+        gyx, gyy = _face_gradients(Y, gb)
+        fdet = gxx * gyy - gxy * gyx
+        if not (fdet > 0).all():
+            bad = int(np.argwhere((fdet <= 0).any(axis=(0, 2)))[0, 0])
+            raise ValueError(f"non-positive mapping Jacobian on a face of element {bad}")
+        self.xf = np.stack([fx, fy])
+        jit = np.stack([np.stack([gyy / fdet, -gyx / fdet]), np.stack([-gxy / fdet, gxx / fdet])])
+        self.jinvT_f = jit
+        ne = X.shape[1]
+        normal = np.empty((2, 4, ne, n_q))
+        sjxw = np.empty((4, ne, n_q))
+        for s, nref in enumerate(_REF_NORMALS):
+            v0 = jit[0, 0, s] * nref[0] + jit[0, 1, s] * nref[1]
+            v1 = jit[1, 0, s] * nref[0] + jit[1, 1, s] * nref[1]
+            norm = np.hypot(v0, v1)
+            normal[0, s] = v0 / norm
+            normal[1, s] = v1 / norm
+            sjxw[s] = fdet[s] * norm * w[None, :]
+        self.normal = normal
+        self.sjxw = sjxw
+        self.face_areas = sjxw.sum(axis=2)
+
+
+def compute_tau_ip(mesh, geom: Geometry2D, k: int):
+    """tau_e = (k+1)^2 (A_int/2 + A_bnd) / V_e (geometry.py:90-108)."""
+    ne = mesh.geom_nodes.shape[2]
+    a_int = np.zeros(ne)
+    a_bnd = np.zeros(ne)
+    f, b = mesh.interior, mesh.boundary
+    np.add.at(a_int, f.em, geom.face_areas[f.sm, f.em])
+    np.add.at(a_int, f.ep, geom.face_areas[f.sp, f.ep])
+    np.add.at(a_bnd, b.elem, geom.face_areas[b.slot, b.elem])
+    return (k + 1) ** 2 * (0.5 * a_int + a_bnd) / geom.volumes
+
+
+class GeneralSpace2D:
+    """Discontinuous Q_k space on a general quadrilateral mesh (reference
+    spaces.py:61-81) with its device context."""
+
+    dim = 2
+    is_general = True
+
+    def __init__(self, mesh, k: int):
+        if k < 1:
+            raise ValueError(f"polynomial degree must be >= 1, got k={k}")
+        if k > 7:
+            raise ValueError("general 2D path: k <= 7")
+        torch = _torch()
+        self.mesh, self.k = mesh, k
+        n = k + 1
+        self.n_q = n
+        self.basis = get_basis(k, n)
+        self.geom = Geometry2D(mesh, n)
+        self.tau_e = compute_tau_ip(mesh, self.geom, k)
+        ne = mesh.geom_nodes.shape[2]
+        self.n_elements = ne
+        f = mesh.interior
+        em, sm = np.asarray(f.em, np.int64), np.asarray(f.sm, np.int64)
+        ep, sp = np.asarray(f.ep, np.int64), np.asarray(f.sp, np.int64)
+        flip = np.asarray(f.flip, bool)
+        nbr = -np.ones((ne, 4), np.int64)
+        nslot = np.zeros((ne, 4), np.int32)
+        nflip = np.zeros((ne, 4), np.int32)
+        nbr[em, sm], nslot[em, sm], nflip[em, sm] = ep, sp, flip
+        nbr[ep, sp], nslot[ep, sp], nflip[ep, sp] = em, sm, flip
+        g = self.geom
+        # own-frame face data; plus sides of interior faces take the minus
+        # side's sJxW and (negated) normal, flip-mapped (spaces.py:140-163)
+        fsj = g.sjxw.copy()
+        fnrm = g.normal.copy()
+        sjm = g.sjxw[sm, em]
+        nm = g.normal[:, sm, em]
+        sjm = np.where(flip[:, None], sjm[:, ::-1], sjm)
+        nm = np.where(flip[None, :, None], nm[:, :, ::-1], nm)
+        fsj[sp, ep] = sjm
+        fnrm[:, sp, ep] = -nm
+        dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to("cuda")
+        q = n
+        self._d = {
+            "jxw": dev(g.jxw.transpose(1, 0, 2)),
+            "jit": dev(g.jinvT.reshape(4, q, ne, q).transpose(2, 0, 1, 3)),
+            "fsj": dev(fsj.transpose(1, 0, 2)),
+            "fnrm": dev(fnrm.transpose(2, 1, 0, 3)),
+            "fjit": dev(g.jinvT_f.reshape(4, 4, ne, q).transpose(2, 1, 0, 3)),
+            "tau": dev(self.tau_e),
+            "nbr": dev(nbr),
+            "nslot": dev(nslot),
+            "nflip": dev(nflip),
+        }
+        t = self.basis
+        self.S_inv = np.linalg.inv(t.S)
+        desc = _lib.G2Desc()
+        desc.n, desc.nq, desc.ncells = n, q, ne
+        P = lambda x: ctypes.c_void_p(x.data_ptr())
+        for name in ("jxw", "jit", "fsj", "fnrm", "fjit", "tau", "nbr", "nslot", "nflip"):
+            setattr(desc, name, P(self._d[name]))
+        self._tabs = [np.ascontiguousarray(a, dtype=np.float64)
+                      for a in (t.S, t.D, self.S_inv, t.left_deriv, t.right_deriv)]
+        H = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        desc.S, desc.D, desc.Si, desc.ld, desc.rd = [H(a) for a in self._tabs]
+        h = ctypes.c_void_p()
+        _lib.call("dg_g2_create", ctypes.byref(desc), ctypes.byref(h))
+        self._h = h
+        self._kinds = {}
+        b = mesh.boundary
+        self.b_groups = {}
+        for i, name in enumerate(mesh.tag_names):
+            sel = np.asarray(b.tag) == i
+            if sel.any():
+                self.b_groups[name] = (np.asarray(b.elem)[sel], np.asarray(b.slot)[sel])
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().dg_g2_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def n_local(self):
+        return (self.k + 1) ** 2
+
+    @property
+    def n_dofs(self):
+        return self.n_elements * self.n_local
+
+    def boundary_tags(self):
+        return list(self.b_groups)
+
+    def kinds(self, bcs):
+        """Device int32 [e][4] boundary kinds of a resolved BC set."""
+        key = bcs.key
+        if key not in self._kinds:
+            from .operators import DirichletBC, NeumannBC
+            kd = np.zeros((self.n_elements, 4), np.int32)
+            for tag, (eb, sb) in self.b_groups.items():
+                kind = bcs.spec.kinds[tag]
+                if isinstance(kind, DirichletBC):
+                    kd[eb, sb] = _lib.BC_VELOCITY_DIRICHLET
+                elif isinstance(kind, NeumannBC):
+                    kd[eb, sb] = _lib.BC_VELOCITY_NEUMANN
+                else:
+                    raise TypeError(f"unsupported boundary kind for tag {tag!r}")
+            self._kinds[key] = _torch().as_tensor(kd).to("cuda")
+        return self._kinds[key]
+
+    # layouts: reference kernel layout (m, ne, m) <-> element-major (ne, m, m)
+    def to_element_major(self, a, ncomp):
+        a = np.asarray(a, dtype=np.float64)
+        m, ne = self.k + 1, self.n_elements
+        if ncomp == 1:
+            return np.ascontiguousarray(a.reshape(m, ne, m).transpose(1, 0, 2))
+        return np.ascontiguousarray(a.reshape(ncomp, m, ne, m).transpose(0, 2, 1, 3))
+
+    def from_element_major(self, a, ncomp):
+        m, ne = self.k + 1, self.n_elements
+        if ncomp == 1:
+            return np.ascontiguousarray(a.reshape(ne, m, m).transpose(1, 0, 2))
+        return np.ascontiguousarray(a.reshape(ncomp, ne, m, m).transpose(0, 2, 1, 3))
+
+
+class GeneralBCs:
+    """Resolved boundary conditions of a general space (operators.py:113-131)."""
+
+    def __init__(self, space: GeneralSpace2D, spec):
+        present = set(space.boundary_tags())
+        missing = present - set(spec.kinds)
+        if missing:
+            raise ValueError(f"boundary tags without a condition: {missing}")
+        from .operators import DirichletBC, NeumannBC
+        self.space, self.spec = space, spec
+        self.dirichlet, self.neumann = [], []
+        for tag in space.boundary_tags():
+            kind = spec.kinds[tag]
+            if isinstance(kind, DirichletBC):
+                self.dirichlet.append((tag, kind))
+            elif isinstance(kind, NeumannBC):
+                self.neumann.append((tag, kind))
+            else:
+                raise TypeError(f"unsupported boundary kind for tag {tag!r}")
+        self.key = tuple((t, type(spec.kinds[t]).__name__) for t in space.boundary_tags())
+
+    @property
+    def has_outflow(self):
+        return len(self.neumann) > 0
+
+
+def _field(space, x, ncomp):
+    """(device tensor, is_numpy, shape) of a field argument."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        if x.device.type != "cuda" or x.dtype != torch.float64:
+            raise ValueError("device operands must be float64 CUDA tensors")
+        if x.numel() != ncomp * space.n_dofs:
+            raise ValueError(f"expected {ncomp * space.n_dofs} values, got {x.numel()}")
+        return x.contiguous().reshape(-1), False, x.shape
+    a = np.asarray(x, dtype=np.float64)
+    if a.size != ncomp * space.n_dofs:
+        raise ValueError(f"expected {ncomp * space.n_dofs} values, got {a.size}")
+    return torch.as_tensor(space.to_element_major(a, ncomp).ravel()).to("cuda"), True, a.shape
+
+
+def _result(space, out, is_np, shape, ncomp):
+    if is_np:
+        return space.from_element_major(out.cpu().numpy(), ncomp).reshape(shape)
+    return out.view(shape)
+
+
+def _ncomp_of(space, x):
+    n = int(np.prod(np.shape(x)))
+    if n % space.n_dofs:
+        raise ValueError("field size is not a multiple of the space size")
+    return n // space.n_dofs
+
+
+def _stream():
+    return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _apply(space, op, x, ncomp, tau_scale=1.0, kinds=None):
+    t, is_np, shape = _field(space, x, ncomp)
+    out = _torch().empty_like(t)
+    kp = ctypes.c_void_p(kinds.data_ptr() if kinds is not None else 0)
+    _lib.call("dg_g2_apply", space.handle, int(op), float(tau_scale), kp,
+              ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(out.data_ptr()), int(ncomp),
+              _stream())
+    return _result(space, out, is_np, shape, ncomp)
+
+
+def mass_apply(space: GeneralSpace2D, u):
+    """Consistent mass per component (operators.py:167-173)."""
+    return _apply(space, 0, u, _ncomp_of(space, u))
+
+
+def inverse_mass_apply(space: GeneralSpace2D, r):
+    """Exact inverse mass per component (operators.py:176-181)."""
+    return _apply(space, 1, r, _ncomp_of(space, r))
+
+
+def apply_pressure_laplace(space: GeneralSpace2D, p, bcs: GeneralBCs, tau_scale: float = 1.0):
+    """SIP pressure Laplacian (operators.py:187-238)."""
+    return _apply(space, 2, p, 1, tau_scale, space.kinds(bcs))
+
+
+def laplace_diagonal(space: GeneralSpace2D, bcs: GeneralBCs, tau_scale: float = 1.0,
+                     like: Optional[object] = None):
+    """Exact Jacobi diagonal (operators.py:675-730): a CUDA tensor
+    (element-major), or reference-layout numpy when ``like='numpy'``."""
+    torch = _torch()
+    out = torch.empty(space.n_dofs, dtype=torch.float64, device="cuda")
+    _lib.call("dg_g2_laplace_diagonal", space.handle, float(tau_scale),
+              ctypes.c_void_p(space.kinds(bcs).data_ptr()), ctypes.c_void_p(out.data_ptr()),
+              _stream())
+    if like == "numpy":
+        return space.from_element_major(out.cpu().numpy(), 1)
+    return out

@@ -61,6 +61,9 @@ class BoundarySpec:
             raise ValueError(f"boundary tags without a condition: {missing}")
 
     def resolve(self, space):
+        if getattr(space, "is_general", False):
+            from .general import GeneralBCs
+            return GeneralBCs(space, self)
         return ResolvedBCs(space, self)
 
 
@@ -167,6 +170,9 @@ def apply_pressure_laplace(space: DgSpace, p, bcs: ResolvedBCs, tau_scale: float
     the device; CPU tensors (element-major, pinned for full overlap) take the
     pipelined host-buffer path; numpy arrays are converted from the
     reference layouts."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.apply_pressure_laplace(space, p, bcs, tau_scale)
     torch = _torch()
     if isinstance(p, torch.Tensor) and p.device.type == "cpu":
         return _laplace_host(space, p, bcs, tau_scale)
@@ -182,6 +188,10 @@ def laplace_diagonal(space: DgSpace, bcs: ResolvedBCs, tau_scale: float = 1.0,
                      like=None):
     """Exact Jacobi diagonal (operators.py:717-730).  Returns a CUDA tensor
     (element-major) unless ``like`` is a numpy array, whose layout is used."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.laplace_diagonal(space, bcs, tau_scale,
+                                        "numpy" if isinstance(like, np.ndarray) else None)
     torch = _torch()
     out = torch.empty(space.n_dofs, dtype=torch.float64, device="cuda")
     ctx = space.ctx(bcs.kinds)
@@ -203,11 +213,17 @@ def _mass(space, u, name):
 
 def mass_apply(space: DgSpace, u):
     """Consistent mass per component (operators.py:167-173)."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.mass_apply(space, u)
     return _mass(space, u, "dg_mass")
 
 
 def inverse_mass_apply(space: DgSpace, r):
     """Exact inverse mass per component (operators.py:176-181)."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.inverse_mass_apply(space, r)
     return _mass(space, r, "dg_inverse_mass")
 
 

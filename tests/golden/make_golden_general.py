@@ -1,0 +1,117 @@
+"""Golden vectors of the reference's GENERAL 2D geometry path (curved
+iso-parametric cells, unstructured connectivity with face flips), produced
+by running the real reference (2D ``dgins``) in the build container:
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden_general.py
+
+Writes ``tests/golden/ref2d_general.npz`` (committed; the GPU box reads only
+the npz).  Per case: the mesh as the reference builds it (geom_nodes, face
+lists, tags), the reference Geometry arrays and tau_e (to pin the host-side
+geometry restatement), seeded inputs and the reference operator outputs, all
+in the reference kernel layout (m, ne, m) / (c, m, ne, m).
+
+Cases: a box mesh with k_geo = 2 warped by a smooth map of our own (the
+reference test-suite's "curved" setting, pkg/tests/test_operators.py:45-50)
+and the laminar cylinder mesh (pkg/src/dgins/cylinder.py, 136 cells, k_geo
+4, curved boundary, 8 flipped interior faces), plus a graded box through
+the same path.
+"""
+
+import os
+import sys
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import numpy as np  # noqa: E402
+
+from dgins import operators as ops  # noqa: E402
+from dgins.cylinder import build_cylinder_mesh  # noqa: E402
+from dgins.mesh import build_box_mesh  # noqa: E402
+from dgins.spaces import DgSpace  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ref2d_general.npz")
+
+
+def z2(x, t):
+    return np.zeros((2,) + x.shape[1:])
+
+
+def z1(x, t):
+    return np.zeros(x.shape[1:])
+
+
+def warp(xy):
+    """A smooth non-affine map of the unit square onto itself."""
+    x, y = xy[0], xy[1]
+    s = np.sin(np.pi * x) * np.sin(np.pi * y)
+    return x + 0.07 * s * (1.0 - y), y - 0.04 * s * (0.5 + x)
+
+
+def curved_box(n):
+    m = build_box_mesh(((0, 1), (0, 1)), (n, n), k_geo=2)
+    m.geom_nodes = np.stack(warp(np.stack([m.geom_nodes[0], m.geom_nodes[1]])))
+    m.vertices = np.stack(warp(m.vertices.T), axis=1)
+    return m
+
+
+CASES = {
+    # name: (mesh builder, degrees, kinds per tag)
+    "curved": (lambda: curved_box(3), (2, 3, 5),
+               {"xmin": "D", "xmax": "N", "ymin": "D", "ymax": "D"}),
+    "cylinder": (lambda: build_cylinder_mesh(level=0, k_geo=4), (3,),
+                 {"inflow": "D", "outflow": "N", "wall": "D", "cylinder": "D"}),
+    "graded": (lambda: build_box_mesh(((0, 2), (-1, 1)), (4, 3), grading=(0.0, 1.2),
+                                      periodic=(True, False)), (3,),
+               {"ymin": "D", "ymax": "N"}),
+}
+
+
+def main():
+    rng = np.random.default_rng(20261019)
+    out = {}
+    for name, (build, degrees, kinds) in CASES.items():
+        mesh = build()
+        f, b = mesh.interior, mesh.boundary
+        out[f"{name}_geom_degree"] = np.array(mesh.geom_degree)
+        out[f"{name}_geom_nodes"] = mesh.geom_nodes
+        for key in ("em", "sm", "ep", "sp", "flip"):
+            out[f"{name}_{key}"] = np.asarray(getattr(f, key))
+        out[f"{name}_belem"] = np.asarray(b.elem)
+        out[f"{name}_bslot"] = np.asarray(b.slot)
+        out[f"{name}_btag"] = np.asarray(b.tag)
+        out[f"{name}_tags"] = np.array(mesh.tag_names)
+        out[f"{name}_kinds"] = np.array([f"{t}:{kinds.get(t, '-')}" for t in mesh.tag_names])
+        spec = ops.BoundarySpec({t: (ops.DirichletBC(z2, z2) if v == "D" else ops.NeumannBC(z2, z1))
+                                 for t, v in kinds.items()})
+        for k in degrees:
+            space = DgSpace(mesh, k)
+            bcs = spec.resolve(space)
+            g = space.geom
+            key = f"{name}_k{k}"
+            out[key + "_jxw"] = g.jxw
+            out[key + "_jinvT"] = g.jinvT
+            out[key + "_normal"] = g.normal
+            out[key + "_sjxw"] = g.sjxw
+            out[key + "_jinvT_f"] = g.jinvT_f
+            out[key + "_tau_e"] = space.tau_e
+            m, ne = k + 1, mesh.n_elements
+            p = rng.standard_normal((m, ne, m))
+            u = rng.standard_normal((2, m, ne, m))
+            out[key + "_p"] = p
+            out[key + "_u"] = u
+            out[key + "_mass_p"] = ops.mass_apply(space, p)
+            out[key + "_mass_u"] = ops.mass_apply(space, u)
+            out[key + "_imass_p"] = ops.inverse_mass_apply(space, p)
+            out[key + "_imass_u"] = ops.inverse_mass_apply(space, u)
+            out[key + "_lap"] = ops.apply_pressure_laplace(space, p, bcs)
+            out[key + "_lap25"] = ops.apply_pressure_laplace(space, p, bcs, tau_scale=2.5)
+            out[key + "_diag"] = ops.laplace_diagonal(space, bcs)
+            print(name, k, "ne", ne, "flips", int(np.sum(f.flip)))
+    np.savez_compressed(OUT, **out)
+    print("wrote", OUT, os.path.getsize(OUT), "bytes")
+
+
+if __name__ == "__main__":
+    main()
