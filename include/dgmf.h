@@ -294,6 +294,31 @@ int dg_g2_destroy(dg_g2 *g);
  * and tau_scale; ncomp fields of ncells*n*n values each (mass ops) */
 int dg_g2_apply(dg_g2 *g, int op, double tau_scale, const int *kind,
                 const double *src, double *dst, int ncomp, void *stream);
+/* The remaining 2D operators on a general mesh: op 2 SIP Laplacian (tau_scale),
+ * 3 viscous Helmholtz (:418-491; gamma0_dt, nu), 4 projection (:372-412;
+ * tau_d [e] / tau_c [e][4] per (cell, slot), either NULL), 5 convective term
+ * (:533-604; on a context built for the over-integration rule: n_hist levels,
+ * beta, Dirichlet data gdata[j] [e][4][2][q] or NULL, body force at the
+ * points [2][e][q][q] or NULL; src unused), 6 divergence a(q, u) (:265-316;
+ * scale, form 0 standard / 1 weak / 2 strong), 7 pressure gradient b(v, p)
+ * (:322-366; form 0 / 1), 8 vorticity moments (:610-618, before the inverse
+ * mass).  Vector fields: 2 components of ncells*n*n values each. */
+typedef struct {
+  int op;
+  double tau_scale;
+  const int *kind;                 /* device [e][4] */
+  double gamma0_dt, nu;
+  const double *tau_d, *tau_c;     /* device */
+  double scale;
+  int form;
+  int n_hist;
+  const double *hist[4];           /* device */
+  double beta[4];
+  const double *gdata[4];          /* device */
+  const double *body;              /* device */
+} dg_g2_params;
+int dg_g2_operator(dg_g2 *g, const dg_g2_params *p, const double *src, double *dst,
+                   void *stream);
 /* exact Jacobi diagonal (operators.py:675-730) */
 int dg_g2_laplace_diagonal(dg_g2 *g, double tau_scale, const int *kind,
                            double *diag, void *stream);

@@ -100,6 +100,15 @@ class G2Desc(ctypes.Structure):
                 ("rd", ctypes.POINTER(ctypes.c_double))]
 
 
+class G2Params(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int), ("tau_scale", ctypes.c_double), ("kind", ctypes.c_void_p),
+                ("gamma0_dt", ctypes.c_double), ("nu", ctypes.c_double),
+                ("tau_d", ctypes.c_void_p), ("tau_c", ctypes.c_void_p),
+                ("scale", ctypes.c_double), ("form", ctypes.c_int), ("n_hist", ctypes.c_int),
+                ("hist", ctypes.c_void_p * 4), ("beta", ctypes.c_double * 4),
+                ("gdata", ctypes.c_void_p * 4), ("body", ctypes.c_void_p)]
+
+
 _P = ctypes.c_void_p
 _D = ctypes.c_double
 _I = ctypes.c_int
@@ -149,6 +158,7 @@ PROTOTYPES = {
     "dg_g2_destroy": [_P],
     "dg_g2_apply": [_P, _I, _D, _P, _P, _P, _I, _P],
     "dg_g2_laplace_diagonal": [_P, _D, _P, _P, _P],
+    "dg_g2_operator": [_P, ctypes.POINTER(G2Params), _P, _P, _P],
     "dg_mg_vcycle": [_P, _P, _P, _P],
     "dg_halo_count": [_P, ctypes.POINTER(_L)],
     "dg_halo_pack": [_P, _P, _P, _P, _P],

@@ -67,11 +67,53 @@ int dg_g2_apply(dg_g2 *g, int op, double tau_scale, const int *kind, const doubl
     return inval("inverse mass requires the n_q = k + 1 Gauss rule");
   if (op == kG2Laplace && ncomp != 1) return inval("the Laplacian acts on one scalar field");
   if (src == dst) return inval("general 2D: src and dst must not alias");
-  G2Params prm{op, tau_scale, kind, -1};
+  G2Params prm{};
+  prm.op = op;
+  prm.tau_scale = tau_scale;
+  prm.kind = kind;
+  prm.local_node = -1;
   const int64_t per = g->geo.ncells * g->geo.n * g->geo.n;
-  for (int c = 0; c < ncomp; ++c)
+  for (int c = 0; c < ncomp; ++c)  // one component at a time
     if (int rc = g2_launch(g, prm, src + c * per, dst + c * per, (cudaStream_t)stream)) return rc;
   return DG_OK;
+}
+
+int dg_g2_operator(dg_g2 *g, const dg_g2_params *p, const double *src, double *dst,
+                   void *stream) {
+  if (!g || !p || !dst) return inval("null argument");
+  const int op = p->op;
+  if (op < kG2Laplace || op > kG2Vorticity) return inval("general 2D: unknown operator");
+  if (!p->kind) return inval("general 2D: boundary kinds required");
+  G2Params prm{};
+  prm.op = op;
+  prm.tau_scale = p->tau_scale;
+  prm.kind = p->kind;
+  prm.local_node = -1;
+  prm.gamma0_dt = p->gamma0_dt;
+  prm.nu = p->nu;
+  prm.tau_d = p->tau_d;
+  prm.tau_c = p->tau_c;
+  prm.scale = p->scale;
+  prm.form = p->form;
+  if (op == kG2Convective) {
+    if (p->n_hist < 1 || p->n_hist > kG2MaxHist) return inval("need 1..4 history levels");
+    prm.n_hist = p->n_hist;
+    for (int j = 0; j < p->n_hist; ++j) {
+      if (!p->hist[j]) return inval("null history level");
+      if (p->hist[j] == dst) return inval("convective term: dst must not alias a history level");
+      prm.hist[j] = p->hist[j];
+      prm.beta[j] = p->beta[j];
+      prm.gdata[j] = p->gdata[j];
+    }
+    prm.body = p->body;
+  } else {
+    if (!src) return inval("null argument");
+    if (src == dst) return inval("general 2D: src and dst must not alias");
+  }
+  if ((op == kG2Divergence && (p->form < 0 || p->form > 2)) ||
+      (op == kG2Gradient && (p->form < 0 || p->form > 1)))
+    return inval("unknown form");
+  return g2_launch(g, prm, src, dst, (cudaStream_t)stream);
 }
 
 int dg_g2_laplace_diagonal(dg_g2 *g, double tau_scale, const int *kind, double *diag,
@@ -79,7 +121,11 @@ int dg_g2_laplace_diagonal(dg_g2 *g, double tau_scale, const int *kind, double *
   if (!g || !kind || !diag) return inval("null argument");
   const int np = g->geo.n * g->geo.n;
   for (int l = 0; l < np; ++l) {
-    G2Params prm{kG2LaplaceLocal, tau_scale, kind, l};
+    G2Params prm{};
+    prm.op = kG2LaplaceLocal;
+    prm.tau_scale = tau_scale;
+    prm.kind = kind;
+    prm.local_node = l;
     if (int rc = g2_launch(g, prm, nullptr, diag, (cudaStream_t)stream)) return rc;
   }
   return DG_OK;

@@ -19,18 +19,31 @@
 // factorisation): per-cell work is a few thousand FMAs and the path is
 // bound by the geometry data it streams (5 doubles per volume point, 7 per
 // face point), like the reference's own layout.
+//
+// Operators (one kernel, NCI input / NCO output components, runtime op):
+//   mass, exact inverse mass, SIP pressure Laplacian (+ its block-diagonal
+//   part for the Jacobi diagonal), viscous Helmholtz, projection, convective
+//   term (over-integration geometry, history levels, Dirichlet data, body
+//   force), divergence (standard / weak / strong), pressure gradient
+//   (standard / weak), vorticity (before its inverse mass).
 #pragma once
 #include "common.cuh"
 
 namespace dg {
 
-constexpr int kG2MaxN = 8, kG2MaxQ = 11;
+constexpr int kG2MaxN = 8, kG2MaxQ = 11, kG2MaxHist = 4;
 
 enum G2Op : int {
   kG2Mass = 0,
   kG2InvMass = 1,
   kG2Laplace = 2,
-  kG2LaplaceLocal = 3,  // neighbour traces zeroed (block-diagonal part)
+  kG2Helmholtz = 3,
+  kG2Projection = 4,
+  kG2Convective = 5,
+  kG2Divergence = 6,
+  kG2Gradient = 7,
+  kG2Vorticity = 8,
+  kG2LaplaceLocal = 9,  // neighbour traces zeroed (block-diagonal part)
 };
 
 struct G2Tab {  // 1D tables of the rule (S, D: n_q x n, row-major)
@@ -55,12 +68,23 @@ struct G2Geo {
 
 struct G2Params {
   int op;
-  double tau_scale;
+  double tau_scale;       // Laplace
   const int *kind;        // [e][4]: 0 interior, DG_BC_VELOCITY_DIRICHLET / _NEUMANN
   int local_node;         // kG2LaplaceLocal: unit vector at this node (-1: use src)
+  double gamma0_dt, nu;   // Helmholtz
+  const double *tau_d;    // projection: [e] or null
+  const double *tau_c;    // projection: [e][4] or null
+  double scale;           // divergence / gradient
+  int form;               // 0 standard, 1 weak, 2 strong
+  int n_hist;             // convective: levels, their beta and Dirichlet data
+  const double *hist[kG2MaxHist];
+  double beta[kG2MaxHist];
+  const double *gdata[kG2MaxHist];  // [e][4][2][q] or null (homogeneous)
+  const double *body;     // [2][e][q][q] body force at the points, or null
 };
 
 // value and reference gradient of a cell field at face point q of slot s
+// (kernels.py:119-156)
 __device__ __forceinline__ void g2_trace(const double *u, int N, const G2Tab &T, int s, int q,
                                          double &v, double &gx, double &gy) {
   v = gx = gy = 0.0;
@@ -89,150 +113,330 @@ __device__ __forceinline__ void g2_trace(const double *u, int N, const G2Tab &T,
   }
 }
 
+__device__ __forceinline__ int g2_nci(int op) {
+  return (op == kG2Helmholtz || op == kG2Projection || op == kG2Convective ||
+          op == kG2Divergence || op == kG2Vorticity) ? 2 : 1;
+}
+__device__ __forceinline__ int g2_nco(int op) {
+  return (op == kG2Helmholtz || op == kG2Projection || op == kG2Convective || op == kG2Gradient)
+             ? 2 : 1;
+}
+
+// Lax-Friedrichs F*(u) . n with the own outward normal (operators.py:597-604)
+__device__ __forceinline__ void g2_lf(double a0, double a1, double b0, double b1, double nx,
+                                      double ny, double &F0, double &F1) {
+  const double unm = a0 * nx + a1 * ny, unp = b0 * nx + b1 * ny;
+  const double lam = 2.0 * fmax(fabs(unm), fabs(unp));
+  F0 = 0.5 * (a0 * unm + b0 * unp) + 0.5 * lam * (a0 - b0);
+  F1 = 0.5 * (a1 * unm + b1 * unp) + 0.5 * lam * (a1 - b1);
+}
+
 template <int CPB>
 __global__ void __launch_bounds__(64 * CPB)
 g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo g,
-          const __grid_constant__ G2Tab T, const G2Params prm) {
-  constexpr int TPC = 64;
+          const __grid_constant__ G2Tab T, const __grid_constant__ G2Params prm) {
+  constexpr int TPC = 64, QS = kG2MaxQ * kG2MaxQ;
   const int N = g.n, NQ = g.nq, NP = N * N, QP = NQ * NQ;
-  __shared__ double su[CPB][kG2MaxN * kG2MaxN];
-  __shared__ double sq[CPB][3][kG2MaxQ * kG2MaxQ];
-  __shared__ double sf[CPB][4][3][kG2MaxQ];
+  const int op = prm.op;
+  const int nci = g2_nci(op), nco = g2_nco(op);
+  const int64_t nc = g.ncells;
+  __shared__ double su[CPB][2][kG2MaxN * kG2MaxN];
+  __shared__ double sq[CPB][2][3][QS];          // [comp][value | ref-x | ref-y test]
+  __shared__ double sf[CPB][4][2][3][kG2MaxQ];  // [slot][comp][value | ref-x | ref-y]
   const int cs = threadIdx.x / TPC, t = threadIdx.x % TPC;
   const int64_t e = (int64_t)blockIdx.x * CPB + cs;
-  const bool valid = e < g.ncells;
-  const int op = prm.op;
-  for (int i = t; i < NP; i += TPC) {
-    double v = 0.0;
-    if (valid) {
-      if (op == kG2LaplaceLocal && prm.local_node >= 0) v = (i == prm.local_node) ? 1.0 : 0.0;
-      else v = src[e * NP + i];
-    }
-    su[cs][i] = v;
-  }
-  __syncthreads();
-  const double *u = su[cs];
+  const bool valid = e < nc;
+  const int nlev = op == kG2Convective ? prm.n_hist : 1;
+  const bool faces = op == kG2Laplace || op == kG2LaplaceLocal ||
+                     (op == kG2Helmholtz && prm.nu != 0.0) ||
+                     (op == kG2Projection && prm.tau_c != nullptr) || op == kG2Convective ||
+                     ((op == kG2Divergence || op == kG2Gradient) && prm.form != 0);
 
-  if (op == kG2InvMass) {
-    // S^-1 diag(1/JxW) S^-T (kernels.py:95-107): Q = (Si^T x Si^T) R / JxW
-    for (int i = t; i < QP; i += TPC) {
-      const int qx = i % NQ, qy = i / NQ;
-      double a = 0.0;
-      for (int j = 0; j < N; ++j) {
-        double b = 0.0;
-        for (int l = 0; l < N; ++l) b = fma(u[j * N + l], T.Si[l * N + qx], b);
-        a = fma(T.Si[j * N + qy], b, a);
+  for (int i = t; i < 2 * 3 * QS; i += TPC) (&sq[cs][0][0][0])[i] = 0.0;
+  for (int i = t; i < 4 * 2 * 3 * kG2MaxQ; i += TPC) (&sf[cs][0][0][0][0])[i] = 0.0;
+
+  for (int lev = 0; lev < nlev; ++lev) {
+    const double *in = op == kG2Convective ? prm.hist[lev] : src;
+    const double beta = op == kG2Convective ? prm.beta[lev] : 1.0;
+    __syncthreads();
+    for (int i = t; i < nci * NP; i += TPC) {
+      const int c = i / NP, o = i % NP;
+      double v = 0.0;
+      if (valid) {
+        if (op == kG2LaplaceLocal && prm.local_node >= 0) v = (o == prm.local_node) ? 1.0 : 0.0;
+        else v = in[((int64_t)c * nc + e) * NP + o];
       }
-      sq[cs][0][i] = valid ? a / g.jxw[e * QP + i] : 0.0;
+      su[cs][c][o] = v;
     }
     __syncthreads();
-    for (int i = t; i < NP; i += TPC) {
-      const int x = i % N, y = i / N;
-      double a = 0.0;
-      for (int qy = 0; qy < NQ; ++qy) {
-        double b = 0.0;
-        for (int qx = 0; qx < NQ; ++qx) b = fma(sq[cs][0][qy * NQ + qx], T.Si[x * N + qx], b);
-        a = fma(T.Si[y * N + qy], b, a);
-      }
-      if (valid) dst[e * NP + i] = a;
-    }
-    return;
-  }
 
-  // ---- volume: data at the quadrature points --------------------------------
-  for (int i = t; i < QP; i += TPC) {
-    const int qx = i % NQ, qy = i / NQ;
-    double v = 0.0, gx = 0.0, gy = 0.0;
-    for (int j = 0; j < N; ++j) {
-      double sv = 0.0, dv = 0.0;
-      for (int l = 0; l < N; ++l) {
-        sv = fma(T.S[qx * N + l], u[j * N + l], sv);
-        dv = fma(T.D[qx * N + l], u[j * N + l], dv);
+    if (op == kG2InvMass) {
+      // S^-1 diag(1/JxW) S^-T (kernels.py:95-107): Q = (Si^T x Si^T) R / JxW
+      const double *u = su[cs][0];
+      for (int i = t; i < QP; i += TPC) {
+        const int qx = i % NQ, qy = i / NQ;
+        double a = 0.0;
+        for (int j = 0; j < N; ++j) {
+          double b = 0.0;
+          for (int l = 0; l < N; ++l) b = fma(u[j * N + l], T.Si[l * N + qx], b);
+          a = fma(T.Si[j * N + qy], b, a);
+        }
+        sq[cs][0][0][i] = valid ? a / g.jxw[e * QP + i] : 0.0;
       }
-      v = fma(T.S[qy * N + j], sv, v);
-      gx = fma(T.S[qy * N + j], dv, gx);
-      gy = fma(T.D[qy * N + j], sv, gy);
+      __syncthreads();
+      for (int i = t; i < NP; i += TPC) {
+        const int x = i % N, y = i / N;
+        double a = 0.0;
+        for (int qy = 0; qy < NQ; ++qy) {
+          double b = 0.0;
+          for (int qx = 0; qx < NQ; ++qx) b = fma(sq[cs][0][0][qy * NQ + qx], T.Si[x * N + qx], b);
+          a = fma(T.Si[y * N + qy], b, a);
+        }
+        if (valid) dst[e * NP + i] = a;
+      }
+      return;
     }
-    double r0 = 0.0, r1 = 0.0, vt = 0.0;
-    if (valid) {
-      const double jw = g.jxw[e * QP + i];
-      if (op == kG2Mass) {
-        vt = v * jw;
-      } else {  // Laplace: (grad q, grad p) (operators.py:199-201)
+
+    // ---- volume: test data at the quadrature points ---------------------------
+    for (int i = t; i < QP; i += TPC) {
+      const int qx = i % NQ, qy = i / NQ;
+      double v[2] = {0.0, 0.0}, px[2] = {0.0, 0.0}, py[2] = {0.0, 0.0};
+      double jw = 0.0, j00 = 0.0, j01 = 0.0, j10 = 0.0, j11 = 0.0;
+      if (valid) {
+        jw = g.jxw[e * QP + i];
         const double *J = g.jit + e * 4 * QP + i;
-        const double j00 = J[0], j01 = J[QP], j10 = J[2 * QP], j11 = J[3 * QP];
-        const double px = j00 * gx + j01 * gy, py = j10 * gx + j11 * gy;
-        const double dx = px * jw, dy = py * jw;
-        r0 = j00 * dx + j10 * dy;
-        r1 = j01 * dx + j11 * dy;
+        j00 = J[0];
+        j01 = J[QP];
+        j10 = J[2 * QP];
+        j11 = J[3 * QP];
+      }
+      for (int c = 0; c < nci; ++c) {
+        const double *u = su[cs][c];
+        double vv = 0.0, gx = 0.0, gy = 0.0;
+        for (int j = 0; j < N; ++j) {
+          double sv = 0.0, dv = 0.0;
+          for (int l = 0; l < N; ++l) {
+            sv = fma(T.S[qx * N + l], u[j * N + l], sv);
+            dv = fma(T.D[qx * N + l], u[j * N + l], dv);
+          }
+          vv = fma(T.S[qy * N + j], sv, vv);
+          gx = fma(T.S[qy * N + j], dv, gx);
+          gy = fma(T.D[qy * N + j], sv, gy);
+        }
+        v[c] = vv;
+        px[c] = j00 * gx + j01 * gy;  // _phys_grad_vol (operators.py:137-140)
+        py[c] = j10 * gx + j11 * gy;
+      }
+      // value test VT[a] and physical gradient test (dx[a], dy[a])
+      double VT[2] = {0.0, 0.0}, dx[2] = {0.0, 0.0}, dy[2] = {0.0, 0.0};
+      switch (op) {
+        case kG2Mass:
+          VT[0] = v[0] * jw;
+          break;
+        case kG2Laplace:
+        case kG2LaplaceLocal:
+          dx[0] = px[0] * jw;
+          dy[0] = py[0] * jw;
+          break;
+        case kG2Helmholtz: {  // operators.py:423-437
+          const double e01 = prm.nu * (py[0] + px[1]);
+          const double t00 = (2.0 * prm.nu * px[0]) * jw, t01 = e01 * jw;
+          const double t11 = (2.0 * prm.nu * py[1]) * jw;
+          dx[0] = t00;
+          dy[0] = t01;
+          dx[1] = t01;
+          dy[1] = t11;
+          VT[0] = prm.gamma0_dt * v[0] * jw;
+          VT[1] = prm.gamma0_dt * v[1] * jw;
+          break;
+        }
+        case kG2Projection:  // operators.py:381-395
+          VT[0] = v[0] * jw;
+          VT[1] = v[1] * jw;
+          if (prm.tau_d) {
+            const double s = valid ? (prm.tau_d[e] * (px[0] + py[1])) * jw : 0.0;
+            dx[0] = s;
+            dy[1] = s;
+          }
+          break;
+        case kG2Convective: {  // operators.py:545-552, 588-591
+          const double t00 = v[0] * v[0] * jw, t01 = v[0] * v[1] * jw, t11 = v[1] * v[1] * jw;
+          dx[0] = beta * t00;
+          dy[0] = beta * t01;
+          dx[1] = beta * t01;
+          dy[1] = beta * t11;
+          if (lev == 0 && prm.body && valid) {
+            VT[0] = prm.body[e * QP + i] * jw;
+            VT[1] = prm.body[(nc + e) * QP + i] * jw;
+          }
+          break;
+        }
+        case kG2Divergence:  // operators.py:270-316
+          if (prm.form == 1) {
+            dx[0] = prm.scale * v[0] * jw;
+            dy[0] = prm.scale * v[1] * jw;
+          } else {
+            VT[0] = -prm.scale * (px[0] + py[1]) * jw;
+          }
+          break;
+        case kG2Gradient:  // operators.py:326-345
+          if (prm.form == 1) {
+            const double s = prm.scale * v[0] * jw;
+            dx[0] = s;
+            dy[1] = s;
+          } else {
+            VT[0] = -prm.scale * px[0] * jw;
+            VT[1] = -prm.scale * py[0] * jw;
+          }
+          break;
+        default:  // vorticity (operators.py:610-618)
+          VT[0] = (px[1] - py[0]) * jw;
+          break;
+      }
+      for (int a = 0; a < nco; ++a) {  // _ref_test_vol (operators.py:143-147)
+        sq[cs][a][0][i] += VT[a];
+        sq[cs][a][1][i] += j00 * dx[a] + j10 * dy[a];
+        sq[cs][a][2][i] += j01 * dx[a] + j11 * dy[a];
       }
     }
-    sq[cs][0][i] = vt;
-    sq[cs][1][i] = r0;
-    sq[cs][2][i] = r1;
-  }
 
-  // ---- faces (Laplace): own-frame SIP fluxes (operators.py:203-236) ----------
-  const bool faces = op == kG2Laplace || op == kG2LaplaceLocal;
-  if (faces) {
-    for (int i = t; i < 4 * NQ; i += TPC) {
-      const int s = i / NQ, q = i % NQ;
-      double V = 0.0, R0 = 0.0, R1 = 0.0;
-      // velocity-Dirichlet sides carry no pressure term (operators.py:189-193)
-      const int kind = valid ? prm.kind[e * 4 + s] : DG_BC_VELOCITY_DIRICHLET;
-      if (valid && kind != DG_BC_VELOCITY_DIRICHLET) {
+    // ---- faces: own-frame fluxes ------------------------------------------------
+    if (faces) {
+      for (int i = t; i < 4 * NQ; i += TPC) {
+        const int s = i / NQ, q = i % NQ;
+        const int kind = valid ? prm.kind[e * 4 + s] : DG_BC_VELOCITY_DIRICHLET;
+        bool active = valid;
+        if (op == kG2Laplace || op == kG2LaplaceLocal) active &= kind != DG_BC_VELOCITY_DIRICHLET;
+        if (op == kG2Helmholtz) active &= kind != DG_BC_VELOCITY_NEUMANN;
+        if (op == kG2Projection || (op == kG2Divergence && prm.form == 2)) active &= kind == 0;
+        if (!active) continue;
         const int64_t fi = (e * 4 + s) * NQ + q;
         const double sj = g.fsj[fi];
-        const double nx = g.fnrm[(e * 4 + s) * 2 * NQ + q], ny = g.fnrm[(e * 4 + s) * 2 * NQ + NQ + q];
+        const double nx = g.fnrm[(e * 4 + s) * 2 * NQ + q];
+        const double ny = g.fnrm[(e * 4 + s) * 2 * NQ + NQ + q];
         const double *J = g.fjit + (e * 4 + s) * 4 * NQ + q;
         const double j00 = J[0], j01 = J[NQ], j10 = J[2 * NQ], j11 = J[3 * NQ];
-        double vo, gxo, gyo;
-        g2_trace(u, N, T, s, q, vo, gxo, gyo);
-        const double gno = nx * (j00 * gxo + j01 * gyo) + ny * (j10 * gxo + j11 * gyo);
-        double Gx, Gy;
-        if (kind == 0) {
-          const int64_t en = g.nbr[e * 4 + s];
-          const int sn = g.nslot[e * 4 + s];
-          const int qn = g.nflip[e * 4 + s] ? NQ - 1 - q : q;
-          double vn = 0.0, gxn = 0.0, gyn = 0.0, gnn = 0.0;
-          if (op == kG2Laplace) {
-            g2_trace(src + en * NP, N, T, sn, qn, vn, gxn, gyn);
-            const double *Jn = g.fjit + (en * 4 + sn) * 4 * NQ + qn;
-            // neighbour gradient in the own outward normal direction
-            gnn = nx * (Jn[0] * gxn + Jn[NQ] * gyn) + ny * (Jn[2 * NQ] * gxn + Jn[3 * NQ] * gyn);
-          }
-          const double tau = prm.tau_scale * fmax(g.tau[e], g.tau[en]);
-          const double jump = vo - vn;
-          V = -(0.5 * (gno + gnn) - tau * jump) * sj;
-          Gx = -0.5 * jump * nx * sj;
-          Gy = -0.5 * jump * ny * sj;
-        } else {  // velocity-Neumann = pressure-Dirichlet side (operators.py:227-233)
-          const double taub = prm.tau_scale * g.tau[e];
-          V = -(gno - 2.0 * taub * vo) * sj;
-          Gx = -vo * nx * sj;
-          Gy = -vo * ny * sj;
+        // own traces (value, physical gradient) of the input components
+        double vo[2] = {0.0, 0.0}, xo[2] = {0.0, 0.0}, yo[2] = {0.0, 0.0};
+        double vn[2] = {0.0, 0.0}, xn[2] = {0.0, 0.0}, yn[2] = {0.0, 0.0};
+        for (int c = 0; c < nci; ++c) {
+          double gx, gy;
+          g2_trace(su[cs][c], N, T, s, q, vo[c], gx, gy);
+          xo[c] = j00 * gx + j01 * gy;  // _phys_grad_face (operators.py:150-153)
+          yo[c] = j10 * gx + j11 * gy;
         }
-        R0 = j00 * Gx + j10 * Gy;
-        R1 = j01 * Gx + j11 * Gy;
+        int64_t en = -1;
+        if (kind == 0) {
+          en = g.nbr[e * 4 + s];
+          if (op != kG2LaplaceLocal) {
+            const int sn = g.nslot[e * 4 + s];
+            const int qn = g.nflip[e * 4 + s] ? NQ - 1 - q : q;
+            const double *Jn = g.fjit + (en * 4 + sn) * 4 * NQ + qn;
+            for (int c = 0; c < nci; ++c) {
+              double gx, gy;
+              g2_trace(in + ((int64_t)c * nc + en) * NP, N, T, sn, qn, vn[c], gx, gy);
+              xn[c] = Jn[0] * gx + Jn[NQ] * gy;
+              yn[c] = Jn[2 * NQ] * gx + Jn[3 * NQ] * gy;
+            }
+          }
+        }
+        // value test V[a] and physical gradient test (Gx[a], Gy[a])
+        double V[2] = {0.0, 0.0}, Gx[2] = {0.0, 0.0}, Gy[2] = {0.0, 0.0};
+        if (op == kG2Laplace || op == kG2LaplaceLocal) {  // operators.py:203-233
+          const double gno = nx * xo[0] + ny * yo[0];
+          if (kind == 0) {
+            const double gnn = nx * xn[0] + ny * yn[0];
+            const double tau = prm.tau_scale * fmax(g.tau[e], g.tau[en]);
+            const double jump = vo[0] - vn[0];
+            V[0] = -(0.5 * (gno + gnn) - tau * jump) * sj;
+            Gx[0] = -0.5 * jump * nx * sj;
+            Gy[0] = -0.5 * jump * ny * sj;
+          } else {
+            const double taub = prm.tau_scale * g.tau[e];
+            V[0] = -(gno - 2.0 * taub * vo[0]) * sj;
+            Gx[0] = -vo[0] * nx * sj;
+            Gy[0] = -vo[0] * ny * sj;
+          }
+        } else if (op == kG2Helmholtz) {  // operators.py:440-483
+          const double nu = prm.nu;
+          const double vo0 = nu * (2.0 * xo[0] * nx + (yo[0] + xo[1]) * ny);
+          const double vo1 = nu * ((yo[0] + xo[1]) * nx + 2.0 * yo[1] * ny);
+          if (kind == 0) {
+            const double vn0 = nu * (2.0 * xn[0] * nx + (yn[0] + xn[1]) * ny);
+            const double vn1 = nu * ((yn[0] + xn[1]) * nx + 2.0 * yn[1] * ny);
+            const double tau = fmax(g.tau[e], g.tau[en]) * nu;
+            const double j0 = vo[0] - vn[0], j1 = vo[1] - vn[1];
+            V[0] = -(0.5 * (vo0 + vn0) - tau * j0) * sj;
+            V[1] = -(0.5 * (vo1 + vn1) - tau * j1) * sj;
+            const double G01 = -0.5 * nu * (j0 * ny + j1 * nx) * sj;
+            Gx[0] = -nu * j0 * nx * sj;
+            Gy[0] = G01;
+            Gx[1] = G01;
+            Gy[1] = -nu * j1 * ny * sj;
+          } else {  // velocity-Dirichlet side
+            const double taub = g.tau[e] * nu;
+            V[0] = -(vo0 - 2.0 * taub * vo[0]) * sj;
+            V[1] = -(vo1 - 2.0 * taub * vo[1]) * sj;
+            const double D01 = -nu * (vo[0] * ny + vo[1] * nx) * sj;
+            Gx[0] = -2.0 * nu * vo[0] * nx * sj;
+            Gy[0] = D01;
+            Gx[1] = D01;
+            Gy[1] = -2.0 * nu * vo[1] * ny * sj;
+          }
+        } else if (op == kG2Projection) {  // operators.py:396-411
+          const double tc = prm.tau_c[e * 4 + s];
+          V[0] = tc * (vo[0] - vn[0]) * sj;
+          V[1] = tc * (vo[1] - vn[1]) * sj;
+        } else if (op == kG2Convective) {  // operators.py:554-586
+          double F0, F1;
+          if (kind == 0) {
+            g2_lf(vo[0], vo[1], vn[0], vn[1], nx, ny, F0, F1);
+          } else if (kind == DG_BC_VELOCITY_DIRICHLET) {
+            const double *gd = prm.gdata[lev];
+            const double g0 = gd ? gd[((e * 4 + s) * 2 + 0) * NQ + q] : 0.0;
+            const double g1 = gd ? gd[((e * 4 + s) * 2 + 1) * NQ + q] : 0.0;
+            g2_lf(vo[0], vo[1], 2 * g0 - vo[0], 2 * g1 - vo[1], nx, ny, F0, F1);
+          } else {
+            const double un = vo[0] * nx + vo[1] * ny;
+            F0 = vo[0] * un;
+            F1 = vo[1] * un;
+          }
+          V[0] = -beta * F0 * sj;
+          V[1] = -beta * F1 * sj;
+        } else if (op == kG2Divergence) {
+          const double uno = vo[0] * nx + vo[1] * ny;
+          const double unn = vn[0] * nx + vn[1] * ny;
+          if (prm.form == 1)  // weak: -scale {u}.n (boundary: own trace)
+            V[0] = -prm.scale * (kind == 0 ? 0.5 * (uno + unn) : uno) * sj;
+          else                // strong: +scale [u].n / 2, interior only
+            V[0] = prm.scale * 0.5 * (uno - unn) * sj;
+        } else {  // weak pressure gradient: -scale {p} n (boundary: own trace)
+          const double pav = kind == 0 ? 0.5 * (vo[0] + vn[0]) : vo[0];
+          V[0] = -prm.scale * pav * nx * sj;
+          V[1] = -prm.scale * pav * ny * sj;
+        }
+        for (int a = 0; a < nco; ++a) {  // _ref_test_face (operators.py:156-159)
+          sf[cs][s][a][0][q] += V[a];
+          sf[cs][s][a][1][q] += j00 * Gx[a] + j10 * Gy[a];
+          sf[cs][s][a][2][q] += j01 * Gx[a] + j11 * Gy[a];
+        }
       }
-      sf[cs][s][0][q] = V;
-      sf[cs][s][1][q] = R0;
-      sf[cs][s][2][q] = R1;
     }
   }
   __syncthreads();
 
   // ---- tests: volume integrate + face lifts (kernels.py:86-92, 159-186) -------
-  for (int i = t; i < NP; i += TPC) {
-    const int x = i % N, y = i / N;
+  for (int i = t; i < nco * NP; i += TPC) {
+    const int a = i / NP, o = i % NP;
+    const int x = o % N, y = o / N;
     double acc = 0.0;
     for (int qy = 0; qy < NQ; ++qy) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
       for (int qx = 0; qx < NQ; ++qx) {
         const int k = qy * NQ + qx;
-        a0 = fma(T.S[qx * N + x], sq[cs][0][k], a0);
-        a1 = fma(T.D[qx * N + x], sq[cs][1][k], a1);
-        a2 = fma(T.S[qx * N + x], sq[cs][2][k], a2);
+        a0 = fma(T.S[qx * N + x], sq[cs][a][0][k], a0);
+        a1 = fma(T.D[qx * N + x], sq[cs][a][1][k], a1);
+        a2 = fma(T.S[qx * N + x], sq[cs][a][2][k], a2);
       }
       acc = fma(T.S[qy * N + y], a0 + a1, acc);
       acc = fma(T.D[qy * N + y], a2, acc);
@@ -240,20 +444,20 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
     if (faces) {
       for (int q = 0; q < NQ; ++q) {
         // slot 0 / 1 (x = -1 / +1): values at x = 0 / N-1, d/dxi via ld / rd
-        const double sy = T.S[q * N + y], dy = T.D[q * N + y];
-        double a = T.ld[x] * sy * sf[cs][0][1][q] + T.rd[x] * sy * sf[cs][1][1][q];
-        if (x == 0) a += sy * sf[cs][0][0][q] + dy * sf[cs][0][2][q];
-        if (x == N - 1) a += sy * sf[cs][1][0][q] + dy * sf[cs][1][2][q];
+        const double sy = T.S[q * N + y], dyv = T.D[q * N + y];
+        double v = T.ld[x] * sy * sf[cs][0][a][1][q] + T.rd[x] * sy * sf[cs][1][a][1][q];
+        if (x == 0) v += sy * sf[cs][0][a][0][q] + dyv * sf[cs][0][a][2][q];
+        if (x == N - 1) v += sy * sf[cs][1][a][0][q] + dyv * sf[cs][1][a][2][q];
         // slot 2 / 3 (y = -1 / +1)
-        const double sx = T.S[q * N + x], dx = T.D[q * N + x];
-        a += T.ld[y] * sx * sf[cs][2][2][q] + T.rd[y] * sx * sf[cs][3][2][q];
-        if (y == 0) a += sx * sf[cs][2][0][q] + dx * sf[cs][2][1][q];
-        if (y == N - 1) a += sx * sf[cs][3][0][q] + dx * sf[cs][3][1][q];
-        acc += a;
+        const double sx = T.S[q * N + x], dxv = T.D[q * N + x];
+        v += T.ld[y] * sx * sf[cs][2][a][2][q] + T.rd[y] * sx * sf[cs][3][a][2][q];
+        if (y == 0) v += sx * sf[cs][2][a][0][q] + dxv * sf[cs][2][a][1][q];
+        if (y == N - 1) v += sx * sf[cs][3][a][0][q] + dxv * sf[cs][3][a][1][q];
+        acc += v;
       }
     }
-    if (valid && (op != kG2LaplaceLocal || prm.local_node < 0 || i == prm.local_node))
-      dst[e * NP + i] = acc;
+    if (valid && (op != kG2LaplaceLocal || prm.local_node < 0 || o == prm.local_node))
+      dst[((int64_t)a * nc + e) * NP + o] = acc;
   }
 }
 

@@ -137,7 +137,24 @@ class GeneralSpace2D:
         nflip = np.zeros((ne, 4), np.int32)
         nbr[em, sm], nslot[em, sm], nflip[em, sm] = ep, sp, flip
         nbr[ep, sp], nslot[ep, sp], nflip[ep, sp] = em, sm, flip
-        g = self.geom
+        self._nbr = (nbr, nslot, nflip, sm, em, sp, ep, flip)
+        self._h, self._d, self._tabs = self._make_ctx(self.geom, self.basis, n)
+        self._over = None
+        self._kinds = {}
+        b = mesh.boundary
+        self.b_groups = {}
+        for i, name in enumerate(mesh.tag_names):
+            sel = np.asarray(b.tag) == i
+            if sel.any():
+                self.b_groups[name] = (np.asarray(b.elem)[sel], np.asarray(b.slot)[sel])
+
+    def _make_ctx(self, g, t, q):
+        """Device geometry arrays (element-major) and a dg_g2 context for one
+        rule (the linear rule n_q = k+1, or the convective over-integration
+        rule)."""
+        torch = _torch()
+        nbr, nslot, nflip, sm, em, sp, ep, flip = self._nbr
+        ne = self.n_elements
         # own-frame face data; plus sides of interior faces take the minus
         # side's sJxW and (negated) normal, flip-mapped (spaces.py:140-163)
         fsj = g.sjxw.copy()
@@ -149,8 +166,7 @@ class GeneralSpace2D:
         fsj[sp, ep] = sjm
         fnrm[:, sp, ep] = -nm
         dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to("cuda")
-        q = n
-        self._d = {
+        d = {
             "jxw": dev(g.jxw.transpose(1, 0, 2)),
             "jit": dev(g.jinvT.reshape(4, q, ne, q).transpose(2, 0, 1, 3)),
             "fsj": dev(fsj.transpose(1, 0, 2)),
@@ -161,36 +177,41 @@ class GeneralSpace2D:
             "nslot": dev(nslot),
             "nflip": dev(nflip),
         }
-        t = self.basis
-        self.S_inv = np.linalg.inv(t.S)
         desc = _lib.G2Desc()
-        desc.n, desc.nq, desc.ncells = n, q, ne
+        desc.n, desc.nq, desc.ncells = self.k + 1, q, ne
         P = lambda x: ctypes.c_void_p(x.data_ptr())
         for name in ("jxw", "jit", "fsj", "fnrm", "fjit", "tau", "nbr", "nslot", "nflip"):
-            setattr(desc, name, P(self._d[name]))
-        self._tabs = [np.ascontiguousarray(a, dtype=np.float64)
-                      for a in (t.S, t.D, self.S_inv, t.left_deriv, t.right_deriv)]
+            setattr(desc, name, P(d[name]))
+        Si = np.linalg.inv(t.S) if q == self.k + 1 else np.zeros((self.k + 1, self.k + 1))
+        tabs = [np.ascontiguousarray(a, dtype=np.float64)
+                for a in (t.S, t.D, Si, t.left_deriv, t.right_deriv)]
         H = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-        desc.S, desc.D, desc.Si, desc.ld, desc.rd = [H(a) for a in self._tabs]
+        desc.S, desc.D, desc.Si, desc.ld, desc.rd = [H(a) for a in tabs]
         h = ctypes.c_void_p()
         _lib.call("dg_g2_create", ctypes.byref(desc), ctypes.byref(h))
-        self._h = h
-        self._kinds = {}
-        b = mesh.boundary
-        self.b_groups = {}
-        for i, name in enumerate(mesh.tag_names):
-            sel = np.asarray(b.tag) == i
-            if sel.any():
-                self.b_groups[name] = (np.asarray(b.elem)[sel], np.asarray(b.slot)[sel])
+        return h, d, tabs
+
+    def over(self):
+        """(handle, geometry) of the convective over-integration rule
+        n_q = floor(3k/2) + 1 (basis.py:103-105, spaces.py:117-122)."""
+        if self._over is None:
+            nq = (3 * self.k) // 2 + 1
+            if nq > 11:
+                raise ValueError("general 2D convective term: n_q <= 11 (k <= 6)")
+            g = Geometry2D(self.mesh, nq)
+            h, d, tabs = self._make_ctx(g, get_basis(self.k, nq), nq)
+            self._over = (h, g, d, tabs)
+        return self._over
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            try:
-                _lib.lib().dg_g2_destroy(h)
-            except Exception:
-                pass
-            self._h = None
+        for h in (getattr(self, "_h", None),
+                  (getattr(self, "_over", None) or (None,))[0]):
+            if h is not None and h.value:
+                try:
+                    _lib.lib().dg_g2_destroy(h)
+                except Exception:
+                    pass
+        self._h = None
 
     @property
     def handle(self):
@@ -334,3 +355,171 @@ def laplace_diagonal(space: GeneralSpace2D, bcs: GeneralBCs, tau_scale: float = 
     if like == "numpy":
         return space.from_element_major(out.cpu().numpy(), 1)
     return out
+
+
+# ---------------------------------------------------------------------------
+# vector operators and right-hand sides (operators.py:262-618)
+
+def _op(space, prm, src, dst, handle=None):
+    _lib.call("dg_g2_operator", handle if handle is not None else space.handle,
+              ctypes.byref(prm), ctypes.c_void_p(src.data_ptr() if src is not None else 0),
+              ctypes.c_void_p(dst.data_ptr()), _stream())
+
+
+def _params(space, op, bcs):
+    prm = _lib.G2Params()
+    prm.op = op
+    prm.kind = ctypes.c_void_p(space.kinds(bcs).data_ptr())
+    return prm
+
+
+def _all_interior_kinds(space):
+    key = ("__interior__",)
+    if key not in space._kinds:
+        space._kinds[key] = _torch().zeros((space.n_elements, 4), dtype=_torch().int32,
+                                           device="cuda")
+    return space._kinds[key]
+
+
+def apply_viscous_helmholtz(space: GeneralSpace2D, u, gamma0_dt: float, nu: float,
+                            bcs: GeneralBCs):
+    """(gamma0/dt) M u + SIP of -div(2 nu eps(u)) (operators.py:418-491)."""
+    t, is_np, shape = _field(space, u, 2)
+    out = _torch().empty_like(t)
+    prm = _params(space, 3, bcs)
+    prm.gamma0_dt, prm.nu = float(gamma0_dt), float(nu)
+    _op(space, prm, t, out)
+    return _result(space, out, is_np, shape, 2)
+
+
+def face_penalty_slots(space: GeneralSpace2D, tau_c_f):
+    """Reference per-interior-face tau_C (mesh.interior order) -> [e][4]."""
+    f = space.mesh.interior
+    tau_c_f = np.asarray(tau_c_f, dtype=np.float64)
+    if tau_c_f.shape != np.shape(f.em):
+        raise ValueError(f"tau_c_f needs one entry per interior face ({np.size(f.em)})")
+    out = np.zeros((space.n_elements, 4))
+    out[np.asarray(f.em), np.asarray(f.sm)] = tau_c_f
+    out[np.asarray(f.ep), np.asarray(f.sp)] = tau_c_f
+    return out
+
+
+def apply_projection_operator(space: GeneralSpace2D, w, tau_d_e, tau_c_f):
+    """M + tau_D div-div + tau_C interior jump penalty (operators.py:372-412).
+    tau_c_f: per interior face (reference order) or a [e][4] CUDA tensor."""
+    torch = _torch()
+    t, is_np, shape = _field(space, w, 2)
+    out = torch.empty_like(t)
+    prm = _lib.G2Params()
+    prm.op = 4
+    prm.kind = ctypes.c_void_p(_all_interior_kinds(space).data_ptr())
+    keep = []
+    if tau_d_e is not None:
+        td = tau_d_e if isinstance(tau_d_e, torch.Tensor) else torch.as_tensor(
+            np.asarray(tau_d_e, dtype=np.float64)).to("cuda")
+        td = td.contiguous()
+        keep.append(td)
+        prm.tau_d = ctypes.c_void_p(td.data_ptr())
+    if tau_c_f is not None:
+        tc = tau_c_f if isinstance(tau_c_f, torch.Tensor) else torch.as_tensor(
+            face_penalty_slots(space, tau_c_f)).to("cuda")
+        tc = tc.contiguous()
+        keep.append(tc)
+        prm.tau_c = ctypes.c_void_p(tc.data_ptr())
+    _op(space, prm, t, out)
+    return _result(space, out, is_np, shape, 2)
+
+
+def eval_divergence_rhs(space: GeneralSpace2D, u, bcs: GeneralBCs, scale: float,
+                        form: str = "standard"):
+    """a(q, u) scaled (operators.py:265-316)."""
+    forms = {"standard": 0, "weak": 1, "strong": 2}
+    if form not in forms:
+        raise ValueError(f"unknown divergence form {form!r}")
+    t, is_np, shape = _field(space, u, 2)
+    out = _torch().empty(space.n_dofs, dtype=_torch().float64, device="cuda")
+    prm = _params(space, 6, bcs)
+    prm.scale, prm.form = float(scale), forms[form]
+    _op(space, prm, t, out)
+    if is_np:
+        return space.from_element_major(out.cpu().numpy(), 1)
+    return out
+
+
+def eval_pressure_gradient_rhs(space: GeneralSpace2D, p, bcs: GeneralBCs, scale: float,
+                               form: str = "standard"):
+    """b(v, p) scaled (operators.py:322-366)."""
+    forms = {"standard": 0, "weak": 1}
+    if form not in forms:
+        raise ValueError(f"unknown pressure-gradient form {form!r}")
+    t, is_np, shape = _field(space, p, 1)
+    out = _torch().empty(2 * space.n_dofs, dtype=_torch().float64, device="cuda")
+    prm = _params(space, 7, bcs)
+    prm.scale, prm.form = float(scale), forms[form]
+    _op(space, prm, t, out)
+    if is_np:
+        return space.from_element_major(out.cpu().numpy(), 2)
+    return out
+
+
+def compute_vorticity(space: GeneralSpace2D, u):
+    """Element-local L2 projection of du2/dx - du1/dy (operators.py:610-618)."""
+    torch = _torch()
+    t, is_np, shape = _field(space, u, 2)
+    r = torch.empty(space.n_dofs, dtype=torch.float64, device="cuda")
+    prm = _lib.G2Params()
+    prm.op = 8
+    prm.kind = ctypes.c_void_p(_all_interior_kinds(space).data_ptr())
+    _op(space, prm, t, r)
+    out = inverse_mass_apply(space, r)
+    if is_np:
+        return space.from_element_major(out.cpu().numpy(), 1)
+    return out
+
+
+def eval_convective_rhs(space: GeneralSpace2D, bcs: GeneralBCs, history, betas, times,
+                        t_np1: float, body_force=None):
+    """sum_i beta_i [(grad v, u u) - (v, F*.n)] + (v, f) with the local
+    Lax-Friedrichs flux on the over-integration rule (operators.py:533-594);
+    Dirichlet data g(x, t_i) enters the mirror state 2g - u (a None callable
+    means homogeneous data)."""
+    torch = _torch()
+    if len(history) < 1 or len(history) > 4:
+        raise ValueError("need 1..4 history levels")
+    if len(times) < len(history) or len(betas) < len(history):
+        raise ValueError("need one beta and one time per history level")
+    h, g, _, _ = space.over()
+    nq = g.jxw.shape[0]
+    ne = space.n_elements
+    fields = [_field(space, u, 2) for u in history]
+    is_np, shape = fields[0][1], fields[0][2]
+    out = torch.empty(2 * space.n_dofs, dtype=torch.float64, device="cuda")
+    prm = _params(space, 5, bcs)
+    prm.n_hist = len(history)
+    keep = []
+    for j, (t, _, _) in enumerate(fields):
+        prm.hist[j] = ctypes.c_void_p(t.data_ptr())
+        prm.beta[j] = float(betas[j])
+        gd = None
+        for tag, bc in bcs.dirichlet:
+            if bc.g is None:
+                continue
+            eb, sb = space.b_groups[tag]
+            x = g.xf[:, sb, eb]                          # (2, nb, q)
+            gu = np.asarray(bc.g(x, times[j]), dtype=np.float64)
+            if gd is None:
+                gd = np.zeros((ne, 4, 2, nq))
+            gd[eb, sb] = np.moveaxis(gu, 0, 1)
+        if gd is not None:
+            tg = torch.as_tensor(gd).to("cuda")
+            keep.append(tg)
+            prm.gdata[j] = ctypes.c_void_p(tg.data_ptr())
+    if body_force is not None:
+        f = np.asarray(body_force(g.xq, t_np1), dtype=np.float64)  # (2, q, ne, q)
+        tb = torch.as_tensor(np.ascontiguousarray(f.transpose(0, 2, 1, 3))).to("cuda")
+        keep.append(tb)
+        prm.body = ctypes.c_void_p(tb.data_ptr())
+    _op(space, prm, None, out, handle=h)
+    if is_np:
+        return space.from_element_major(out.cpu().numpy(), 2).reshape(shape)
+    return out.view(shape)

@@ -230,6 +230,9 @@ def inverse_mass_apply(space: DgSpace, r):
 def apply_viscous_helmholtz(space: DgSpace, u, gamma0_dt: float, nu: float,
                             bcs: ResolvedBCs):
     """(gamma0/dt) M u + SIP of -div(2 nu eps(u)) (operators.py:418-491)."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.apply_viscous_helmholtz(space, u, gamma0_dt, nu, bcs)
     a = _Arg(space, u, space.dim)
     out = a.new_out()
     ctx = space.ctx(bcs.kinds)
@@ -257,6 +260,9 @@ def apply_projection_operator(space: DgSpace, w, tau_d_e, tau_c_f):
     tau_d_e: per cell (or None).  tau_c_f: per interior face in the order of
     ``space.interior_faces()`` as the reference passes it, or already in the
     device layout [d*ne + e] (a CUDA tensor of dim*ne entries), or None."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.apply_projection_operator(space, w, tau_d_e, tau_c_f)
     torch = _torch()
     a = _Arg(space, w, space.dim)
     out = a.new_out()
@@ -290,6 +296,9 @@ def eval_convective_rhs(space: DgSpace, bcs: ResolvedBCs, history, betas, times,
     callable means homogeneous data, as for every boundary callable here); the data and
     the body force are sampled on the host (they are the caller's Python
     callables) and integrated on the device."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.eval_convective_rhs(space, bcs, history, betas, times, t_np1, body_force)
     import ctypes
     if len(times) < len(history) or len(betas) < len(history):
         raise ValueError("need one beta and one time per history level")
@@ -463,6 +472,9 @@ def eval_divergence_rhs(space: DgSpace, u, bcs: ResolvedBCs, scale: float,
                         form: str = "standard"):
     """a(q, u) scaled: 'standard' volume form, 'weak' with central flux or
     its 'strong' rewrite (operators.py:265-316)."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.eval_divergence_rhs(space, u, bcs, scale, form)
     if form not in _FORMS:
         raise ValueError(f"unknown divergence form {form!r}")
     torch = _torch()
@@ -495,6 +507,9 @@ def eval_pressure_gradient_rhs(space: DgSpace, p, bcs: ResolvedBCs, scale: float
                                form: str = "standard"):
     """b(v, p) scaled: standard -(v, scale grad p) or weak with central flux
     (operators.py:322-366)."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.eval_pressure_gradient_rhs(space, p, bcs, scale, form)
     if form not in ("standard", "weak"):
         raise ValueError(f"unknown pressure-gradient form {form!r}")
     torch = _torch()
@@ -509,6 +524,9 @@ def eval_pressure_gradient_rhs(space: DgSpace, p, bcs: ResolvedBCs, scale: float
 def compute_vorticity(space: DgSpace, u):
     """Element-local L2 projection of curl u (operators.py:610-618): a scalar
     field in 2D (the reference), the three curl components in 3D."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.compute_vorticity(space, u)
     torch = _torch()
     a = _Arg(space, u, space.dim)
     nw = 1 if space.dim == 2 else 3

@@ -42,6 +42,15 @@ def z1(x, t):
     return np.zeros(x.shape[1:])
 
 
+def g_data(x, t):
+    """Smooth velocity-Dirichlet data (vector)."""
+    return np.stack([np.sin(2.0 * x[0] + t) * np.cos(x[1]), 0.3 * np.cos(x[0] - 2.0 * t) + x[1]])
+
+
+def force(x, t):
+    return np.stack([0.2 + np.cos(x[1]) * np.sin(t), x[0] * x[1] - 0.1])
+
+
 def warp(xy):
     """A smooth non-affine map of the unit square onto itself."""
     x, y = xy[0], xy[1]
@@ -85,6 +94,8 @@ def main():
         out[f"{name}_kinds"] = np.array([f"{t}:{kinds.get(t, '-')}" for t in mesh.tag_names])
         spec = ops.BoundarySpec({t: (ops.DirichletBC(z2, z2) if v == "D" else ops.NeumannBC(z2, z1))
                                  for t, v in kinds.items()})
+        spec_g = ops.BoundarySpec({t: (ops.DirichletBC(g_data, z2) if v == "D"
+                                       else ops.NeumannBC(z2, z1)) for t, v in kinds.items()})
         for k in degrees:
             space = DgSpace(mesh, k)
             bcs = spec.resolve(space)
@@ -108,6 +119,26 @@ def main():
             out[key + "_lap"] = ops.apply_pressure_laplace(space, p, bcs)
             out[key + "_lap25"] = ops.apply_pressure_laplace(space, p, bcs, tau_scale=2.5)
             out[key + "_diag"] = ops.laplace_diagonal(space, bcs)
+            u2 = rng.standard_normal((2, m, ne, m))
+            out[key + "_u2"] = u2
+            out[key + "_helm"] = ops.apply_viscous_helmholtz(space, u, 3.0, 0.7, bcs)
+            out[key + "_helm0"] = ops.apply_viscous_helmholtz(space, u, 3.0, 0.0, bcs)
+            td = rng.uniform(0.1, 0.5, ne)
+            tc = rng.uniform(0.1, 0.5, mesh.interior.n)
+            out[key + "_tau_d"] = td
+            out[key + "_tau_c"] = tc
+            out[key + "_proj"] = ops.apply_projection_operator(space, u, td, tc)
+            out[key + "_projD"] = ops.apply_projection_operator(space, u, td, None)
+            out[key + "_projC"] = ops.apply_projection_operator(space, u, None, tc)
+            for form in ("standard", "weak", "strong"):
+                out[key + f"_div_{form}"] = ops.eval_divergence_rhs(space, u, bcs, 1.7, form)
+            for form in ("standard", "weak"):
+                out[key + f"_grad_{form}"] = ops.eval_pressure_gradient_rhs(space, p, bcs, 0.9, form)
+            out[key + "_vort"] = ops.compute_vorticity(space, u)
+            bcs_g = spec_g.resolve(space)
+            out[key + "_conv1"] = ops.eval_convective_rhs(space, bcs, [u], (1.0,), (0.0,), 0.0)
+            out[key + "_conv2"] = ops.eval_convective_rhs(space, bcs_g, [u, u2], (2.0, -1.0),
+                                                          (0.3, 0.2), 0.4, body_force=force)
             print(name, k, "ne", ne, "flips", int(np.sum(f.flip)))
     np.savez_compressed(OUT, **out)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")

@@ -65,3 +65,39 @@ def test_general_device_tensors_and_solver():
     r = b - ops.apply_pressure_laplace(space, xs, bcs)
     assert float(r.norm()) < 1e-8 * float(b.norm())
     assert relerr(ops.inverse_mass_apply(space, ops.mass_apply(space, y)).cpu(), y.cpu()) < 1e-12
+
+
+def g_data(x, t):
+    return np.stack([np.sin(2.0 * x[0] + t) * np.cos(x[1]), 0.3 * np.cos(x[0] - 2.0 * t) + x[1]])
+
+
+def force(x, t):
+    return np.stack([0.2 + np.cos(x[1]) * np.sin(t), x[0] * x[1] - 0.1])
+
+
+@pytest.mark.parametrize("name,k", [(n, k) for n, ks in CASES.items() for k in ks])
+def test_general_vector_operators_match_reference(name, k):
+    Z, space, bcs = setup(name, k)
+    key = f"{name}_k{k}"
+    p, u, u2 = Z[key + "_p"], Z[key + "_u"], Z[key + "_u2"]
+    assert relerr(ops.apply_viscous_helmholtz(space, u, 3.0, 0.7, bcs), Z[key + "_helm"]) < TOL
+    assert relerr(ops.apply_viscous_helmholtz(space, u, 3.0, 0.0, bcs), Z[key + "_helm0"]) < TOL
+    td, tc = Z[key + "_tau_d"], Z[key + "_tau_c"]
+    assert relerr(ops.apply_projection_operator(space, u, td, tc), Z[key + "_proj"]) < TOL
+    assert relerr(ops.apply_projection_operator(space, u, td, None), Z[key + "_projD"]) < TOL
+    assert relerr(ops.apply_projection_operator(space, u, None, tc), Z[key + "_projC"]) < TOL
+    for form in ("standard", "weak", "strong"):
+        assert relerr(ops.eval_divergence_rhs(space, u, bcs, 1.7, form),
+                      Z[key + f"_div_{form}"]) < TOL, form
+    for form in ("standard", "weak"):
+        assert relerr(ops.eval_pressure_gradient_rhs(space, p, bcs, 0.9, form),
+                      Z[key + f"_grad_{form}"]) < TOL, form
+    assert relerr(ops.compute_vorticity(space, u), Z[key + "_vort"]) < TOL
+    assert relerr(ops.eval_convective_rhs(space, bcs, [u], (1.0,), (0.0,), 0.0),
+                  Z[key + "_conv1"]) < TOL
+    spec_g = ops.BoundarySpec({t: (ops.DirichletBC(g_data) if v == "D" else ops.NeumannBC(None, None))
+                               for t, v in kinds(Z, name).items()})
+    bcs_g = spec_g.resolve(space)
+    got = ops.eval_convective_rhs(space, bcs_g, [u, u2], (2.0, -1.0), (0.3, 0.2), 0.4,
+                                  body_force=force)
+    assert relerr(got, Z[key + "_conv2"]) < TOL
