@@ -302,7 +302,14 @@ int dg_g2_apply(dg_g2 *g, int op, double tau_scale, const int *kind,
  * points [2][e][q][q] or NULL; src unused), 6 divergence a(q, u) (:265-316;
  * scale, form 0 standard / 1 weak / 2 strong), 7 pressure gradient b(v, p)
  * (:322-366; form 0 / 1), 8 vorticity moments (:610-618, before the inverse
- * mass).  Vector fields: 2 components of ncells*n*n values each. */
+ * mass), and the boundary-data right-hand sides with data sampled by the
+ * caller at the face points (fdata, device): 10 pressure-Dirichlet data
+ * (:241-259; g_p [e][4][q], tau_scale), 11 viscous boundary data (:494-527;
+ * [e][4][3][q] = g0 g1 on velocity-Dirichlet sides, h0 h1 g_p on
+ * velocity-Neumann sides; nu), 12 consistent pressure Neumann data
+ * (:621-672; history velocity levels hist[j], vorticity levels vort[j],
+ * beta, nu, fdata [e][4][2][q] = dg/dt - f or NULL).  Vector fields: 2
+ * components of ncells*n*n values each. */
 typedef struct {
   int op;
   double tau_scale;
@@ -316,6 +323,8 @@ typedef struct {
   double beta[4];
   const double *gdata[4];          /* device */
   const double *body;              /* device */
+  const double *vort[4];           /* device */
+  const double *fdata;             /* device */
 } dg_g2_params;
 int dg_g2_operator(dg_g2 *g, const dg_g2_params *p, const double *src, double *dst,
                    void *stream);

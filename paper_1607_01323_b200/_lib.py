@@ -106,7 +106,8 @@ class G2Params(ctypes.Structure):
                 ("tau_d", ctypes.c_void_p), ("tau_c", ctypes.c_void_p),
                 ("scale", ctypes.c_double), ("form", ctypes.c_int), ("n_hist", ctypes.c_int),
                 ("hist", ctypes.c_void_p * 4), ("beta", ctypes.c_double * 4),
-                ("gdata", ctypes.c_void_p * 4), ("body", ctypes.c_void_p)]
+                ("gdata", ctypes.c_void_p * 4), ("body", ctypes.c_void_p),
+                ("vort", ctypes.c_void_p * 4), ("fdata", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p

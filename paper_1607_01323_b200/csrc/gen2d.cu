@@ -82,7 +82,8 @@ int dg_g2_operator(dg_g2 *g, const dg_g2_params *p, const double *src, double *d
                    void *stream) {
   if (!g || !p || !dst) return inval("null argument");
   const int op = p->op;
-  if (op < kG2Laplace || op > kG2Vorticity) return inval("general 2D: unknown operator");
+  if (op < kG2Laplace || op > kG2PressureNeumann || op == kG2LaplaceLocal)
+    return inval("general 2D: unknown operator");
   if (!p->kind) return inval("general 2D: boundary kinds required");
   G2Params prm{};
   prm.op = op;
@@ -95,18 +96,22 @@ int dg_g2_operator(dg_g2 *g, const dg_g2_params *p, const double *src, double *d
   prm.tau_c = p->tau_c;
   prm.scale = p->scale;
   prm.form = p->form;
-  if (op == kG2Convective) {
+  prm.fdata = p->fdata;
+  if (op == kG2Convective || op == kG2PressureNeumann) {
     if (p->n_hist < 1 || p->n_hist > kG2MaxHist) return inval("need 1..4 history levels");
     prm.n_hist = p->n_hist;
     for (int j = 0; j < p->n_hist; ++j) {
       if (!p->hist[j]) return inval("null history level");
-      if (p->hist[j] == dst) return inval("convective term: dst must not alias a history level");
+      if (op == kG2PressureNeumann && !p->vort[j]) return inval("null vorticity level");
+      if (p->hist[j] == dst || p->vort[j] == dst)
+        return inval("dst must not alias a history level");
       prm.hist[j] = p->hist[j];
       prm.beta[j] = p->beta[j];
       prm.gdata[j] = p->gdata[j];
+      prm.vort[j] = p->vort[j];
     }
     prm.body = p->body;
-  } else {
+  } else if (op != kG2GpDirichlet && op != kG2ViscousBc) {
     if (!src) return inval("null argument");
     if (src == dst) return inval("general 2D: src and dst must not alias");
   }

@@ -25,7 +25,10 @@
 //   part for the Jacobi diagonal), viscous Helmholtz, projection, convective
 //   term (over-integration geometry, history levels, Dirichlet data, body
 //   force), divergence (standard / weak / strong), pressure gradient
-//   (standard / weak), vorticity (before its inverse mass).
+//   (standard / weak), vorticity (before its inverse mass), and the
+//   boundary-data right-hand sides (pressure-Dirichlet data, viscous
+//   boundary data, consistent pressure Neumann data) whose data callables
+//   the host samples at the face points.
 #pragma once
 #include "common.cuh"
 
@@ -44,6 +47,9 @@ enum G2Op : int {
   kG2Gradient = 7,
   kG2Vorticity = 8,
   kG2LaplaceLocal = 9,  // neighbour traces zeroed (block-diagonal part)
+  kG2GpDirichlet = 10,  // pressure-Dirichlet data (operators.py:241-259)
+  kG2ViscousBc = 11,    // viscous boundary data (operators.py:494-527)
+  kG2PressureNeumann = 12,  // consistent pressure Neumann data (operators.py:621-672)
 };
 
 struct G2Tab {  // 1D tables of the rule (S, D: n_q x n, row-major)
@@ -81,6 +87,11 @@ struct G2Params {
   double beta[kG2MaxHist];
   const double *gdata[kG2MaxHist];  // [e][4][2][q] or null (homogeneous)
   const double *body;     // [2][e][q][q] body force at the points, or null
+  const double *vort[kG2MaxHist];   // pressure Neumann: vorticity levels (scalar)
+  const double *fdata;    // boundary-data ops: host-sampled data per (cell, slot, point):
+                          //   gp Dirichlet [e][4][q]; viscous bc [e][4][3][q]
+                          //   (g0 g1 - | h0 h1 g_p); pressure Neumann [e][4][2][q]
+                          //   (dg/dt - f), or null
 };
 
 // value and reference gradient of a cell field at face point q of slot s
@@ -114,12 +125,14 @@ __device__ __forceinline__ void g2_trace(const double *u, int N, const G2Tab &T,
 }
 
 __device__ __forceinline__ int g2_nci(int op) {
+  if (op == kG2GpDirichlet || op == kG2ViscousBc) return 0;
+  if (op == kG2PressureNeumann) return 3;  // u (2) + vorticity (1)
   return (op == kG2Helmholtz || op == kG2Projection || op == kG2Convective ||
           op == kG2Divergence || op == kG2Vorticity) ? 2 : 1;
 }
 __device__ __forceinline__ int g2_nco(int op) {
-  return (op == kG2Helmholtz || op == kG2Projection || op == kG2Convective || op == kG2Gradient)
-             ? 2 : 1;
+  return (op == kG2Helmholtz || op == kG2Projection || op == kG2Convective ||
+          op == kG2Gradient || op == kG2ViscousBc) ? 2 : 1;
 }
 
 // Lax-Friedrichs F*(u) . n with the own outward normal (operators.py:597-604)
@@ -140,14 +153,15 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
   const int op = prm.op;
   const int nci = g2_nci(op), nco = g2_nco(op);
   const int64_t nc = g.ncells;
-  __shared__ double su[CPB][2][kG2MaxN * kG2MaxN];
+  __shared__ double su[CPB][3][kG2MaxN * kG2MaxN];
   __shared__ double sq[CPB][2][3][QS];          // [comp][value | ref-x | ref-y test]
   __shared__ double sf[CPB][4][2][3][kG2MaxQ];  // [slot][comp][value | ref-x | ref-y]
   const int cs = threadIdx.x / TPC, t = threadIdx.x % TPC;
   const int64_t e = (int64_t)blockIdx.x * CPB + cs;
   const bool valid = e < nc;
-  const int nlev = op == kG2Convective ? prm.n_hist : 1;
-  const bool faces = op == kG2Laplace || op == kG2LaplaceLocal ||
+  const bool bdata = op == kG2GpDirichlet || op == kG2ViscousBc || op == kG2PressureNeumann;
+  const int nlev = (op == kG2Convective || op == kG2PressureNeumann) ? prm.n_hist : 1;
+  const bool faces = bdata || op == kG2Laplace || op == kG2LaplaceLocal ||
                      (op == kG2Helmholtz && prm.nu != 0.0) ||
                      (op == kG2Projection && prm.tau_c != nullptr) || op == kG2Convective ||
                      ((op == kG2Divergence || op == kG2Gradient) && prm.form != 0);
@@ -156,14 +170,16 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
   for (int i = t; i < 4 * 2 * 3 * kG2MaxQ; i += TPC) (&sf[cs][0][0][0][0])[i] = 0.0;
 
   for (int lev = 0; lev < nlev; ++lev) {
-    const double *in = op == kG2Convective ? prm.hist[lev] : src;
-    const double beta = op == kG2Convective ? prm.beta[lev] : 1.0;
+    const bool hist = op == kG2Convective || op == kG2PressureNeumann;
+    const double *in = hist ? prm.hist[lev] : src;
+    const double beta = hist ? prm.beta[lev] : 1.0;
     __syncthreads();
     for (int i = t; i < nci * NP; i += TPC) {
       const int c = i / NP, o = i % NP;
       double v = 0.0;
       if (valid) {
         if (op == kG2LaplaceLocal && prm.local_node >= 0) v = (o == prm.local_node) ? 1.0 : 0.0;
+        else if (c == 2) v = prm.vort[lev][e * NP + o];  // pressure Neumann: vorticity
         else v = in[((int64_t)c * nc + e) * NP + o];
       }
       su[cs][c][o] = v;
@@ -198,9 +214,9 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
     }
 
     // ---- volume: test data at the quadrature points ---------------------------
-    for (int i = t; i < QP; i += TPC) {
+    for (int i = t; i < (bdata ? 0 : QP); i += TPC) {
       const int qx = i % NQ, qy = i / NQ;
-      double v[2] = {0.0, 0.0}, px[2] = {0.0, 0.0}, py[2] = {0.0, 0.0};
+      double v[3] = {0.0, 0.0, 0.0}, px[3] = {0.0, 0.0, 0.0}, py[3] = {0.0, 0.0, 0.0};
       double jw = 0.0, j00 = 0.0, j01 = 0.0, j10 = 0.0, j11 = 0.0;
       if (valid) {
         jw = g.jxw[e * QP + i];
@@ -309,6 +325,9 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
         if (op == kG2Laplace || op == kG2LaplaceLocal) active &= kind != DG_BC_VELOCITY_DIRICHLET;
         if (op == kG2Helmholtz) active &= kind != DG_BC_VELOCITY_NEUMANN;
         if (op == kG2Projection || (op == kG2Divergence && prm.form == 2)) active &= kind == 0;
+        if (op == kG2GpDirichlet) active &= kind == DG_BC_VELOCITY_NEUMANN;
+        if (op == kG2ViscousBc) active &= kind != 0;
+        if (op == kG2PressureNeumann) active &= kind == DG_BC_VELOCITY_DIRICHLET;
         if (!active) continue;
         const int64_t fi = (e * 4 + s) * NQ + q;
         const double sj = g.fsj[fi];
@@ -317,8 +336,8 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
         const double *J = g.fjit + (e * 4 + s) * 4 * NQ + q;
         const double j00 = J[0], j01 = J[NQ], j10 = J[2 * NQ], j11 = J[3 * NQ];
         // own traces (value, physical gradient) of the input components
-        double vo[2] = {0.0, 0.0}, xo[2] = {0.0, 0.0}, yo[2] = {0.0, 0.0};
-        double vn[2] = {0.0, 0.0}, xn[2] = {0.0, 0.0}, yn[2] = {0.0, 0.0};
+        double vo[3] = {0.0, 0.0, 0.0}, xo[3] = {0.0, 0.0, 0.0}, yo[3] = {0.0, 0.0, 0.0};
+        double vn[3] = {0.0, 0.0, 0.0}, xn[3] = {0.0, 0.0, 0.0}, yn[3] = {0.0, 0.0, 0.0};
         for (int c = 0; c < nci; ++c) {
           double gx, gy;
           g2_trace(su[cs][c], N, T, s, q, vo[c], gx, gy);
@@ -326,7 +345,7 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
           yo[c] = j10 * gx + j11 * gy;
         }
         int64_t en = -1;
-        if (kind == 0) {
+        if (kind == 0 && !bdata) {
           en = g.nbr[e * 4 + s];
           if (op != kG2LaplaceLocal) {
             const int sn = g.nslot[e * 4 + s];
@@ -342,7 +361,38 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
         }
         // value test V[a] and physical gradient test (Gx[a], Gy[a])
         double V[2] = {0.0, 0.0}, Gx[2] = {0.0, 0.0}, Gy[2] = {0.0, 0.0};
-        if (op == kG2Laplace || op == kG2LaplaceLocal) {  // operators.py:203-233
+        if (op == kG2PressureNeumann) {
+          // beta (div(u x u) + nu curl w), accumulated over the levels in the
+          // gradient slots of side (s, q); finalised after the level loop
+          const double div = xo[0] + yo[1];
+          const double c0 = vo[0] * div + vo[0] * xo[0] + vo[1] * yo[0];
+          const double c1 = vo[1] * div + vo[0] * xo[1] + vo[1] * yo[1];
+          sf[cs][s][0][1][q] += beta * (c0 + prm.nu * yo[2]);
+          sf[cs][s][0][2][q] += beta * (c1 - prm.nu * xo[2]);
+          continue;
+        }
+        if (op == kG2GpDirichlet) {
+          const double gp = prm.fdata ? prm.fdata[(e * 4 + s) * NQ + q] : 0.0;
+          V[0] = 2.0 * prm.tau_scale * g.tau[e] * gp * sj;
+          Gx[0] = -gp * nx * sj;
+          Gy[0] = -gp * ny * sj;
+        } else if (op == kG2ViscousBc) {
+          const double *fd = prm.fdata ? prm.fdata + (e * 4 + s) * 3 * NQ + q : nullptr;
+          const double d0 = fd ? fd[0] : 0.0, d1 = fd ? fd[NQ] : 0.0, d2 = fd ? fd[2 * NQ] : 0.0;
+          if (kind == DG_BC_VELOCITY_DIRICHLET) {
+            const double taub = g.tau[e] * prm.nu;
+            V[0] = 2.0 * taub * d0 * sj;
+            V[1] = 2.0 * taub * d1 * sj;
+            const double D01 = -prm.nu * (d0 * ny + d1 * nx) * sj;
+            Gx[0] = -2.0 * prm.nu * d0 * nx * sj;
+            Gy[0] = D01;
+            Gx[1] = D01;
+            Gy[1] = -2.0 * prm.nu * d1 * ny * sj;
+          } else {
+            V[0] = (d0 + d2 * nx) * sj;
+            V[1] = (d1 + d2 * ny) * sj;
+          }
+        } else if (op == kG2Laplace || op == kG2LaplaceLocal) {  // operators.py:203-233
           const double gno = nx * xo[0] + ny * yo[0];
           if (kind == 0) {
             const double gnn = nx * xn[0] + ny * yn[0];
@@ -424,6 +474,27 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
     }
   }
   __syncthreads();
+  if (op == kG2PressureNeumann) {  // V = -((dg/dt - f + hp) . n) sJxW (operators.py:657-669)
+    for (int i = t; i < 4 * NQ; i += TPC) {
+      const int s = i / NQ, q = i % NQ;
+      double V = 0.0;
+      if (valid && prm.kind[e * 4 + s] == DG_BC_VELOCITY_DIRICHLET) {
+        const int64_t fi = (e * 4 + s) * NQ + q;
+        const double nx = g.fnrm[(e * 4 + s) * 2 * NQ + q];
+        const double ny = g.fnrm[(e * 4 + s) * 2 * NQ + NQ + q];
+        double h0 = sf[cs][s][0][1][q], h1 = sf[cs][s][0][2][q];
+        if (prm.fdata) {
+          h0 = prm.fdata[((e * 4 + s) * 2 + 0) * NQ + q] + h0;
+          h1 = prm.fdata[((e * 4 + s) * 2 + 1) * NQ + q] + h1;
+        }
+        V = -(h0 * nx + h1 * ny) * g.fsj[fi];
+      }
+      sf[cs][s][0][0][q] = V;
+      sf[cs][s][0][1][q] = 0.0;
+      sf[cs][s][0][2][q] = 0.0;
+    }
+    __syncthreads();
+  }
 
   // ---- tests: volume integrate + face lifts (kernels.py:86-92, 159-186) -------
   for (int i = t; i < nco * NP; i += TPC) {

@@ -523,3 +523,115 @@ def eval_convective_rhs(space: GeneralSpace2D, bcs: GeneralBCs, history, betas, 
     if is_np:
         return space.from_element_major(out.cpu().numpy(), 2).reshape(shape)
     return out.view(shape)
+
+
+# ---------------------------------------------------------------------------
+# boundary-data right-hand sides: the data callables are the caller's Python
+# functions, sampled on the host at the face Gauss points (geometry xf);
+# traces of device fields and the lifts run on the device
+
+def _face_data(space, groups, ncomp):
+    """[e][4][ncomp][q] device array from (tag, fn(x) -> (ncomp, nb, q)) entries,
+    or None when there is no data."""
+    g = space.geom
+    out = None
+    for tag, fn in groups:
+        eb, sb = space.b_groups[tag]
+        val = np.asarray(fn(g.xf[:, sb, eb]), dtype=np.float64)
+        if val.ndim == 2:
+            val = val[None]
+        if out is None:
+            out = np.zeros((space.n_elements, 4, ncomp, space.n_q))
+        out[eb, sb, :val.shape[0]] = np.moveaxis(val, 0, 1)
+    if out is None:
+        return None
+    return _torch().as_tensor(out).to("cuda")
+
+
+def _like_out(space, out, ncomp, like):
+    torch = _torch()
+    if isinstance(like, torch.Tensor) or (isinstance(like, str) and like == "device"):
+        return out
+    return space.from_element_major(out.cpu().numpy(), ncomp)
+
+
+def gp_dirichlet_rhs(space: GeneralSpace2D, bcs: GeneralBCs, t: float, tau_scale: float = 1.0,
+                     like=None):
+    """Pressure-Dirichlet data g_p on velocity-Neumann faces (operators.py:241-259)."""
+    torch = _torch()
+    fd = _face_data(space, [(tag, lambda x, bc=bc: bc.g_p(x, t)) for tag, bc in bcs.neumann
+                            if bc.g_p is not None], 1)
+    out = torch.empty(space.n_dofs, dtype=torch.float64, device="cuda")
+    prm = _params(space, 10, bcs)
+    prm.tau_scale = float(tau_scale)
+    prm.fdata = ctypes.c_void_p(fd.data_ptr() if fd is not None else 0)
+    _op(space, prm, None, out)
+    return _like_out(space, out, 1, like)
+
+
+def viscous_rhs_bc(space: GeneralSpace2D, bcs: GeneralBCs, t: float, nu: float, like=None):
+    """Boundary-data terms of the viscous solve (operators.py:494-527)."""
+    torch = _torch()
+    groups = []
+    for tag, bc in bcs.dirichlet:
+        if bc.g is not None:
+            groups.append((tag, lambda x, bc=bc: np.concatenate(
+                [np.asarray(bc.g(x, t), dtype=np.float64), np.zeros((1,) + x.shape[1:])])))
+    for tag, bc in bcs.neumann:
+        if bc.h is None and bc.g_p is None:
+            continue
+        def fn(x, bc=bc):
+            h = np.asarray(bc.h(x, t), dtype=np.float64) if bc.h is not None else \
+                np.zeros((2,) + x.shape[1:])
+            gp = np.asarray(bc.g_p(x, t), dtype=np.float64) if bc.g_p is not None else \
+                np.zeros(x.shape[1:])
+            return np.concatenate([h, gp[None]])
+        groups.append((tag, fn))
+    fd = _face_data(space, groups, 3)
+    out = torch.empty(2 * space.n_dofs, dtype=torch.float64, device="cuda")
+    prm = _params(space, 11, bcs)
+    prm.nu = float(nu)
+    prm.fdata = ctypes.c_void_p(fd.data_ptr() if fd is not None else 0)
+    _op(space, prm, None, out)
+    return _like_out(space, out, 2, like)
+
+
+def eval_pressure_neumann_rhs(space: GeneralSpace2D, bcs: GeneralBCs, history, vorticity_history,
+                              betas, nu: float, t_np1: float, body_force=None, like=None):
+    """Consistent pressure Neumann data on velocity-Dirichlet faces
+    (operators.py:621-672): -(dg/dt + sum_i beta_i (div(u u) + nu curl w)
+    - f) . n against the pressure test functions."""
+    torch = _torch()
+    if len(history) < 1 or len(history) > 4:
+        raise ValueError("need 1..4 history levels")
+    if len(vorticity_history) < len(history) or len(betas) < len(history):
+        raise ValueError("need one vorticity level and one beta per history level")
+    out = torch.zeros(space.n_dofs, dtype=torch.float64, device="cuda")
+    if not bcs.dirichlet:
+        return _like_out(space, out, 1, like if like is not None else
+                         (history[0] if isinstance(history[0], torch.Tensor) else None))
+    groups = []
+    for tag, bc in bcs.dirichlet:
+        def fn(x, bc=bc):
+            h = np.asarray(bc.dg_dt(x, t_np1), dtype=np.float64) if bc.dg_dt is not None else \
+                np.zeros((2,) + x.shape[1:])
+            if body_force is not None:
+                h = h - np.asarray(body_force(x, t_np1), dtype=np.float64)
+            return h
+        if bc.dg_dt is not None or body_force is not None:
+            groups.append((tag, fn))
+    fd = _face_data(space, groups, 2)
+    us = [_field(space, u, 2)[0] for u in history]
+    ws = [_field(space, w, 1)[0] for w in vorticity_history[:len(history)]]
+    prm = _params(space, 12, bcs)
+    prm.nu = float(nu)
+    prm.n_hist = len(us)
+    for j, (u, w) in enumerate(zip(us, ws)):
+        prm.hist[j] = ctypes.c_void_p(u.data_ptr())
+        prm.vort[j] = ctypes.c_void_p(w.data_ptr())
+        prm.beta[j] = float(betas[j])
+    prm.fdata = ctypes.c_void_p(fd.data_ptr() if fd is not None else 0)
+    _op(space, prm, None, out)
+    if like is None and isinstance(history[0], torch.Tensor):
+        like = "device"
+    return _like_out(space, out, 1, like)

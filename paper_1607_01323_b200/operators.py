@@ -443,6 +443,9 @@ def gp_dirichlet_rhs(space: DgSpace, bcs: ResolvedBCs, t: float, tau_scale: floa
                      like=None):
     """Pressure-Dirichlet data g_p on velocity-Neumann faces for the Poisson
     right side (operators.py:241-259)."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.gp_dirichlet_rhs(space, bcs, t, tau_scale, like)
     entries = [(tag, lambda x, bc=bc: bc.g_p(x, t)) for tag, bc in bcs.neumann
                if bc.g_p is not None]
     return _bnd_call("dg_gp_dirichlet_rhs", space, bcs, entries, 1, like, float(tau_scale))
@@ -452,6 +455,9 @@ def viscous_rhs_bc(space: DgSpace, bcs: ResolvedBCs, t: float, nu: float, like=N
     """Boundary-data terms of the viscous solve (operators.py:494-527):
     Dirichlet g with 2 tau nu and the symmetric-gradient test, Neumann
     h + g_p n."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.viscous_rhs_bc(space, bcs, t, nu, like)
     entries = [(tag, lambda x, bc=bc: bc.g(x, t)) for tag, bc in bcs.dirichlet
                if bc.g is not None]
 
@@ -545,6 +551,10 @@ def eval_pressure_neumann_rhs(space: DgSpace, bcs: ResolvedBCs, history, vortici
     -(dg/dt + sum_i beta_i (div(u u) + nu curl w) - f) . n
     (operators.py:621-672).  dg/dt and f are sampled on the host at the face
     points (caller's callables); the traces run on the device."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.eval_pressure_neumann_rhs(space, bcs, history, vorticity_history, betas, nu,
+                                                 t_np1, body_force, like)
     import ctypes
     torch = _torch()
     nw = 1 if space.dim == 2 else 3

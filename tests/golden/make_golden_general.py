@@ -47,6 +47,18 @@ def g_data(x, t):
     return np.stack([np.sin(2.0 * x[0] + t) * np.cos(x[1]), 0.3 * np.cos(x[0] - 2.0 * t) + x[1]])
 
 
+def dg_data(x, t):
+    return np.stack([np.cos(2.0 * x[0] + t) * np.cos(x[1]), 0.6 * np.sin(x[0] - 2.0 * t)])
+
+
+def h_data(x, t):
+    return np.stack([0.4 * x[1] + np.sin(t), np.cos(3.0 * x[0]) * x[1]])
+
+
+def gp_data(x, t):
+    return 0.5 + np.sin(x[0] + 2.0 * x[1] + t)
+
+
 def force(x, t):
     return np.stack([0.2 + np.cos(x[1]) * np.sin(t), x[0] * x[1] - 0.1])
 
@@ -96,6 +108,9 @@ def main():
                                  for t, v in kinds.items()})
         spec_g = ops.BoundarySpec({t: (ops.DirichletBC(g_data, z2) if v == "D"
                                        else ops.NeumannBC(z2, z1)) for t, v in kinds.items()})
+        spec_d = ops.BoundarySpec({t: (ops.DirichletBC(g_data, dg_data) if v == "D"
+                                       else ops.NeumannBC(h_data, gp_data))
+                                   for t, v in kinds.items()})
         for k in degrees:
             space = DgSpace(mesh, k)
             bcs = spec.resolve(space)
@@ -139,6 +154,16 @@ def main():
             out[key + "_conv1"] = ops.eval_convective_rhs(space, bcs, [u], (1.0,), (0.0,), 0.0)
             out[key + "_conv2"] = ops.eval_convective_rhs(space, bcs_g, [u, u2], (2.0, -1.0),
                                                           (0.3, 0.2), 0.4, body_force=force)
+            bcs_d = spec_d.resolve(space)
+            w1 = rng.standard_normal((m, ne, m))
+            w2 = rng.standard_normal((m, ne, m))
+            out[key + "_w1"] = w1
+            out[key + "_w2"] = w2
+            out[key + "_gp"] = ops.gp_dirichlet_rhs(space, bcs_d, 0.35, tau_scale=1.7)
+            out[key + "_vbc"] = ops.viscous_rhs_bc(space, bcs_d, 0.35, 0.03)
+            out[key + "_pn"] = ops.eval_pressure_neumann_rhs(space, bcs_d, [u, u2], [w1, w2],
+                                                             (2.0, -1.0), 0.03, 0.45,
+                                                             body_force=force)
             print(name, k, "ne", ne, "flips", int(np.sum(f.flip)))
     np.savez_compressed(OUT, **out)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")

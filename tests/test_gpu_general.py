@@ -101,3 +101,31 @@ def test_general_vector_operators_match_reference(name, k):
     got = ops.eval_convective_rhs(space, bcs_g, [u, u2], (2.0, -1.0), (0.3, 0.2), 0.4,
                                   body_force=force)
     assert relerr(got, Z[key + "_conv2"]) < TOL
+
+
+def dg_data(x, t):
+    return np.stack([np.cos(2.0 * x[0] + t) * np.cos(x[1]), 0.6 * np.sin(x[0] - 2.0 * t)])
+
+
+def h_data(x, t):
+    return np.stack([0.4 * x[1] + np.sin(t), np.cos(3.0 * x[0]) * x[1]])
+
+
+def gp_data(x, t):
+    return 0.5 + np.sin(x[0] + 2.0 * x[1] + t)
+
+
+@pytest.mark.parametrize("name,k", [(n, k) for n, ks in CASES.items() for k in ks])
+def test_general_boundary_data_rhs_match_reference(name, k):
+    Z, space, _ = setup(name, k)
+    key = f"{name}_k{k}"
+    spec = ops.BoundarySpec({t: (ops.DirichletBC(g_data, dg_data) if v == "D"
+                                 else ops.NeumannBC(h_data, gp_data))
+                             for t, v in kinds(Z, name).items()})
+    bcs = spec.resolve(space)
+    u, u2, w1, w2 = Z[key + "_u"], Z[key + "_u2"], Z[key + "_w1"], Z[key + "_w2"]
+    assert relerr(ops.gp_dirichlet_rhs(space, bcs, 0.35, tau_scale=1.7), Z[key + "_gp"]) < TOL
+    assert relerr(ops.viscous_rhs_bc(space, bcs, 0.35, 0.03), Z[key + "_vbc"]) < TOL
+    got = ops.eval_pressure_neumann_rhs(space, bcs, [u, u2], [w1, w2], (2.0, -1.0), 0.03, 0.45,
+                                        body_force=force)
+    assert relerr(got, Z[key + "_pn"]) < TOL
