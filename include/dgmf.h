@@ -328,6 +328,14 @@ typedef struct {
 } dg_g2_params;
 int dg_g2_operator(dg_g2 *g, const dg_g2_params *p, const double *src, double *dst,
                    void *stream);
+/* multigrid transfer on a refined general mesh (multigrid.py:33-73):
+ * prolong (1): out[fine] (+)= (E_dy x E_dx) in[parent[fine]] with
+ * quadrant = 2 dy + dx; restrict (0): out[coarse] = sum over
+ * children[coarse][4] (-1 = none) of the transposed embedding.  Device
+ * int64 parent / children, int32 quadrant. */
+int dg_g2_transfer(int k, int prolong, int64_t n_fine, const int64_t *parent,
+                   const int *quadrant, int64_t n_coarse, const int64_t *children,
+                   const double *in, double *out, int add, void *stream);
 /* exact Jacobi diagonal (operators.py:675-730) */
 int dg_g2_laplace_diagonal(dg_g2 *g, double tau_scale, const int *kind,
                            double *diag, void *stream);

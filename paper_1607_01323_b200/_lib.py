@@ -160,6 +160,7 @@ PROTOTYPES = {
     "dg_g2_apply": [_P, _I, _D, _P, _P, _P, _I, _P],
     "dg_g2_laplace_diagonal": [_P, _D, _P, _P, _P],
     "dg_g2_operator": [_P, ctypes.POINTER(G2Params), _P, _P, _P],
+    "dg_g2_transfer": [_I, _I, _L, _P, _P, _L, _P, _P, _P, _I, _P],
     "dg_mg_vcycle": [_P, _P, _P, _P],
     "dg_halo_count": [_P, ctypes.POINTER(_L)],
     "dg_halo_pack": [_P, _P, _P, _P, _P],

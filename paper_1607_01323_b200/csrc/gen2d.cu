@@ -1,10 +1,13 @@
 // Host side of the general-geometry 2D operators (gen2d.cuh): the context
 // holds the caller's device geometry / connectivity arrays (not owned) and
 // the 1D tables; the C-ABI entry points are declared in include/dgmf.h.
+#include <algorithm>
 #include <string>
+#include <vector>
 
 #include "ctx.h"
 #include "gen2d.cuh"
+#include "tables.h"
 
 using namespace dg;
 
@@ -136,4 +139,33 @@ int dg_g2_laplace_diagonal(dg_g2 *g, double tau_scale, const int *kind, double *
   return DG_OK;
 }
 
+int dg_g2_transfer(int k, int prolong, int64_t n_fine, const int64_t *parent, const int *quadrant,
+                   int64_t n_coarse, const int64_t *children, const double *in, double *out,
+                   int add, void *stream) {
+  if (k < 1 || k + 1 > kG2MaxN) return inval("general 2D transfer: 1 <= k <= 7");
+  if (!in || !out || (prolong && (!parent || !quadrant)) || (!prolong && !children))
+    return inval("null argument");
+  if (in == out) return inval("transfer: in and out must not alias");
+  const int N = k + 1;
+  G2Emb T;
+  std::vector<double> nodes, V, Dv, pts(N);
+  gll_nodes(k, nodes);
+  for (int c = 0; c < 2; ++c) {
+    for (int q = 0; q < N; ++q) pts[q] = 0.5 * (nodes[q] + (c ? 1.0 : -1.0));
+    lagrange_tables(nodes, pts, V, Dv);
+    for (int i = 0; i < N * N; ++i) T.E[c][i] = V[i];
+  }
+  const int64_t n = (prolong ? n_fine : n_coarse) * N * N;
+  if (n == 0) return DG_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (prolong)
+    g2_prolong_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(in, out, N, n_fine, parent,
+                                                              quadrant, T, add);
+  else
+    g2_restrict_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(in, out, N, n_coarse, children, T);
+  DG_LAUNCH_CHECK(prolong ? "g2_prolong_kernel" : "g2_restrict_kernel");
+  return DG_OK;
+}
+
 }  // extern "C"
+

@@ -532,4 +532,61 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
   }
 }
 
+// Multigrid transfers on a refined general mesh (reference multigrid.py:
+// 33-73): child (quadrant qd = 2 dy + dx) of parent p carries the tensor
+// embedding (E_dy x E_dx) of p's polynomial; restriction is its transpose,
+// summed parent-centrically over the four children (fixed order, no atomics).
+struct G2Emb {
+  double E[2][kG2MaxN * kG2MaxN];  // E[c][q][i] = l_i(0.5 (x_q -/+ 1))
+};
+
+__global__ void g2_prolong_kernel(const double *__restrict__ xc, double *__restrict__ xf, int N,
+                                  int64_t nfine, const int64_t *__restrict__ parent,
+                                  const int *__restrict__ quadrant,
+                                  const __grid_constant__ G2Emb T, int add) {
+  const int NP = N * N;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nfine * NP; i += stride) {
+    const int64_t f = i / NP;
+    const int o = (int)(i % NP), x = o % N, y = o / N;
+    const int qd = quadrant[f], dx = qd & 1, dy = qd >> 1;
+    const double *pc = xc + parent[f] * NP;
+    double a = 0.0;
+    for (int j = 0; j < N; ++j) {
+      double b = 0.0;
+      for (int l = 0; l < N; ++l) b = fma(T.E[dx][x * N + l], pc[j * N + l], b);
+      a = fma(T.E[dy][y * N + j], b, a);
+    }
+    xf[i] = add ? xf[i] + a : a;
+  }
+}
+
+__global__ void g2_restrict_kernel(const double *__restrict__ xf, double *__restrict__ xc, int N,
+                                   int64_t ncoarse, const int64_t *__restrict__ children,
+                                   const __grid_constant__ G2Emb T) {
+  const int NP = N * N;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncoarse * NP;
+       i += stride) {
+    const int64_t p = i / NP;
+    const int o = (int)(i % NP), il = o % N, jl = o / N;
+    double acc = 0.0;
+    for (int qd = 0; qd < 4; ++qd) {
+      const int64_t f = children[p * 4 + qd];
+      if (f < 0) continue;
+      const int dx = qd & 1, dy = qd >> 1;
+      const double *cf = xf + f * NP;
+      double a = 0.0;
+      for (int y = 0; y < N; ++y) {
+        double b = 0.0;
+        for (int x = 0; x < N; ++x) b = fma(T.E[dx][x * N + il], cf[y * N + x], b);
+        a = fma(T.E[dy][y * N + jl], b, a);
+      }
+      acc += a;
+    }
+    xc[i] = acc;
+  }
+}
+
 }  // namespace dg
+

@@ -635,3 +635,168 @@ def eval_pressure_neumann_rhs(space: GeneralSpace2D, bcs: GeneralBCs, history, v
     if like is None and isinstance(history[0], torch.Tensor):
         like = "device"
     return _like_out(space, out, 1, like)
+
+
+# ---------------------------------------------------------------------------
+# zero-mean projections, penalty parameters (device tensors)
+
+def _basis_integrals(space: GeneralSpace2D):
+    """w_i = integral of l_i = (M 1)_i, element-major (device), cached."""
+    if getattr(space, "_wint", None) is None:
+        torch = _torch()
+        ones = torch.ones(space.n_dofs, dtype=torch.float64, device="cuda")
+        space._wint = mass_apply(space, ones)
+        space._area = float(space.geom.volumes.sum())
+    return space._wint, space._area
+
+
+def zero_mean_project(space: GeneralSpace2D, p):
+    """Subtract the L2 mean (solvers.py:179-184)."""
+    t, is_np, shape = _field(space, p, 1)
+    w, area = _basis_integrals(space)
+    out = t - (t @ w) / area
+    return _result(space, out, is_np, shape, 1)
+
+
+def zero_mean_project_dual(space: GeneralSpace2D, b):
+    """b - (sum b / |Omega|) w, w_i = integral of l_i (solvers.py:187-198)."""
+    t, is_np, shape = _field(space, b, 1)
+    w, area = _basis_integrals(space)
+    out = t - (t.sum() / area) * w
+    return _result(space, out, is_np, shape, 1)
+
+
+def compute_penalty_parameters(space: GeneralSpace2D, u, dt: float, cfl: float, cfg):
+    """tau_D per cell and tau_C per (cell, slot) (operators.py:736-755; 2D
+    h = sqrt(V)); tau_c comes back in the [e][4] layout the general
+    apply_projection_operator takes (0 on boundary sides)."""
+    if cfl <= 0:
+        raise ValueError(f"CFL must be positive, got {cfl}")
+    torch = _torch()
+    t, _, _ = _field(space, u, 2)
+    w, _ = _basis_integrals(space)
+    ne, npl = space.n_elements, space.n_local
+    uw = (t.view(2, ne, npl) * w.view(1, ne, npl)).sum(dim=2)
+    vol = torch.as_tensor(space.geom.volumes, device="cuda")
+    norm = torch.hypot(uw[0], uw[1]) / vol
+    td = tc = None
+    if cfg.uses_divdiv:
+        td = (cfg.zeta_d_star / cfl) * norm * torch.sqrt(vol) * dt
+    if cfg.uses_jump:
+        tce = (cfg.zeta_c_star / cfl) * norm * dt
+        nbr = space._d["nbr"]
+        inner = nbr >= 0
+        tc = torch.where(inner, 0.5 * (tce[:, None] + tce[nbr.clamp(min=0)]),
+                         torch.zeros(nbr.shape, dtype=torch.float64, device="cuda"))
+    return td, tc
+
+
+# ---------------------------------------------------------------------------
+# geometric multigrid on refined general meshes (multigrid.py:33-175)
+
+class Transfer2D:
+    """Polynomial embedding between a general space and its refinement
+    (multigrid.py:33-73): needs the fine mesh's parent / quadrant links."""
+
+    def __init__(self, coarse: GeneralSpace2D, fine: GeneralSpace2D):
+        if getattr(fine.mesh, "parent", None) is None:
+            raise ValueError("fine mesh lacks parent links; build the hierarchy by refinement")
+        if coarse.k != fine.k:
+            raise ValueError("multigrid levels need the same degree")
+        torch = _torch()
+        parent = np.asarray(fine.mesh.parent, np.int64)
+        quad = np.asarray(fine.mesh.quadrant, np.int32)
+        children = -np.ones((coarse.n_elements, 4), np.int64)
+        children[parent, quad] = np.arange(fine.n_elements)
+        self.coarse, self.fine = coarse, fine
+        self._parent = torch.as_tensor(parent).to("cuda")
+        self._quad = torch.as_tensor(quad).to("cuda")
+        self._children = torch.as_tensor(children).to("cuda")
+
+    def _call(self, prolong, x, out, add=0):
+        P = lambda t: ctypes.c_void_p(t.data_ptr())
+        _lib.call("dg_g2_transfer", self.fine.k, int(prolong), self.fine.n_elements,
+                  P(self._parent), P(self._quad), self.coarse.n_elements, P(self._children),
+                  P(x), P(out), int(add), _stream())
+
+    def prolong(self, xc, out=None, add=False):
+        t, is_np, _ = _field(self.coarse, xc, 1)
+        torch = _torch()
+        if out is None:
+            out = torch.empty(self.fine.n_dofs, dtype=torch.float64, device="cuda")
+        self._call(True, t, out, int(add))
+        return self.fine.from_element_major(out.cpu().numpy(), 1) if is_np else out
+
+    def restrict(self, xf):
+        torch = _torch()
+        t, is_np, _ = _field(self.fine, xf, 1)
+        out = torch.empty(self.coarse.n_dofs, dtype=torch.float64, device="cuda")
+        self._call(False, t, out)
+        return self.coarse.from_element_major(out.cpu().numpy(), 1) if is_np else out
+
+
+class GeneralMultigrid:
+    """V-cycle preconditioner on a refined general hierarchy (reference
+    MultigridHierarchy, multigrid.py:76-151): Chebyshev(degree, range)-Jacobi
+    smoothing with the device operator, a seeded 20-step Lanczos lambda_max
+    per level, the fixed-count coarse Chebyshev; every operation is a device
+    kernel.  ``vcycle`` drops into ``solvers.pcg(op, mg.vcycle, b)``."""
+
+    def __init__(self, spaces, bc_spec, tau_scale: float = 1.0, degree: int = 5,
+                 smoothing_range: float = 20.0, coarse_tol: float = 1e-3, est_iters: int = 20,
+                 safety: float = 1.1, seed: int = 987, project=None):
+        import math
+        from .solvers import ChebyshevConfig, eigen_estimate_via_cg
+        if len(spaces) < 1:
+            raise ValueError("hierarchy needs at least one level")
+        rng = np.random.default_rng(seed)
+        self.levels = []
+        self.tau_scale = tau_scale
+        for lvl, space in enumerate(spaces):
+            bcs = bc_spec.resolve(space)
+            op = (lambda s, b: lambda p: apply_pressure_laplace(s, p, b, tau_scale))(space, bcs)
+            diag = laplace_diagonal(space, bcs, tau_scale)
+            m, ne = space.k + 1, space.n_elements
+            seed_vec = _torch().as_tensor(space.to_element_major(
+                rng.standard_normal((m, ne, m)), 1).ravel()).to("cuda")
+            est_op = op
+            if project is not None:
+                seed_vec = project(space, seed_vec)
+                est_op = (lambda o, s: lambda p: project(s, o(p)))(op, space)
+            lmax, lmin = eigen_estimate_via_cg(est_op, diag, seed_vec, est_iters)
+            level = {"space": space, "op": op, "diag": diag,
+                     "cheb": ChebyshevConfig(degree, smoothing_range, safety * lmax),
+                     "lambda_max": safety * lmax}
+            if lvl == 0:
+                kappa = (safety * lmax) / max(lmin / safety, 1e-12 * lmax)
+                q = (math.sqrt(kappa) - 1.0) / (math.sqrt(kappa) + 1.0)
+                n = math.ceil(math.log(2.0 / coarse_tol) / -math.log(max(q, 1e-12)))
+                level["coarse_iters"] = max(n, 1)
+                level["coarse_range"] = kappa
+            self.levels.append(level)
+        self.transfers = [Transfer2D(c["space"], f["space"])
+                          for c, f in zip(self.levels[:-1], self.levels[1:])]
+
+    @property
+    def n_levels(self):
+        return len(self.levels)
+
+    def vcycle(self, b):
+        top = self.levels[-1]["space"]
+        t, is_np, shape = _field(top, b, 1)
+        x = self._cycle(t, self.n_levels - 1)
+        return top.from_element_major(x.cpu().numpy(), 1).reshape(shape) if is_np else x.view(shape)
+
+    def _cycle(self, b, lvl):
+        from .solvers import ChebyshevConfig, chebyshev_smooth
+        lev = self.levels[lvl]
+        if lvl == 0:
+            cfg = ChebyshevConfig(lev["coarse_iters"], max(lev["coarse_range"], 1.0 + 1e-8),
+                                  lev["cheb"].lambda_max)
+            return chebyshev_smooth(lev["op"], lev["diag"], cfg, b)
+        x = chebyshev_smooth(lev["op"], lev["diag"], lev["cheb"], b)
+        r = b - lev["op"](x)
+        tr = self.transfers[lvl - 1]
+        xc = self._cycle(tr.restrict(r), lvl - 1)
+        tr.prolong(xc, out=x, add=True)
+        return chebyshev_smooth(lev["op"], lev["diag"], lev["cheb"], b, x)

@@ -645,6 +645,9 @@ def compute_penalty_parameters(space: DgSpace, u, dt: float, cfl: float, cfg: Va
     (operators.py:736-755; h = V^(1/dim)).  Returns device tensors (tau_c in
     the face layout apply_projection_operator accepts) or None where the
     variant has no such term."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.compute_penalty_parameters(space, u, dt, cfl, cfg)
     if cfl <= 0:
         raise ValueError(f"CFL must be positive, got {cfl}")
     torch = _torch()

@@ -194,11 +194,17 @@ def _zm(space, v, name):
 
 def zero_mean_project(space, p):
     """Subtract the L2 mean (solvers.py:179-184)."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.zero_mean_project(space, p)
     return _zm(space, p, "dg_zero_mean")
 
 
 def zero_mean_project_dual(space, b):
     """b - (sum b / |Omega|) w, w_i = integral of l_i (solvers.py:187-198)."""
+    if getattr(space, "is_general", False):
+        from . import general
+        return general.zero_mean_project_dual(space, b)
     return _zm(space, b, "dg_zero_mean_dual")
 
 

@@ -19,10 +19,13 @@ def load():
 def mesh(Z, name):
     faces = SimpleNamespace(**{k: Z[f"{name}_{k}"] for k in ("em", "sm", "ep", "sp", "flip")})
     bnd = SimpleNamespace(elem=Z[f"{name}_belem"], slot=Z[f"{name}_bslot"], tag=Z[f"{name}_btag"])
-    return SimpleNamespace(geom_degree=int(Z[f"{name}_geom_degree"]),
-                           geom_nodes=Z[f"{name}_geom_nodes"], interior=faces, boundary=bnd,
-                           tag_names=[str(t) for t in Z[f"{name}_tags"]],
-                           n_elements=Z[f"{name}_geom_nodes"].shape[2])
+    m = SimpleNamespace(geom_degree=int(Z[f"{name}_geom_degree"]),
+                        geom_nodes=Z[f"{name}_geom_nodes"], interior=faces, boundary=bnd,
+                        tag_names=[str(t) for t in Z[f"{name}_tags"]],
+                        n_elements=Z[f"{name}_geom_nodes"].shape[2], parent=None, quadrant=None)
+    if f"{name}_parent" in Z:
+        m.parent, m.quadrant = Z[f"{name}_parent"], Z[f"{name}_quadrant"]
+    return m
 
 
 def kinds(Z, name):

@@ -27,7 +27,9 @@ sys.path.insert(0, "/root/reference/pkg/src")
 import numpy as np  # noqa: E402
 
 from dgins import operators as ops  # noqa: E402
-from dgins.cylinder import build_cylinder_mesh  # noqa: E402
+from dgins import solvers as sol  # noqa: E402
+from dgins.cylinder import build_cylinder_mesh, cylinder_mesh_hierarchy  # noqa: E402
+from dgins.multigrid import MultigridHierarchy  # noqa: E402
 from dgins.mesh import build_box_mesh  # noqa: E402
 from dgins.spaces import DgSpace  # noqa: E402
 
@@ -164,7 +166,64 @@ def main():
             out[key + "_pn"] = ops.eval_pressure_neumann_rhs(space, bcs_d, [u, u2], [w1, w2],
                                                              (2.0, -1.0), 0.03, 0.45,
                                                              body_force=force)
+            out[key + "_zm"] = sol.zero_mean_project(space, p)
+            out[key + "_zmd"] = sol.zero_mean_project_dual(space, p)
+            td, tcf = ops.compute_penalty_parameters(space, u, 1e-3, 0.8,
+                                                     ops.VariantConfig("V4", 1.3, 0.7))
+            out[key + "_pen_d"] = td
+            out[key + "_pen_c"] = tcf
             print(name, k, "ne", ne, "flips", int(np.sum(f.flip)))
+    # multigrid on the refined cylinder hierarchy (multigrid.py:76-175):
+    # pressure-Dirichlet outflow (non-singular) and all velocity-Dirichlet
+    # sides (pure Neumann pressure: projected Lanczos, dual-projected rhs)
+    for mname, kinds in (("mgcyl", {"inflow": "D", "outflow": "N", "wall": "D", "cylinder": "D"}),
+                         ("mgcylN", {"inflow": "D", "outflow": "D", "wall": "D", "cylinder": "D"})):
+        meshes = cylinder_mesh_hierarchy(1, k_geo=4)
+        k = 2
+        spaces = [DgSpace(m, k) for m in meshes]
+        spec = ops.BoundarySpec({t: (ops.DirichletBC(z2, z2) if v == "D" else ops.NeumannBC(z2, z1))
+                                 for t, v in kinds.items()})
+        singular = mname == "mgcylN"
+        mg = MultigridHierarchy(spaces, spec,
+                                project=sol.zero_mean_project if singular else None)
+        top = spaces[-1]
+        bcs = spec.resolve(top)
+        m, ne = k + 1, top.mesh.n_elements
+        b = rng.standard_normal((m, ne, m))
+        if singular:
+            b = sol.zero_mean_project_dual(top, b)
+        out[f"{mname}_b"] = b
+        out[f"{mname}_lmax"] = np.array([lv.cheb.lambda_max for lv in mg.levels])
+        out[f"{mname}_coarse_iters"] = np.array(mg.levels[0].coarse_iters)
+        out[f"{mname}_vcycle"] = mg.vcycle(b)
+        if singular:
+            op = lambda x: sol.zero_mean_project_dual(top, ops.apply_pressure_laplace(top, x, bcs))
+        else:
+            op = lambda x: ops.apply_pressure_laplace(top, x, bcs)
+        hist = []
+
+        def rec(r):
+            z = mg.vcycle(r)
+            hist.append(np.sqrt(max(np.vdot(r, z).real, 0.0)))
+            return z
+        x, st = sol.pcg(op, rec, b, rel_tol=1e-8, max_iter=100)
+        out[f"{mname}_pcg_iters"] = np.array(st.iterations)
+        out[f"{mname}_pcg_hist"] = np.array(hist)
+        out[f"{mname}_pcg_x"] = x
+        for lvl, mm in enumerate(meshes):
+            pre = f"{mname}_L{lvl}"
+            f, bb = mm.interior, mm.boundary
+            out[pre + "_geom_nodes"] = mm.geom_nodes
+            out[pre + "_geom_degree"] = np.array(mm.geom_degree)
+            for kk in ("em", "sm", "ep", "sp", "flip"):
+                out[pre + "_" + kk] = np.asarray(getattr(f, kk))
+            out[pre + "_belem"], out[pre + "_bslot"], out[pre + "_btag"] = bb.elem, bb.slot, bb.tag
+            out[pre + "_tags"] = np.array(mm.tag_names)
+            out[pre + "_kinds"] = np.array([f"{t}:{kinds.get(t, '-')}" for t in mm.tag_names])
+            if mm.parent is not None:
+                out[pre + "_parent"] = np.asarray(mm.parent)
+                out[pre + "_quadrant"] = np.asarray(mm.quadrant)
+        print(mname, "levels", len(meshes), "iters", st.iterations, "coarse", mg.levels[0].coarse_iters)
     np.savez_compressed(OUT, **out)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")
 

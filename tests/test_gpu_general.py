@@ -129,3 +129,51 @@ def test_general_boundary_data_rhs_match_reference(name, k):
     got = ops.eval_pressure_neumann_rhs(space, bcs, [u, u2], [w1, w2], (2.0, -1.0), 0.03, 0.45,
                                         body_force=force)
     assert relerr(got, Z[key + "_pn"]) < TOL
+
+
+@pytest.mark.parametrize("name,k", [(n, k) for n, ks in CASES.items() for k in ks])
+def test_general_projections_and_penalties_match_reference(name, k):
+    Z, space, _ = setup(name, k)
+    key = f"{name}_k{k}"
+    p, u = Z[key + "_p"], Z[key + "_u"]
+    assert relerr(sol.zero_mean_project(space, p), Z[key + "_zm"]) < TOL
+    assert relerr(sol.zero_mean_project_dual(space, p), Z[key + "_zmd"]) < TOL
+    td, tc = ops.compute_penalty_parameters(space, torch.as_tensor(
+        space.to_element_major(u, 2).ravel()).cuda(), 1e-3, 0.8, ops.VariantConfig("V4", 1.3, 0.7))
+    assert relerr(td.cpu().numpy(), Z[key + "_pen_d"]) < TOL
+    f = space.mesh.interior
+    assert relerr(tc.cpu().numpy()[f.em, f.sm], Z[key + "_pen_c"]) < TOL
+    assert relerr(tc.cpu().numpy()[f.ep, f.sp], Z[key + "_pen_c"]) < TOL
+
+
+@pytest.mark.parametrize("mname", ["mgcyl", "mgcylN"])
+def test_general_multigrid_matches_reference(mname):
+    """Refined cylinder hierarchy (136 -> 544 curved cells, k = 2): per-level
+    Lanczos lambda_max, the coarse Chebyshev count, one V-cycle and the
+    MG-preconditioned CG (iterations and residual history) against the
+    reference's MultigridHierarchy (multigrid.py:76-175)."""
+    from paper_1607_01323_b200.general import GeneralMultigrid
+    Z = load()
+    k = 2
+    spaces = [GeneralSpace2D(mesh(Z, f"{mname}_L{lvl}"), k) for lvl in range(2)]
+    spec = ops.BoundarySpec({t: (ops.DirichletBC(None) if v == "D" else ops.NeumannBC(None, None))
+                             for t, v in kinds(Z, f"{mname}_L0").items()})
+    singular = mname == "mgcylN"
+    mg = GeneralMultigrid(spaces, spec, project=sol.zero_mean_project if singular else None)
+    lm = np.array([lv["lambda_max"] for lv in mg.levels])
+    assert relerr(lm, Z[f"{mname}_lmax"]) < 1e-10
+    assert mg.levels[0]["coarse_iters"] == int(Z[f"{mname}_coarse_iters"])
+    top = spaces[-1]
+    b = Z[f"{mname}_b"]
+    assert relerr(mg.vcycle(b), Z[f"{mname}_vcycle"]) < 1e-9
+    bcs = spec.resolve(top)
+    bt = torch.as_tensor(top.to_element_major(b, 1).ravel()).cuda()
+    if singular:
+        op = lambda x: sol.zero_mean_project_dual(top, ops.apply_pressure_laplace(top, x, bcs))
+    else:
+        op = lambda x: ops.apply_pressure_laplace(top, x, bcs)
+    x, st = sol.pcg(op, mg.vcycle, bt, rel_tol=1e-8, max_iter=100)
+    assert st.iterations == int(Z[f"{mname}_pcg_iters"])
+    hw = Z[f"{mname}_pcg_hist"][:st.iterations + 1]
+    assert np.allclose(np.asarray(st.history), hw, rtol=1e-8, atol=0)
+    assert relerr(top.from_element_major(x.cpu().numpy(), 1), Z[f"{mname}_pcg_x"]) < 1e-7
