@@ -235,6 +235,38 @@ def run_c4_step(nsteps=3):
             "steps": steps}
 
 
+def run_degree_sweep(peak_gbs):
+    """C5 degree sweep: SIP Laplace vmult at 64^3 cells,
+    Q2..Q7, walls as C1; DoF/s and the HBM roofline fraction at 16 B/DoF
+    (CUDA events, 20 reps after warm-up; inputs > L2 from Q3 up)."""
+    import torch
+    from paper_1607_01323_b200 import mesh as M, operators as ops
+    from paper_1607_01323_b200.spaces import DgSpace
+    out = {}
+    mesh = M.build_box_mesh(((0, 1),) * 3, (64, 64, 64))
+    for k in range(2, 8):
+        space = DgSpace(mesh, k)
+        bcs = ops.BoundarySpec({t: ops.DirichletBC(None) for t in mesh.boundary_tags()}).resolve(space)
+        x = torch.rand(space.n_dofs, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+        f = lambda: ops.apply_pressure_laplace(space, x, bcs)
+        for _ in range(3):
+            f()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 20
+        dps = space.n_dofs / ms * 1e3
+        out[f"Q{k}"] = {"dofs": space.n_dofs, "ms": ms, "dof_per_s": dps,
+                        "hbm_frac": dps * 16.0 / (peak_gbs * 1e9)}
+        del x, y
+    return out
+
+
 def run_small_configs():
     """BASELINE configs 1 and 3 (latency / fp64-heavy cases, not roofline
     configs): C1 8^3 Q3 walls Laplace vmult with both wall kinds; C3
@@ -453,9 +485,10 @@ def main():
     step = None
     if rank == 0 and world == 1 and not args.no_step:
         step = run_c4_step()
-    small = None
+    small = dsweep = None
     if rank == 0 and world == 1 and not args.no_step:
         small = run_small_configs()
+        dsweep = run_degree_sweep(hbm_peak()[0])
     sweep = []
     if rank == 0 and world == 1 and args.sweep:
         sweep = run_sweep()
@@ -509,6 +542,8 @@ def main():
             line["c4_step"] = step
         if small:
             line["configs"] = small
+        if dsweep:
+            line["degree_sweep_64cubed"] = dsweep
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
