@@ -626,6 +626,17 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   __syncthreads();  // #5
   // ---- phase Z: z-lines of Q and G --------------------------------------------
   const int zbase = c * CS + ta * RP + tb;  // (y, x) line along z, stride N*RP
+  if (EPI == kEpiCheb && active && !(g.exp_flags & 8)) {  // DG_EXP=8: off (timing A/B)
+    // the Chebyshev epilogue reads rc, diag and x at this line's points:
+    // start their L2 fetches now so they overlap the z functionals / sweep
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const size_t gi = e * NP + (i * N + ta) * N + tb;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(ea.rc + gi));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(ea.diag + gi));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(ea.x + gi));
+    }
+  }
   if (has_line) {
 #pragma unroll
     for (int q = 0; q < N; ++q) v[q] = buf0[zbase + q * N * RP];
