@@ -25,6 +25,17 @@ from .spaces import _torch
 _REF_NORMALS = ((-1.0, 0.0), (1.0, 0.0), (0.0, -1.0), (0.0, 1.0))
 
 
+def _lagrange(nodes, x):
+    """V[q][i] = l_i(x_q) for the Lagrange basis on `nodes`."""
+    nodes, x = np.asarray(nodes, dtype=np.float64), np.asarray(x, dtype=np.float64)
+    V = np.ones((x.size, nodes.size))
+    for i in range(nodes.size):
+        for j in range(nodes.size):
+            if j != i:
+                V[:, i] *= (x - nodes[j]) / (nodes[i] - nodes[j])
+    return V
+
+
 def _vol(F, S1, S2):
     """out[a, e, b] = sum_j sum_i S1[a, j] S2[b, i] F[j, e, i] (kernel layout)."""
     return np.einsum("aj,jei,bi->aeb", S1, F, S2, optimize=True)
@@ -227,6 +238,26 @@ class GeneralSpace2D:
 
     def boundary_tags(self):
         return list(self.b_groups)
+
+    def node_coords(self):
+        """Physical coordinates of the field nodes, (2, m, ne, m) (restates
+        spaces.py:86-105: the geometry mapping evaluated at the GLL nodes of
+        degree k)."""
+        if getattr(self, "_node_coords", None) is None:
+            from .basis import gll_nodes
+            gb = get_basis(self.mesh.geom_degree, 2)
+            T = _lagrange(gb.nodes, gll_nodes(self.k))
+            X, Y = self.mesh.geom_nodes[0], self.mesh.geom_nodes[1]
+            self._node_coords = np.stack([_vol(X, T, T), _vol(Y, T, T)])
+        return self._node_coords
+
+    def interpolate(self, fn, t: float, ncomp: int):
+        """Nodal interpolant of fn(x, t) (spaces.py:107-113)."""
+        x = self.node_coords()
+        vals = fn(x, t)
+        if ncomp == 1 and np.asarray(vals).shape != (1,) + x.shape[1:]:
+            vals = np.asarray(vals)[None]
+        return np.ascontiguousarray(np.asarray(vals, dtype=float))
 
     def kinds(self, bcs):
         """Device int32 [e][4] boundary kinds of a resolved BC set."""

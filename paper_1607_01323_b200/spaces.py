@@ -152,6 +152,23 @@ class DgSpace:
             out.append(np.broadcast_to(c.reshape(shape), self.field_shape()))
         return np.stack(out)
 
+    def node_coords_reference(self):
+        """Node coordinates in the reference layout: (2, m, ne, m) in 2D
+        (spaces.py:86-105); element-major (3, ne, z, y, x) in 3D."""
+        x = self.node_coords()
+        if self.dim == 2:
+            return np.ascontiguousarray(x.transpose(0, 2, 1, 3))
+        return x
+
+    def interpolate(self, fn, t: float, ncomp: int):
+        """Nodal interpolant of fn(x, t) (spaces.py:107-113), x in the
+        reference layout; returns fn's values in that layout."""
+        x = self.node_coords_reference()
+        vals = fn(x, t)
+        if ncomp == 1 and np.asarray(vals).shape != (1,) + x.shape[1:]:
+            vals = np.asarray(vals)[None]
+        return np.ascontiguousarray(np.asarray(vals, dtype=float))
+
     # --- layout conversion (reference kernel layout <-> element-major) ---
     def is_reference_layout(self, a, ncomp):
         """2D reference kernel layout (m, ne, m) / (ncomp, m, ne, m)."""
@@ -185,3 +202,58 @@ def tag_kinds_tuple(space, kinds_by_tag):
     for t, kind in kinds_by_tag.items():
         out[TAG_NAMES.index(t)] = kind
     return tuple(out)
+
+
+class FieldVector:
+    """DoF storage for one field (reference spaces.py:18-58): ``data`` in the
+    reference layout ((ncomp, m, ne, m) in 2D, element-major in 3D), with the
+    element-major serialisation (component, element, [z,] y, x) the device
+    vectors use.  Works with DgSpace and the general 2D space."""
+
+    def __init__(self, data: np.ndarray, k: int):
+        self.data = data
+        self.k = k
+
+    @classmethod
+    def zeros(cls, space, ncomp: int) -> "FieldVector":
+        m = space.k + 1
+        ne = space.n_elements if hasattr(space, "n_elements") else space.mesh.n_elements
+        if space.dim == 2:
+            return cls(np.zeros((ncomp, m, ne, m)), space.k)
+        return cls(np.zeros((ncomp, ne, m, m, m)), space.k)
+
+    @property
+    def ncomp(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def n_elements(self) -> int:
+        return self.data.shape[2] if self.data.ndim == 4 else self.data.shape[1]
+
+    def copy(self) -> "FieldVector":
+        return FieldVector(self.data.copy(), self.k)
+
+    def has_nan(self) -> bool:
+        return bool(np.isnan(self.data).any())
+
+    def element_major(self) -> np.ndarray:
+        """Flat vector ordered (component, element, [z,] y-node, x-node)."""
+        if self.data.ndim == 4:
+            return np.ascontiguousarray(self.data.transpose(0, 2, 1, 3)).ravel()
+        return np.ascontiguousarray(self.data).ravel()
+
+    def to_device(self):
+        """The element-major vector as a CUDA tensor (the device operators'
+        input)."""
+        return _torch().as_tensor(self.element_major()).to("cuda")
+
+    @classmethod
+    def from_element_major(cls, flat, space, ncomp: int) -> "FieldVector":
+        if hasattr(flat, "detach"):
+            flat = flat.detach().cpu().numpy()
+        m = space.k + 1
+        ne = space.n_elements if hasattr(space, "n_elements") else space.mesh.n_elements
+        if space.dim == 2:
+            a = np.asarray(flat).reshape(ncomp, ne, m, m)
+            return cls(np.ascontiguousarray(a.transpose(0, 2, 1, 3)), space.k)
+        return cls(np.asarray(flat).reshape(ncomp, ne, m, m, m).copy(), space.k)

@@ -166,6 +166,7 @@ def main():
             out[key + "_pn"] = ops.eval_pressure_neumann_rhs(space, bcs_d, [u, u2], [w1, w2],
                                                              (2.0, -1.0), 0.03, 0.45,
                                                              body_force=force)
+            out[key + "_xn"] = space.node_coords()
             out[key + "_zm"] = sol.zero_mean_project(space, p)
             out[key + "_zmd"] = sol.zero_mean_project_dual(space, p)
             td, tcf = ops.compute_penalty_parameters(space, u, 1e-3, 0.8,

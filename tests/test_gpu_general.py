@@ -177,3 +177,12 @@ def test_general_multigrid_matches_reference(mname):
     hw = Z[f"{mname}_pcg_hist"][:st.iterations + 1]
     assert np.allclose(np.asarray(st.history), hw, rtol=1e-8, atol=0)
     assert relerr(top.from_element_major(x.cpu().numpy(), 1), Z[f"{mname}_pcg_x"]) < 1e-7
+
+
+@pytest.mark.parametrize("name,k", [(n, k) for n, ks in CASES.items() for k in ks])
+def test_general_node_coords_and_interpolate(name, k):
+    Z, space, _ = setup(name, k)
+    key = f"{name}_k{k}"
+    assert relerr(space.node_coords(), Z[key + "_xn"]) < 1e-14
+    f = space.interpolate(lambda x, t: np.stack([x[0] + t, x[0] * x[1]]), 0.5, 2)
+    assert f.shape == (2,) + Z[key + "_xn"].shape[1:]

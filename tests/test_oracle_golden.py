@@ -164,3 +164,18 @@ def test_element_local_pcg_matches_reference(name, k):
         else:               # converged solves: counts to +-2 (see make_golden)
             assert np.abs(iters - want).max() <= 2, (tag, iters, want)
             assert relerr(flat(x), Z[f"{key}_{tag}_x"]) < (1e-10 if tag == "el12" else 1e-6)
+
+
+def test_field_vector_roundtrip():
+    """FieldVector (reference spaces.py:18-58): zeros, element-major
+    serialisation and back, in the 2D reference layout."""
+    from types import SimpleNamespace
+    from paper_1607_01323_b200.spaces import FieldVector
+    space = SimpleNamespace(k=2, dim=2, n_elements=5)
+    fv = FieldVector.zeros(space, 2)
+    assert fv.data.shape == (2, 3, 5, 3) and fv.ncomp == 2 and fv.n_elements == 5
+    fv.data[...] = np.random.default_rng(0).standard_normal(fv.data.shape)
+    flat = fv.element_major()
+    assert np.array_equal(flat.reshape(2, 5, 3, 3), fv.data.transpose(0, 2, 1, 3))
+    back = FieldVector.from_element_major(flat, space, 2)
+    assert np.array_equal(back.data, fv.data) and not back.has_nan()
