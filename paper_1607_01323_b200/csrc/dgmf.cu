@@ -332,7 +332,7 @@ static int64_t laplace_bricks(const dg_ctx *c) {
   int bx = 0, by = 0, bz = 1;
   if (c->dim == 3) {
     static const int B[9][3] = {{0, 0, 0}, {0, 0, 0}, {8, 4, 4}, {4, 4, 4}, {4, 4, 2},
-                                {4, 2, 2}, {2, 2, 2}, {2, 2, 2}, {2, 2, 2}};
+                                {4, 2, 2}, {2, 2, 1}, {2, 1, 1}, {2, 1, 1}};
     bx = B[c->n][0]; by = B[c->n][1]; bz = B[c->n][2];
   } else {
     static const int B[9][2] = {{0, 0}, {0, 0}, {16, 16}, {16, 8}, {16, 8}, {8, 8}, {8, 8}, {8, 8}, {8, 8}};
@@ -356,7 +356,7 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
   }
   // v4 bricks here also for k = 4: its 416-thread CTAs stream the CG vectors of
   // the epilogue faster than the 96-thread register-plane CTAs
-  DG_E(3, 3, 4, 4, 4) DG_E(3, 4, 4, 4, 2) DG_E(3, 5, 4, 2, 2) DG_E(3, 6, 2, 2, 2)
+  DG_E(3, 3, 4, 4, 4) DG_E(3, 4, 4, 4, 2) DG_E(3, 5, 4, 2, 2) DG_E(3, 6, 2, 2, 1)
   DG_E(2, 3, 16, 8, 1) DG_E(2, 4, 16, 8, 1) DG_E(2, 5, 8, 8, 1) DG_E(2, 6, 8, 8, 1)
 #undef DG_E
   return DG_ENOTSUP;
@@ -397,9 +397,11 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
       case 5:
         if (variant == 4) return launch_laplace<3, 5, 4, 2, 2>(c, src, dst, tau_scale, part, st);
         return launch_laplace6<5, 4, 2, 2>(c, src, dst, tau_scale, part, st);
-      case 6: return launch_laplace<3, 6, 2, 2, 2>(c, src, dst, tau_scale, part, st);
-      case 7: return launch_laplace<3, 7, 2, 2, 2>(c, src, dst, tau_scale, part, st);
-      case 8: return launch_laplace<3, 8, 2, 2, 2>(c, src, dst, tau_scale, part, st);
+      // k >= 5: flatter bricks (measured at 64^3: Q5 2x2x1 69 vs 2x2x2 62 GDoF/s,
+      // Q6 2x1x1 62 vs 52, Q7 2x1x1 63 vs 57 at 48^3; profiles/NOTES.md)
+      case 6: return launch_laplace<3, 6, 2, 2, 1>(c, src, dst, tau_scale, part, st);
+      case 7: return launch_laplace<3, 7, 2, 1, 1>(c, src, dst, tau_scale, part, st);
+      case 8: return launch_laplace<3, 8, 2, 1, 1>(c, src, dst, tau_scale, part, st);
     }
   } else {
     switch (c->n) {
