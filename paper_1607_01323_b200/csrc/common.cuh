@@ -52,18 +52,24 @@ struct Geo {
 // 1D reference matrices on [-1,1] for n = k+1 GLL nodes, Gauss rule n_q = n:
 // M = S^T W S, K = D^T W D, endpoint derivative rows.  Passed by value
 // (kernel parameter space -> constant bank operands of DFMA).
-template <int N>
-struct LapTab {
+template <int N, class R = double>
+struct LapTab {  // R: the arithmetic type (double; float for the fp32 V-cycle)
   static constexpr int H = N / 2, NE = (N + 1) / 2;
-  double M[N * N];
-  double K[N * N];
-  double dL[N];
-  double dR[N];
+  R M[N * N];
+  R K[N * N];
+  R dL[N];
+  R dR[N];
   // even-odd (centro-symmetric) splits: A v = merge(Ae e, Ao o) with
   // e_j = v_j + v_{N-1-j}, o_j = v_j - v_{N-1-j} (e_H = v_H for odd N)
-  double Me[NE * NE], Mo[H * H > 0 ? H * H : 1];
-  double Ke[NE * NE], Ko[H * H > 0 ? H * H : 1];
-  double dLe[NE], dLo[H > 0 ? H : 1];
+  R Me[NE * NE], Mo[H * H > 0 ? H * H : 1];
+  R Ke[NE * NE], Ko[H * H > 0 ? H * H : 1];
+  R dLe[NE], dLo[H > 0 ? H : 1];
+};
+
+// non-deduced context for scalar arguments of templated helpers
+template <class X>
+struct Ident {
+  using type = X;
 };
 
 template <int N>

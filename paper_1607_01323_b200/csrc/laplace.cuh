@@ -42,22 +42,24 @@ __host__ __device__ constexpr int row_pitch() {
   return (N % 2 == 0) ? N + 1 : N;  // odd shared-memory row pitch
 }
 
-struct NbrInfo {
+template <class R>
+struct NbrInfoT {
   int kind;           // 0 in-brick, 1 halo, 2 boundary none, 3 boundary neumann
   int cb;             // in-brick cell index
-  double h;           // neighbour size in the face-normal direction
-  double hi;          // its inverse
-  double tau;         // neighbour tau_e
-  const double *src;  // halo: neighbour cell data (global)
+  R h;                // neighbour size in the face-normal direction
+  R hi;               // its inverse
+  R tau;              // neighbour tau_e
+  const R *src;       // halo: neighbour cell data (global)
 };
+using NbrInfo = NbrInfoT<double>;
 
 // Resolve the neighbour of owned cell (ix,iy,iz) across side (D, S).
-template <int D, int S, int DIM, int N, int BX, int BY, int BZ>
-__device__ __forceinline__ NbrInfo resolve_nbr(const Geo &g, const double *u, int ix, int iy,
-                                               int iz, int x0, int y0, int z0, int ex, int ey,
-                                               int ez) {
+template <int D, int S, int DIM, int N, int BX, int BY, int BZ, class R>
+__device__ __forceinline__ NbrInfoT<R> resolve_nbr(const Geo &g, const R *u, int ix, int iy,
+                                                   int iz, int x0, int y0, int z0, int ex,
+                                                   int ey, int ez) {
   constexpr int NP = (DIM == 3) ? N * N * N : N * N;
-  NbrInfo r;
+  NbrInfoT<R> r;
   r.cb = 0;
   r.src = nullptr;
   r.h = 1.0;
@@ -73,7 +75,8 @@ __device__ __forceinline__ NbrInfo resolve_nbr(const Geo &g, const double *u, in
     } else if (m == kGhost) {
       const int t = iy + g.ny * iz;
       r.kind = 1;
-      r.src = g.ghost[S] + (size_t)t * NP;
+      // x-slab ghost layers are fp64 (the fp32 V-cycle runs on whole meshes)
+      r.src = reinterpret_cast<const R *>(g.ghost[S]) + (size_t)t * NP;
       r.h = g.ghost_h[S];
       r.hi = g.ghost_hi[S];
       r.tau = g.ghost_tau[S][t];
@@ -100,7 +103,7 @@ __device__ __forceinline__ NbrInfo resolve_nbr(const Geo &g, const double *u, in
   return r;
 }
 
-template <int DIM, int N, int BX, int BY, int BZ>
+template <int DIM, int N, int BX, int BY, int BZ, class R = double>
 struct LapCfg {
   static constexpr int RP = row_pitch<N>();
   static constexpr int NC = BX * BY * BZ;
@@ -117,17 +120,18 @@ struct LapCfg {
   static constexpr int BUF = NC * CS;
   static constexpr int FBUF = NC * 4 * LPC;      // [cell][v0,g0,v1,g1][LPC]
   static constexpr int SIDEC = 6;                // face coefficients per (cell, side)
-  // shared memory carve-up (doubles, then pointers, then ints)
+  // shared memory carve-up (R values, then pointers, the mbarrier, ints)
   static constexpr int OFF_BUF1 = BUF;
   static constexpr int OFF_FBUF = 2 * BUF;
   static constexpr int OFF_HRAW = OFF_FBUF + FBUF;
   static constexpr int OFF_HBUF = OFF_HRAW + HSIZE;
   static constexpr int OFF_SIDE = OFF_HBUF + HSIZE;          // [cell][side][6]
   static constexpr int OFF_CELL = OFF_SIDE + SIDEC * NC * NSIDE;  // [cell][4]: s_d scaled K
-  static constexpr int OFF_PTR = OFF_CELL + 4 * NC;          // halo sources
-  static constexpr int OFF_BAR = OFF_PTR + NSLOT;            // mbarrier (TMA)
-  static constexpr int NDBL = OFF_BAR + 1;
-  static constexpr size_t SMEM = sizeof(double) * (size_t)NDBL + sizeof(int) * NC * NSIDE;
+  static constexpr int NDAT = OFF_CELL + 4 * NC;             // R values
+  static constexpr size_t PTR_B = ((sizeof(R) * NDAT + 7) / 8) * 8;  // halo sources (bytes)
+  static constexpr size_t BAR_B = PTR_B + 8 * (size_t)NSLOT;         // mbarrier (TMA)
+  static constexpr size_t INT_B = BAR_B + 8;                         // side offsets
+  static constexpr size_t SMEM = INT_B + sizeof(int) * NC * NSIDE;
 };
 
 // ---- TMA bulk copy (cp.async.bulk) + mbarrier helpers -----------------------
@@ -169,8 +173,8 @@ __device__ __forceinline__ int slot_of(int d, int s, int pos) {
 }
 
 // ---- even-odd helpers on register arrays ------------------------------------
-template <int N>
-__device__ __forceinline__ void eo_split(const double *v, double *e, double *o) {
+template <int N, class R>
+__device__ __forceinline__ void eo_split(const R *v, R *e, R *o) {
   constexpr int H = N / 2;
 #pragma unroll
   for (int j = 0; j < H; ++j) {
@@ -180,27 +184,27 @@ __device__ __forceinline__ void eo_split(const double *v, double *e, double *o) 
   if (N & 1) e[H] = v[H];
 }
 // E = sc * Ae e ; O = sc * Ao o  (accumulate = false) or E += ..., O += ...
-template <int N, bool ACC>
-__device__ __forceinline__ void eo_apply(const double *Ae, const double *Ao, const double *e,
-                                         const double *o, double sc, double *E, double *O) {
+template <int N, bool ACC, class R>
+__device__ __forceinline__ void eo_apply(const R *Ae, const R *Ao, const R *e, const R *o,
+                                         typename Ident<R>::type sc, R *E, R *O) {
   constexpr int H = N / 2, NE = (N + 1) / 2;
 #pragma unroll
   for (int i = 0; i < NE; ++i) {
-    double a = 0.0;
+    R a = 0.0;
 #pragma unroll
     for (int j = 0; j < NE; ++j) a += Ae[i * NE + j] * e[j];
     E[i] = ACC ? E[i] + sc * a : sc * a;
   }
 #pragma unroll
   for (int i = 0; i < H; ++i) {
-    double a = 0.0;
+    R a = 0.0;
 #pragma unroll
     for (int j = 0; j < H; ++j) a += Ao[i * H + j] * o[j];
     O[i] = ACC ? O[i] + sc * a : sc * a;
   }
 }
-template <int N>
-__device__ __forceinline__ void eo_merge(const double *E, const double *O, double *y) {
+template <int N, class R>
+__device__ __forceinline__ void eo_merge(const R *E, const R *O, R *y) {
   constexpr int H = N / 2;
 #pragma unroll
   for (int i = 0; i < H; ++i) {
@@ -219,28 +223,38 @@ __device__ __forceinline__ void eo_merge(const double *E, const double *O, doubl
 //              (w = integrals of the basis functions, the dual zero-mean
 //              weights) for pAp of the projected operator
 enum LapEpi : int { kEpiStore = 0, kEpiCheb = 1, kEpiDot = 2 };
-struct EpiArgs {
-  double *rc;
-  const double *diag;
-  double *x;
-  double *dnew;
+template <class R>
+struct EpiArgsT {
+  R *rc;
+  const R *diag;
+  R *x;
+  R *dnew;
   double a, b;
   double *partials;      // [brick][4]
   double wint[kMaxN];    // integrals of the 1D basis functions on [-1,1]
 };
+using EpiArgs = EpiArgsT<double>;
 
-template <int EPI, int DIM, int N>
-__device__ __forceinline__ void epi_store(const double *__restrict__ u, double *__restrict__ out,
-                                          const EpiArgs &ea, size_t gi, double y, double wq,
+template <int EPI, int DIM, int N, class R>
+__device__ __forceinline__ void epi_store(const R *__restrict__ u, R *__restrict__ out,
+                                          const EpiArgsT<R> &ea, size_t gi, R y, double wq,
                                           double *acc) {
   if (EPI == kEpiStore) {
     out[gi] = y;
   } else if (EPI == kEpiCheb) {
-    const double r = __dsub_rn(ea.rc[gi], y);
-    const double dn = __dadd_rn(__dmul_rn(ea.a, u[gi]), __dmul_rn(ea.b, __ddiv_rn(r, ea.diag[gi])));
-    ea.rc[gi] = r;
-    ea.dnew[gi] = dn;
-    ea.x[gi] = __dadd_rn(ea.x[gi], dn);
+    if constexpr (std::is_same<R, double>::value) {
+      const double r = __dsub_rn(ea.rc[gi], y);
+      const double dn = __dadd_rn(__dmul_rn(ea.a, u[gi]), __dmul_rn(ea.b, __ddiv_rn(r, ea.diag[gi])));
+      ea.rc[gi] = r;
+      ea.dnew[gi] = dn;
+      ea.x[gi] = __dadd_rn(ea.x[gi], dn);
+    } else {
+      const R r = ea.rc[gi] - y;
+      const R dn = (R)ea.a * u[gi] + (R)ea.b * (r / ea.diag[gi]);
+      ea.rc[gi] = r;
+      ea.dnew[gi] = dn;
+      ea.x[gi] = ea.x[gi] + dn;
+    }
   } else {
     out[gi] = y;
     const double p = u[gi];
@@ -251,7 +265,8 @@ __device__ __forceinline__ void epi_store(const double *__restrict__ u, double *
 }
 
 // deterministic CTA reduction of acc[0..2] -> ea.partials[blk*4 + k]
-__device__ __forceinline__ void epi_reduce(double *acc, double *red, const EpiArgs &ea, int blk) {
+template <class EA>
+__device__ __forceinline__ void epi_reduce(double *acc, double *red, const EA &ea, int blk) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     double v = acc[k];
@@ -272,24 +287,26 @@ __device__ __forceinline__ void epi_reduce(double *acc, double *red, const EpiAr
 }
 
 // part: 0 all cells, 1 skip bricks touching a ghost side, 2 only those
-template <int DIM, int N, int BX, int BY, int BZ, int EPI = kEpiStore>
-__global__ void __launch_bounds__(LapCfg<DIM, N, BX, BY, BZ>::THREADS, (N >= 7 ? 1 : 2))
-laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g,
-                     const LapTab<N> T, const double tau_scale, const int part,
-                     const EpiArgs ea = EpiArgs{}) {
-  using C = LapCfg<DIM, N, BX, BY, BZ>;
+template <int DIM, int N, int BX, int BY, int BZ, int EPI = kEpiStore, class R = double>
+__global__ void __launch_bounds__(LapCfg<DIM, N, BX, BY, BZ, R>::THREADS, (N >= 7 ? 1 : 2))
+laplace_vmult_kernel(const R *__restrict__ u, R *__restrict__ out, const Geo g,
+                     const LapTab<N, R> T, const double tau_scale, const int part,
+                     const EpiArgsT<R> ea = EpiArgsT<R>{}) {
+  static_assert(EPI != kEpiDot || std::is_same<R, double>::value, "fused dot epilogue: fp64 only");
+  using C = LapCfg<DIM, N, BX, BY, BZ, R>;
   constexpr int RP = C::RP, LPC = C::LPC, CS = C::CS, NP = C::NP, NSIDE = C::NSIDE;
   constexpr int H = N / 2, NE = (N + 1) / 2;
-  extern __shared__ double smem[];
-  double *buf0 = smem;
-  double *buf1 = smem + C::OFF_BUF1;
-  double *fbuf = smem + C::OFF_FBUF;
-  double *hraw = smem + C::OFF_HRAW;
-  double *hbuf = smem + C::OFF_HBUF;
-  double *sside = smem + C::OFF_SIDE;
-  double *scell = smem + C::OFF_CELL;
-  const double **hsrc = reinterpret_cast<const double **>(smem + C::OFF_PTR);
-  int *soff = reinterpret_cast<int *>(smem + C::NDBL);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R *smem = reinterpret_cast<R *>(smem_raw);
+  R *buf0 = smem;
+  R *buf1 = smem + C::OFF_BUF1;
+  R *fbuf = smem + C::OFF_FBUF;
+  R *hraw = smem + C::OFF_HRAW;
+  R *hbuf = smem + C::OFF_HBUF;
+  R *sside = smem + C::OFF_SIDE;
+  R *scell = smem + C::OFF_CELL;
+  const R **hsrc = reinterpret_cast<const R **>(smem_raw + C::PTR_B);
+  int *soff = reinterpret_cast<int *>(smem_raw + C::INT_B);
 
   const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z + g.bz0;
   const int x0 = bx * BX, y0 = by * BY, z0 = bz * BZ;
@@ -306,12 +323,12 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
     const int c = it / NSIDE, side = it % NSIDE;
     const int d = side >> 1, s = side & 1;
     const int jx = c % BX, jy = (c / BX) % BY, jz = c / (BX * BY);
-    double a_vo = 0.0, a_go = 0.0, a_vn = 0.0, a_gn = 0.0, b_vo = 0.0, b_vn = 0.0;
+    R a_vo = 0.0, a_go = 0.0, a_vn = 0.0, a_gn = 0.0, b_vo = 0.0, b_vn = 0.0;
     int off = C::OFF_FBUF + (c * 4 + (s ? 2 : 0)) * LPC;  // own data (any valid)
-    const double *hsrc_cell = nullptr;
+    const R *hsrc_cell = nullptr;
     if (jx < ex && jy < ey && jz < ez) {
       const int ix = x0 + jx, iy = y0 + jy, iz = z0 + jz;
-      NbrInfo nb;
+      NbrInfoT<R> nb;
 #define DG_RES(DD, SS) \
   resolve_nbr<DD, SS, DIM, N, BX, BY, BZ>(g, u, ix, iy, iz, x0, y0, z0, ex, ey, ez)
       switch (side) {
@@ -323,17 +340,17 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
         default: nb = DG_RES(2, 1); break;
       }
 #undef DG_RES
-      const double taue = g.tau[(size_t)ix + (size_t)g.nx * (iy + (size_t)g.ny * iz)];
-      const double h0 = g.hx[ix], h1 = g.hy[iy], h2 = (DIM == 3) ? g.hz[iz] : 2.0;
-      const double hd = d == 0 ? h0 : (d == 1 ? h1 : h2);
-      double sfac;  // s_d = prod of the other half sizes
+      const R taue = g.tau[(size_t)ix + (size_t)g.nx * (iy + (size_t)g.ny * iz)];
+      const R h0 = g.hx[ix], h1 = g.hy[iy], h2 = (DIM == 3) ? g.hz[iz] : 2.0;
+      const R hd = d == 0 ? h0 : (d == 1 ? h1 : h2);
+      R sfac;  // s_d = prod of the other half sizes
       if (DIM == 3) sfac = d == 0 ? 0.25 * h1 * h2 : (d == 1 ? 0.25 * h0 * h2 : 0.25 * h0 * h1);
       else sfac = d == 0 ? 0.5 * h1 : 0.5 * h0;
-      const double hi = 1.0 / hd;
-      const double sg = s ? -1.0 : 1.0;  // sign of the own outward normal flips go terms
+      const R hi = 1.0 / hd;
+      const R sg = s ? -1.0 : 1.0;  // sign of the own outward normal flips go terms
       if (nb.kind <= 1) {                // interior face (operators.py:217-225)
-        const double hni = 1.0 / nb.h;
-        const double tau = tau_scale * fmax(taue, nb.tau);
+        const R hni = 1.0 / nb.h;
+        const R tau = tau_scale * fmax(taue, nb.tau);
         a_vo = tau; a_go = sg * hi; a_vn = -tau; a_gn = sg * hni;
         b_vo = sg * hi; b_vn = -sg * hi;
         if (nb.kind == 0) {
@@ -345,13 +362,13 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
           hsrc_cell = nb.src;
         }
       } else if (nb.kind == kBndNeumann) {  // pressure-Dirichlet face (operators.py:227-233)
-        const double tau = tau_scale * taue;
+        const R tau = tau_scale * taue;
         a_vo = 2.0 * tau; a_go = 2.0 * sg * hi;
         b_vo = 2.0 * sg * hi;
       }
       a_vo *= sfac; a_go *= sfac; a_vn *= sfac; a_gn *= sfac; b_vo *= sfac; b_vn *= sfac;
     }
-    double *sc = sside + C::SIDEC * it;
+    R *sc = sside + C::SIDEC * it;
     sc[0] = a_vo; sc[1] = a_go; sc[2] = a_vn; sc[3] = a_gn; sc[4] = b_vo; sc[5] = b_vn;
     soff[it] = off;
     {  // every halo slot is written exactly once, by its brick-edge cell
@@ -365,13 +382,13 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   }
   for (int cc = tid; cc < C::NC; cc += blockDim.x) {
     const int jx = cc % BX, jy = (cc / BX) % BY, jz = cc / (BX * BY);
-    double h0 = 1.0, h1 = 1.0, h2 = 2.0;
+    R h0 = 1.0, h1 = 1.0, h2 = 2.0;
     if (jx < ex && jy < ey && jz < ez) {
       h0 = g.hx[x0 + jx];
       h1 = g.hy[y0 + jy];
       if (DIM == 3) h2 = g.hz[z0 + jz];
     }
-    double *ct = scell + 4 * cc;  // (2/h_d) s_d: scale of K along d
+    R *ct = scell + 4 * cc;  // (2/h_d) s_d: scale of K along d
     if (DIM == 3) {
       ct[0] = 0.5 * h1 * h2 / h0;
       ct[1] = 0.5 * h0 * h2 / h1;
@@ -384,9 +401,9 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   }
   // ---- own cells -> buf0: rows of x-adjacent cells are contiguous in both
   // global and (odd N, unpadded) shared memory -> one TMA bulk copy per row
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::BAR_B);
   constexpr int ROW = BX * NP;
-  const bool tma = (RP == N) && !(ex & 1) && !(g.nx & 1) &&
+  const bool tma = std::is_same<R, double>::value && (RP == N) && !(ex & 1) && !(g.nx & 1) &&
                    ((reinterpret_cast<uintptr_t>(u) & 15) == 0);
   if (tma) {
     if (tid == 0) {
@@ -394,12 +411,12 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
       int rows = 0;
       for (int r = 0; r < BY * BZ; ++r)
         if (r % BY < ey && r / BY < ez) ++rows;
-      mbar_expect_tx(bar, (uint32_t)(rows * ex * NP * sizeof(double)));
+      mbar_expect_tx(bar, (uint32_t)(rows * ex * NP * sizeof(R)));
       for (int r = 0; r < BY * BZ; ++r) {
         const int jy = r % BY, jz = r / BY;
         if (jy >= ey || jz >= ez) continue;
         const size_t e0 = (size_t)x0 + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz));
-        bulk_g2s(buf0 + r * ROW, u + e0 * NP, (uint32_t)(ex * NP * sizeof(double)), bar);
+        bulk_g2s(buf0 + r * ROW, u + e0 * NP, (uint32_t)(ex * NP * sizeof(R)), bar);
       }
     }
   } else {
@@ -407,7 +424,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
       const int r = i / ROW, w = i - r * ROW;
       const int jx = w / NP, o = w - jx * NP;
       const int jy = r % BY, jz = r / BY;
-      double v = 0.0;
+      R v = 0.0;
       if (jx < ex && jy < ey && jz < ez)
         v = u[((size_t)x0 + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz))) * NP + w];
       int so;
@@ -428,7 +445,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   if (!(g.exp_flags & 1)) {  // exp_flags bit 0: skip halo (timing experiments only)
     constexpr int NIT = C::NSLOT * LPC;
     constexpr int ROUNDS = (NIT + C::THREADS - 1) / C::THREADS;
-    double x[ROUNDS][N];
+    R x[ROUNDS][N];
     int item[ROUNDS], sd[ROUNDS];
 #pragma unroll
     for (int k = 0; k < ROUNDS; ++k) {
@@ -437,7 +454,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
       sd[k] = 0;
       if (i < NIT) {
         const int slot = i / LPC, p = i - slot * LPC;
-        const double *src = hsrc[slot];
+        const R *src = hsrc[slot];
         if (src != nullptr) {
           int d, s;
           if (slot < C::SLOT1) { d = 0; s = slot >= C::NS0; }
@@ -459,7 +476,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
     for (int k = 0; k < ROUNDS; ++k) {
       if (item[k] < 0) continue;
       const int slot = item[k] / LPC, p = item[k] - slot * LPC;
-      double v, gsum = 0.0;
+      R v, gsum = 0.0;
       if (sd[k]) {  // neighbour on our hi side faces us with its LEFT end
         v = x[k][0];
 #pragma unroll
@@ -484,14 +501,14 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   const bool active = has_line && jx < ex && jy < ey && jz < ez;
   const size_t e = (size_t)(x0 + jx) + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz));
   const int ta = (DIM == 3) ? t / N : 0, tb = (DIM == 3) ? t - ta * N : t;
-  double v[N], ev[NE], ov[H > 0 ? H : 1], E[NE], O[H > 0 ? H : 1];
-  double v0 = 0.0, v1 = 0.0, g0 = 0.0, g1 = 0.0;
+  R v[N], ev[NE], ov[H > 0 ? H : 1], E[NE], O[H > 0 ? H : 1];
+  R v0 = 0.0, v1 = 0.0, g0 = 0.0, g1 = 0.0;
   double eacc[3] = {0.0, 0.0, 0.0};  // kEpiDot partial sums
 
   // own face functionals of line v (even/odd split ev/ov): values and
   // reference derivatives at both ends -> fbuf
   auto functionals = [&]() {
-    double ge = 0.0, go = 0.0;
+    R ge = 0.0, go = 0.0;
 #pragma unroll
     for (int j = 0; j < NE; ++j) ge += T.dLe[j] * ev[j];
 #pragma unroll
@@ -511,17 +528,17 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
     constexpr int d = decltype(dconst)::value;
     if (g.exp_flags & 2) return;  // timing experiment: no face terms
     const int s0 = c * NSIDE + 2 * d, s1 = s0 + 1;
-    const double *c0 = sside + C::SIDEC * s0, *c1 = sside + C::SIDEC * s1;
-    const double vn0 = smem[soff[s0] + t], gn0 = smem[soff[s0] + LPC + t];
-    const double vn1 = smem[soff[s1] + t], gn1 = smem[soff[s1] + LPC + t];
-    const double cv0 = c0[0] * v0 + c0[1] * g0 + c0[2] * vn0 + c0[3] * gn0;
-    const double cd0 = c0[4] * v0 + c0[5] * vn0;
-    const double cv1 = c1[0] * v1 + c1[1] * g1 + c1[2] * vn1 + c1[3] * gn1;
-    const double cd1 = c1[4] * v1 + c1[5] * vn1;
+    const R *c0 = sside + C::SIDEC * s0, *c1 = sside + C::SIDEC * s1;
+    const R vn0 = smem[soff[s0] + t], gn0 = smem[soff[s0] + LPC + t];
+    const R vn1 = smem[soff[s1] + t], gn1 = smem[soff[s1] + LPC + t];
+    const R cv0 = c0[0] * v0 + c0[1] * g0 + c0[2] * vn0 + c0[3] * gn0;
+    const R cd0 = c0[4] * v0 + c0[5] * vn0;
+    const R cv1 = c1[0] * v1 + c1[1] * g1 + c1[2] * vn1 + c1[3] * gn1;
+    const R cd1 = c1[4] * v1 + c1[5] * vn1;
     // value rows e_0 / e_{N-1}; derivative rows dL, dR = -reverse(dL)
     E[0] += 0.5 * (cv0 + cv1);
     if (H > 0) O[0] += 0.5 * (cv0 - cv1);
-    const double dm = cd0 - cd1, dp = cd0 + cd1;
+    const R dm = cd0 - cd1, dp = cd0 + cd1;
 #pragma unroll
     for (int i = 0; i < NE; ++i) E[i] += T.dLe[i] * dm;
 #pragma unroll
@@ -543,12 +560,12 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
     for (int i = tid; i < (C::NSLOT - C::SLOT1) * 2 * ROWS; i += blockDim.x) {
       const int sw = i / ROWS, a = i - sw * ROWS;  // sw = (slot - SLOT1)*2 + which
       const int off = (C::SLOT1 * 2 + sw) * LPC + a * N;
-      double x[N];
+      R x[N];
 #pragma unroll
       for (int q = 0; q < N; ++q) x[q] = hraw[off + q];
 #pragma unroll
       for (int i2 = 0; i2 < N; ++i2) {
-        double acc = 0.0;
+        R acc = 0.0;
 #pragma unroll
         for (int q = 0; q < N; ++q) acc += T.M[i2 * N + q] * x[q];
         hbuf[off + i2] = acc;
@@ -556,7 +573,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
     }
   }
   if (active) {
-    double y[N];
+    R y[N];
     eo_apply<N, false>(T.Me, T.Mo, ev, ov, 1.0, E, O);
     eo_merge<N>(E, O, y);
 #pragma unroll
@@ -572,13 +589,13 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   if (DIM == 3 && !(g.exp_flags & 4)) {
     for (int i = tid; i < 2 * C::NS2 * 2 * N; i += blockDim.x) {
       const int sw = i / N, xcol = i - sw * N;  // sw = (slot - SLOT2)*2 + which
-      double *col = hbuf + (C::SLOT2 * 2 + sw) * LPC + xcol;
-      double x[N];
+      R *col = hbuf + (C::SLOT2 * 2 + sw) * LPC + xcol;
+      R x[N];
 #pragma unroll
       for (int q = 0; q < N; ++q) x[q] = col[q * N];
 #pragma unroll
       for (int i2 = 0; i2 < N; ++i2) {
-        double acc = 0.0;
+        R acc = 0.0;
 #pragma unroll
         for (int q = 0; q < N; ++q) acc += T.M[i2 * N + q] * x[q];
         col[i2 * N] = acc;
@@ -595,7 +612,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   }
   __syncthreads();  // #4
   if (active) {
-    double y[N], te[NE], to[H > 0 ? H : 1];
+    R y[N], te[NE], to[H > 0 ? H : 1];
 #pragma unroll
     for (int q = 0; q < N; ++q) y[q] = buf1[ybase + q * RP];
     eo_split<N>(y, te, to);
@@ -620,7 +637,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
     }
   }
   if (DIM == 2) {
-    if (EPI == kEpiDot) epi_reduce(eacc, fbuf, ea, bx + gridDim.x * (by + gridDim.y * bz));
+    if (EPI == kEpiDot) epi_reduce(eacc, reinterpret_cast<double *>(fbuf), ea, bx + gridDim.x * (by + gridDim.y * bz));
     return;
   }
   __syncthreads();  // #5
@@ -645,7 +662,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
   }
   __syncthreads();  // #6
   if (active) {
-    double y[N], ge[NE], go[H > 0 ? H : 1];
+    R y[N], ge[NE], go[H > 0 ? H : 1];
 #pragma unroll
     for (int q = 0; q < N; ++q) y[q] = buf1[zbase + q * N * RP];
     eo_split<N>(y, ge, go);
@@ -661,7 +678,7 @@ laplace_vmult_kernel(const double *__restrict__ u, double *__restrict__ out, con
       epi_store<EPI, DIM, N>(u, out, ea, e * NP + (i * N + ta) * N + tb, y[i], wxy * ea.wint[i],
                              eacc);
   }
-  if (EPI == kEpiDot) epi_reduce(eacc, fbuf, ea, bx + gridDim.x * (by + gridDim.y * bz));
+  if (EPI == kEpiDot) epi_reduce(eacc, reinterpret_cast<double *>(fbuf), ea, bx + gridDim.x * (by + gridDim.y * bz));
 }
 
 }  // namespace dg
