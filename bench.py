@@ -364,6 +364,18 @@ def run_cg(dist_on):
                         "solve_ms": 1e3 * dtm,
                         "rel_diff_vs_chebyshev": float((xm.reshape(-1) - x.reshape(-1)).norm()
                                                        / x.reshape(-1).norm())}
+    # the paper's single-precision V-cycle inside the fp64 CG
+    mg32 = MG.MultigridHierarchy(spaces, spec, project=sol.zero_mean_project, precision="fp32")
+    MG.laplace_pcg_mg(mg32, bb, project_dual=True, rel_tol=1e-10, max_iter=3)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    x32, st32 = MG.laplace_pcg_mg(mg32, bb, project_dual=True, rel_tol=1e-10, max_iter=200)
+    torch.cuda.synchronize()
+    dt32 = time.perf_counter() - t0
+    out["multigrid_fp32"] = {"iterations": st32.iterations, "converged": st32.converged,
+                             "solve_ms": 1e3 * dt32,
+                             "rel_diff_vs_fp64_mg": float((x32 - xm.reshape(-1)).norm()
+                                                          / xm.reshape(-1).norm())}
     return out
 
 

@@ -257,6 +257,12 @@ int dg_mg_create(dg_ctx *const *levels, int n_levels, const double *const *diag,
                  dg_mg **out);
 int dg_mg_destroy(dg_mg *mg);
 /* MultigridHierarchy.vcycle (multigrid.py:133-151): x = V(b), finest level */
+/* Run the V-cycle in single precision (bits = 32; the paper's multigrid is
+ * fp32) or back in fp64 (bits = 64, the default and the
+ * reference's arithmetic).  fp32: the same algorithm on float level vectors,
+ * diagonals and dense coarse operator; input / output stay fp64, so the
+ * outer CG (dg_laplace_pcg_mg) is unchanged.  3D hierarchies. */
+int dg_mg_set_precision(dg_mg *mg, int bits);
 int dg_mg_vcycle(dg_mg *mg, const double *b, double *x, void *stream);
 /* dg_laplace_pcg with the V-cycle as preconditioner (prm->cheb_* unused);
  * ctx must be the hierarchy's finest level */

@@ -155,6 +155,7 @@ PROTOTYPES = {
     "dg_mg_restrict": [_P, _P, _P, _P, _P],
     "dg_mg_create": [_P, _I, _P, _P, _I, _D, _I, _D, _D, ctypes.POINTER(_P)],
     "dg_mg_destroy": [_P],
+    "dg_mg_set_precision": [_P, _I],
     "dg_g2_create": [ctypes.POINTER(G2Desc), ctypes.POINTER(_P)],
     "dg_g2_destroy": [_P],
     "dg_g2_apply": [_P, _I, _D, _P, _P, _P, _I, _P],

@@ -326,6 +326,59 @@ static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_
   return DG_OK;
 }
 
+// ---- fp32 Laplace (the fp32 V-cycle): the same v4 kernel
+// instantiated in single precision, 1D tables rounded once from the fp64 ones
+template <int N>
+static LapTab<N, float> lap_tab_f(const Basis1D &b) {
+  const LapTab<N> d = lap_tab<N>(b);
+  LapTab<N, float> t;
+  const double *src = reinterpret_cast<const double *>(&d);
+  float *dst = reinterpret_cast<float *>(&t);
+  static_assert(sizeof(LapTab<N>) == 2 * sizeof(LapTab<N, float>), "table layouts");
+  for (size_t i = 0; i < sizeof(LapTab<N>) / sizeof(double); ++i) dst[i] = (float)src[i];
+  return t;
+}
+
+template <int DIM, int N, int BX, int BY, int BZ, int EPI>
+static int launch_laplace_f(dg_ctx *c, const float *src, float *dst, double tau_scale,
+                            cudaStream_t st, const EpiArgsT<float> &ea) {
+  using C = LapCfg<DIM, N, BX, BY, BZ, float>;
+  auto kern = laplace_vmult_kernel<DIM, N, BX, BY, BZ, EPI, float>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  Geo g = c->geo();
+  g.bz0 = 0;
+  const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, (g.nz + BZ - 1) / BZ);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab_f<N>(c->basis), tau_scale, 0, ea);
+  DG_LAUNCH_CHECK("laplace_vmult_kernel<float>");
+  return DG_OK;
+}
+
+// out = L src (epi = kEpiStore) or the fused Chebyshev step (kEpiCheb), fp32,
+// 3D whole-mesh contexts
+static int laplace_dispatch_f(dg_ctx *c, const float *src, float *dst, double tau_scale, int epi,
+                              const EpiArgsT<float> &ea, cudaStream_t st) {
+  if (c->dim != 3 || c->mode[0] == kGhost || c->mode[1] == kGhost)
+    return inval("fp32 Laplace: 3D whole-mesh contexts");
+#define DG_F(NN, X, Y, Z)                                                                   \
+  case NN:                                                                                  \
+    return epi == kEpiCheb                                                                  \
+               ? launch_laplace_f<3, NN, X, Y, Z, kEpiCheb>(c, src, dst, tau_scale, st, ea) \
+               : launch_laplace_f<3, NN, X, Y, Z, kEpiStore>(c, src, dst, tau_scale, st, ea);
+  // fp32 halves the shared memory per cell: larger bricks than fp64 at
+  // k = 3, 4 (measured on the config-4 / config-2 V-cycles: 4x4x4 1.24 vs
+  // 4x4x2 1.31 ms; 8x2x2 1.70 vs 4x2x2 1.85 ms)
+  switch (c->n) {
+    DG_F(2, 8, 4, 4) DG_F(3, 4, 4, 4) DG_F(4, 4, 4, 4) DG_F(5, 8, 2, 2) DG_F(6, 2, 2, 1)
+    DG_F(7, 2, 1, 1) DG_F(8, 2, 1, 1)
+  }
+#undef DG_F
+  return inval("unsupported degree");
+}
+
 // number of CTAs (bricks) of the default Laplace configuration: the size of
 // the kEpiDot partial-sum array
 static int64_t laplace_bricks(const dg_ctx *c) {

@@ -113,7 +113,8 @@ class MultigridHierarchy:
     def __init__(self, spaces, bc_spec, tau_scale: float = 1.0, degree: int = 5,
                  smoothing_range: float = 20.0, coarse_tol: float = 1e-3, est_iters: int = 20,
                  safety: float = 1.1, seed: int = 987, project: Optional[Callable] = None,
-                 dense_coarse_limit: int = 4096, seed_draw: Callable = reference_seed_draw):
+                 dense_coarse_limit: int = 4096, seed_draw: Callable = reference_seed_draw,
+                 precision: str = "fp64"):
         if len(spaces) < 1:
             raise ValueError("hierarchy needs at least one level")
         if degree < 0:
@@ -157,6 +158,13 @@ class MultigridHierarchy:
                   int(degree), float(smoothing_range), int(c0.coarse_iters),
                   float(c0.coarse_range), float(tau_scale), ctypes.byref(h))
         self._h = h
+        if precision not in ("fp64", "fp32"):
+            raise ValueError("precision must be 'fp64' or 'fp32'")
+        self.precision = precision
+        if precision == "fp32":
+            # the paper's single-precision V-cycle; the outer
+            # CG stays fp64
+            _lib.call("dg_mg_set_precision", h, 32)
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -54,6 +54,7 @@ class StepConfig:
     rel_tol_proj: float = 1e-12
     max_iter: int = 1000
     body_force: Optional[Callable] = None
+    mg_precision: str = "fp64"   # "fp32": the paper's single-precision V-cycle
 
 
 @dataclass
@@ -83,7 +84,8 @@ class VelocityCorrection:
         self.tau_scale = (cfg.variant.dt_ref / cfg.dt) if cfg.variant.variant == "V1" else 1.0
         self.g0, self.alpha, self.beta = bdf_ex_constants(cfg.J)
         proj = None if self.outflow else sol.zero_mean_project
-        self.mg = MG.MultigridHierarchy(mg_spaces, bc_spec, tau_scale=self.tau_scale, project=proj)
+        self.mg = MG.MultigridHierarchy(mg_spaces, bc_spec, tau_scale=self.tau_scale, project=proj,
+                                        precision=cfg.mg_precision)
 
     def _pressure(self, rhs, p0):
         cfg, sp, bcs = self.cfg, self.space, self.bcs

@@ -123,3 +123,37 @@ def test_3d_vcycle_vs_oracle(k):
     assert np.linalg.norm(lhs - rhs) <= 1e-12 * max(np.linalg.norm(rhs), 1.0)
     x, st = MG.laplace_pcg_mg(mg, dev(b), rel_tol=1e-8, max_iter=40)
     assert st.converged and st.iterations <= 15
+
+
+@pytest.mark.parametrize("k,singular", [(2, True), (3, False), (4, True), (5, False)])
+def test_fp32_vcycle(k, singular):
+    """The fp32 V-cycle (dg_mg_set_precision): one cycle
+    agrees with the fp64 cycle to single-precision accuracy, and the fp64
+    MG-PCG it preconditions reaches the same solution (rel_tol 1e-10) in at
+    most two more iterations."""
+    meshes = MG.box_mesh_hierarchy(((0, 1), (0, 2), (0, 1)), (2, 2, 2), 2, grading=(0.0, 1.2, 0.0),
+                                   periodic=(True, False, True))
+    spaces = [DgSpace(m, k) for m in meshes]
+    spec = ops.BoundarySpec({"ymin": ops.DirichletBC(None),
+                             "ymax": ops.DirichletBC(None) if singular else ops.NeumannBC(None, None)})
+    proj = sol.zero_mean_project if singular else None
+    mg64 = MG.MultigridHierarchy(spaces, spec, project=proj)
+    mg32 = MG.MultigridHierarchy(spaces, spec, project=proj, precision="fp32")
+    top = spaces[-1]
+    g = torch.Generator(device="cuda").manual_seed(k)
+    b = torch.rand(top.n_dofs, dtype=torch.float64, device="cuda", generator=g) - 0.5
+    if singular:
+        b = sol.zero_mean_project_dual(top, b)
+    v64, v32 = mg64.vcycle(b), mg32.vcycle(b)
+    assert relerr(v32.cpu().numpy(), v64.cpu().numpy()) < 1e-4
+    x64, s64 = MG.laplace_pcg_mg(mg64, b, project_dual=singular, rel_tol=1e-10)
+    x32, s32 = MG.laplace_pcg_mg(mg32, b, project_dual=singular, rel_tol=1e-10)
+    assert s64.converged and s32.converged
+    assert s32.iterations <= s64.iterations + 2
+    if singular:
+        x64, x32 = sol.zero_mean_project(top, x64), sol.zero_mean_project(top, x32)
+    assert relerr(x32.cpu().numpy(), x64.cpu().numpy()) < 1e-8
+    mg32_back = MG.MultigridHierarchy(spaces, spec, project=proj, precision="fp32")
+    from paper_1607_01323_b200 import _lib
+    _lib.call("dg_mg_set_precision", mg32_back.handle, 64)
+    assert torch.equal(mg32_back.vcycle(b), v64)
