@@ -135,6 +135,13 @@ def chebyshev_smooth(op: Callable, diag, cfg: ChebyshevConfig, rhs, x=None,
     return x
 
 
+def chebyshev_error_factor(kappa: float, n: int) -> float:
+    """Classic Chebyshev error bound 2 q^n, q = (sqrt(kappa)-1)/(sqrt(kappa)+1)
+    (solvers.py:132-135); host arithmetic, the bound behind the coarse count."""
+    q = (np.sqrt(kappa) - 1.0) / (np.sqrt(kappa) + 1.0)
+    return float(2.0 * q ** n)
+
+
 def eigen_estimate_via_cg(op: Callable, prec_diag, b, n_iter: int = 20):
     """Lanczos estimates from CG coefficients (solvers.py:138-176)."""
     b = _to_dev(b)

@@ -179,3 +179,10 @@ def test_field_vector_roundtrip():
     assert np.array_equal(flat.reshape(2, 5, 3, 3), fv.data.transpose(0, 2, 1, 3))
     back = FieldVector.from_element_major(flat, space, 2)
     assert np.array_equal(back.data, fv.data) and not back.has_nan()
+
+
+def test_chebyshev_error_factor():
+    """solvers.py:132-135: 2 q^n with q = (sqrt(k)-1)/(sqrt(k)+1)."""
+    from paper_1607_01323_b200.solvers import chebyshev_error_factor
+    assert abs(chebyshev_error_factor(9.0, 3) - 2.0 * 0.5 ** 3) < 1e-15
+    assert chebyshev_error_factor(1.0, 5) == 0.0
