@@ -18,13 +18,27 @@ struct dg_g2 {
 
 namespace {
 
-int g2_launch(dg_g2 *g, const G2Params &prm, const double *src, double *dst, cudaStream_t st) {
-  constexpr int CPB = 2;
+template <int N, int NQ>
+int g2_launch_nq(dg_g2 *g, const G2Params &prm, const double *src, double *dst, cudaStream_t st) {
+  using C = G2Cfg<N, NQ>;
   if (g->geo.ncells == 0) return DG_OK;
-  const unsigned grid = (unsigned)((g->geo.ncells + CPB - 1) / CPB);
-  g2_kernel<CPB><<<grid, 64 * CPB, 0, st>>>(src, dst, g->geo, g->tab, prm);
+  const unsigned grid = (unsigned)((g->geo.ncells + C::CPB - 1) / C::CPB);
+  g2_kernel<N, NQ><<<grid, C::THREADS, 0, st>>>(src, dst, g->geo, g->tab, prm);
   DG_LAUNCH_CHECK("g2_kernel");
   return DG_OK;
+}
+
+// (n, n_q) pairs: the linear rule n_q = n and the convective over-integration
+// rule n_q = floor(3k/2) + 1 (basis.py:103-105)
+int g2_launch(dg_g2 *g, const G2Params &prm, const double *src, double *dst, cudaStream_t st) {
+  const int n = g->geo.n, nq = g->geo.nq;
+#define DG_G(NN, QQ) \
+  if (n == NN && nq == QQ) return g2_launch_nq<NN, QQ>(g, prm, src, dst, st);
+  DG_G(2, 2) DG_G(3, 3) DG_G(4, 4) DG_G(5, 5) DG_G(6, 6) DG_G(7, 7) DG_G(8, 8)
+  DG_G(3, 4) DG_G(4, 5) DG_G(5, 7) DG_G(6, 8) DG_G(7, 10) DG_G(8, 11)
+#undef DG_G
+  return inval("general 2D: unsupported (n, n_q) = (" + std::to_string(n) + ", " +
+               std::to_string(nq) + ")");
 }
 
 }  // namespace

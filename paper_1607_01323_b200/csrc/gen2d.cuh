@@ -144,18 +144,29 @@ __device__ __forceinline__ void g2_lf(double a0, double a1, double b0, double b1
   F1 = 0.5 * (a1 * unm + b1 * unp) + 0.5 * lam * (a1 - b1);
 }
 
-template <int CPB>
-__global__ void __launch_bounds__(64 * CPB)
+// threads per cell: one per quadrature point (at least one per node and per
+// face point), several cells per CTA; shared arrays sized for (N, NQ)
+template <int N, int NQ>
+struct G2Cfg {
+  static constexpr int NP = N * N, QP = NQ * NQ;
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
+  static constexpr int TPC = mx(mx(QP, NP), 4 * NQ);
+  static constexpr int CPB = TPC >= 128 ? 1 : 128 / TPC;
+  static constexpr int THREADS = CPB * TPC;
+};
+
+template <int N, int NQ>
+__global__ void __launch_bounds__(G2Cfg<N, NQ>::THREADS)
 g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo g,
           const __grid_constant__ G2Tab T, const __grid_constant__ G2Params prm) {
-  constexpr int TPC = 64, QS = kG2MaxQ * kG2MaxQ;
-  const int N = g.n, NQ = g.nq, NP = N * N, QP = NQ * NQ;
+  using C = G2Cfg<N, NQ>;
+  constexpr int TPC = C::TPC, CPB = C::CPB, NP = C::NP, QP = C::QP;
   const int op = prm.op;
   const int nci = g2_nci(op), nco = g2_nco(op);
   const int64_t nc = g.ncells;
-  __shared__ double su[CPB][3][kG2MaxN * kG2MaxN];
-  __shared__ double sq[CPB][2][3][QS];          // [comp][value | ref-x | ref-y test]
-  __shared__ double sf[CPB][4][2][3][kG2MaxQ];  // [slot][comp][value | ref-x | ref-y]
+  __shared__ double su[CPB][3][NP];
+  __shared__ double sq[CPB][2][3][QP];         // [comp][value | ref-x | ref-y test]
+  __shared__ double sf[CPB][4][2][3][NQ];      // [slot][comp][value | ref-x | ref-y]
   const int cs = threadIdx.x / TPC, t = threadIdx.x % TPC;
   const int64_t e = (int64_t)blockIdx.x * CPB + cs;
   const bool valid = e < nc;
@@ -166,8 +177,8 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
                      (op == kG2Projection && prm.tau_c != nullptr) || op == kG2Convective ||
                      ((op == kG2Divergence || op == kG2Gradient) && prm.form != 0);
 
-  for (int i = t; i < 2 * 3 * QS; i += TPC) (&sq[cs][0][0][0])[i] = 0.0;
-  for (int i = t; i < 4 * 2 * 3 * kG2MaxQ; i += TPC) (&sf[cs][0][0][0][0])[i] = 0.0;
+  for (int i = t; i < 2 * 3 * QP; i += TPC) (&sq[cs][0][0][0])[i] = 0.0;
+  for (int i = t; i < 4 * 2 * 3 * NQ; i += TPC) (&sf[cs][0][0][0][0])[i] = 0.0;
 
   for (int lev = 0; lev < nlev; ++lev) {
     const bool hist = op == kG2Convective || op == kG2PressureNeumann;
