@@ -358,6 +358,7 @@ g2_kernel(const double *__restrict__ src, double *__restrict__ dst, const G2Geo 
         int64_t en = -1;
         if (kind == 0 && !bdata) {
           en = g.nbr[e * 4 + s];
+          if (en < 0) continue;  // kinds must mark boundary slots; never read outside
           if (op != kG2LaplaceLocal) {
             const int sn = g.nslot[e * 4 + s];
             const int qn = g.nflip[e * 4 + s] ? NQ - 1 - q : q;

@@ -405,11 +405,20 @@ def _params(space, op, bcs):
 
 
 def _all_interior_kinds(space):
-    key = ("__interior__",)
+    """Kinds from the connectivity alone: 0 on interior (incl. periodic)
+    slots, velocity-Dirichlet on boundary slots (operators whose face terms
+    are interior-only: projection; and the face-free vorticity)."""
+    key = ("__structural__",)
     if key not in space._kinds:
-        space._kinds[key] = _torch().zeros((space.n_elements, 4), dtype=_torch().int32,
-                                           device="cuda")
+        nbr = space._d["nbr"]
+        space._kinds[key] = torch_where_kinds(nbr)
     return space._kinds[key]
+
+
+def torch_where_kinds(nbr):
+    torch = _torch()
+    return torch.where(nbr >= 0, torch.zeros_like(nbr), torch.full_like(nbr, _lib.BC_VELOCITY_DIRICHLET)
+                       ).to(torch.int32).contiguous()
 
 
 def apply_viscous_helmholtz(space: GeneralSpace2D, u, gamma0_dt: float, nu: float,

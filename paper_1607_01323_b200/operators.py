@@ -102,6 +102,42 @@ def ctypes_ptr(v):
     return ctypes.c_void_p(int(v))
 
 
+def _route_2d(space):
+    """2D Cartesian spaces run the vector operators on their general-geometry
+    view (gen2d kernels, several small cells per CTA); DG_2D_GENERIC=1 keeps
+    the per-cell quadrature-point kernel (A/B timing)."""
+    import os
+    return (space.dim == 2 and not getattr(space, "is_general", False)
+            and os.environ.get("DG_2D_GENERIC", "0") == "0")
+
+
+def _to_dev_em(space, x, ncomp):
+    """(CUDA element-major tensor, numpy shape or None) with the Cartesian
+    space's own layout rules."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        return x, None
+    a = np.asarray(x, dtype=np.float64)
+    return torch.as_tensor(space.to_element_major(a, ncomp).ravel()).to("cuda"), a.shape
+
+
+def _from_dev_em(space, out, ncomp, shape):
+    if shape is None:
+        return out
+    return space.from_element_major(out.cpu().numpy(), ncomp, shape)
+
+
+def _view_bcs(space, bcs):
+    """(general view, its resolved BCs) of a 2D Cartesian space and BC set."""
+    view = space.general_view()
+    key = ("view", tuple(id(bc) for _, bc in bcs.dirichlet + bcs.neumann))
+    cache = space.__dict__.setdefault("_view_bcs", {})
+    if key not in cache:
+        spec = BoundarySpec({t: bc for t, bc in bcs.dirichlet + bcs.neumann})
+        cache[key] = (spec, spec.resolve(view))
+    return view, cache[key][1]
+
+
 class _Arg:
     """Input adapter: device tensor view + a function giving the result back
     in the caller's type/layout."""
@@ -233,6 +269,12 @@ def apply_viscous_helmholtz(space: DgSpace, u, gamma0_dt: float, nu: float,
     if getattr(space, "is_general", False):
         from . import general
         return general.apply_viscous_helmholtz(space, u, gamma0_dt, nu, bcs)
+    if _route_2d(space):
+        from . import general
+        view, vb = _view_bcs(space, bcs)
+        t, shape = _to_dev_em(space, u, 2)
+        return _from_dev_em(space, general.apply_viscous_helmholtz(view, t, gamma0_dt, nu, vb),
+                            2, shape)
     a = _Arg(space, u, space.dim)
     out = a.new_out()
     ctx = space.ctx(bcs.kinds)
@@ -254,6 +296,27 @@ def face_penalty_layout(space, tau_c_f):
     return out
 
 
+def _cart_tau_c_slots(space, tau_c_f):
+    """Cartesian tau_C (reference face order, or the device layout [d*ne+e])
+    -> the general view's [e][4] layout."""
+    torch = _torch()
+    if tau_c_f is None or not isinstance(tau_c_f, torch.Tensor):
+        return tau_c_f  # reference face order = the view's interior order
+    em, sm, ep, sp = space.interior_faces()
+    key = "_tcs_index"
+    if getattr(space, key, None) is None:
+        ne = space.mesh.n_elements
+        src = torch.as_tensor((sm // 2) * ne + em).to("cuda")
+        setattr(space, key, (src, torch.as_tensor(em * 4 + sm).to("cuda"),
+                             torch.as_tensor(ep * 4 + sp).to("cuda")))
+    src, a, b = getattr(space, key)
+    out = torch.zeros(space.mesh.n_elements * 4, dtype=torch.float64, device="cuda")
+    vals = tau_c_f.reshape(-1)[src]
+    out[a] = vals
+    out[b] = vals
+    return out.view(space.mesh.n_elements, 4)
+
+
 def apply_projection_operator(space: DgSpace, w, tau_d_e, tau_c_f):
     """M + tau_D div-div + tau_C interior jump penalty (operators.py:372-412).
 
@@ -263,6 +326,12 @@ def apply_projection_operator(space: DgSpace, w, tau_d_e, tau_c_f):
     if getattr(space, "is_general", False):
         from . import general
         return general.apply_projection_operator(space, w, tau_d_e, tau_c_f)
+    if _route_2d(space):
+        from . import general
+        t, shape = _to_dev_em(space, w, 2)
+        out = general.apply_projection_operator(space.general_view(), t, tau_d_e,
+                                                _cart_tau_c_slots(space, tau_c_f))
+        return _from_dev_em(space, out, 2, shape)
     torch = _torch()
     a = _Arg(space, w, space.dim)
     out = a.new_out()
@@ -299,6 +368,15 @@ def eval_convective_rhs(space: DgSpace, bcs: ResolvedBCs, history, betas, times,
     if getattr(space, "is_general", False):
         from . import general
         return general.eval_convective_rhs(space, bcs, history, betas, times, t_np1, body_force)
+    # convective: the general kernel wins at k <= 3 (n_q <= 5), the per-cell
+    # kernel above that (profiles/NOTES.md)
+    if _route_2d(space) and space.k <= 3 and space.n_q_over == (3 * space.k) // 2 + 1:
+        from . import general
+        view, vb = _view_bcs(space, bcs)
+        conv = [_to_dev_em(space, u, 2) for u in history]
+        out = general.eval_convective_rhs(view, vb, [t for t, _ in conv], betas, times, t_np1,
+                                          body_force)
+        return _from_dev_em(space, out, 2, conv[0][1])
     import ctypes
     if len(times) < len(history) or len(betas) < len(history):
         raise ValueError("need one beta and one time per history level")

@@ -152,6 +152,40 @@ class DgSpace:
             out.append(np.broadcast_to(c.reshape(shape), self.field_shape()))
         return np.stack(out)
 
+    def general_view(self):
+        """The same 2D box as a general-geometry space (bilinear mapping,
+        the box's own face lists and cell order): the general 2D kernels
+        (csrc/gen2d.cuh) then run the vector operators, which they do faster
+        than the per-cell quadrature-point kernel on small 2D cells."""
+        if self.dim != 2:
+            raise ValueError("general view: 2D spaces")
+        if getattr(self, "_gview", None) is None:
+            from types import SimpleNamespace
+            from .general import GeneralSpace2D
+            nx, ny = self.mesh.counts
+            vx, vy = self.mesh.axis_vertices
+            e = np.arange(self.mesh.n_elements)
+            ix, iy = e % nx, e // nx
+            geom = np.empty((2, 2, e.size, 2))
+            geom[0] = np.stack([vx[ix], vx[ix + 1]], axis=1)[None, :, :]
+            geom[1] = np.stack([vy[iy], vy[iy + 1]], axis=1).T[:, :, None]
+            em, sm, ep, sp = self.interior_faces()
+            names = list(TAG_NAMES[:4])
+            bel, bsl, btg = [], [], []
+            for side, sel in enumerate((ix == 0, ix == nx - 1, iy == 0, iy == ny - 1)):
+                if self.mesh.periodic[side // 2]:
+                    continue
+                bel.append(e[sel]); bsl.append(np.full(int(sel.sum()), side))
+                btg.append(np.full(int(sel.sum()), side))
+            cat = lambda a: np.concatenate(a) if a else np.zeros(0, np.int64)
+            view = SimpleNamespace(
+                geom_degree=1, geom_nodes=geom, n_elements=e.size, tag_names=names,
+                interior=SimpleNamespace(em=em, sm=sm, ep=ep, sp=sp, flip=np.zeros(em.size, bool)),
+                boundary=SimpleNamespace(elem=cat(bel), slot=cat(bsl), tag=cat(btg)),
+                parent=None, quadrant=None)
+            self._gview = GeneralSpace2D(view, self.k)
+        return self._gview
+
     def node_coords_reference(self):
         """Node coordinates in the reference layout: (2, m, ne, m) in 2D
         (spaces.py:86-105); element-major (3, ne, z, y, x) in 3D."""

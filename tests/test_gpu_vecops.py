@@ -151,3 +151,26 @@ def test_config3_full_size_properties():
     r1 = ops.eval_convective_rhs(gsp, gbcs, [u], (1.0,), (0.0,), 0.0)
     r2 = ops.eval_convective_rhs(gsp, gbcs, [u, u], (1.5, 0.5), (0.0, 0.0), 0.0)
     assert ((r2 - 2.0 * r1).norm() / r1.norm()).item() < 1e-13
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 5])
+def test_2d_view_routing_matches_per_cell_kernel(k, monkeypatch):
+    """2D Cartesian Helmholtz / projection / convective run on the general
+    view (gen2d kernels); the per-cell quadrature-point kernel
+    (DG_2D_GENERIC=1) gives the same results to rounding."""
+    mesh = M.build_box_mesh(((0, 2), (-1, 1)), (5, 4), grading=(0.0, 1.3), periodic=(True, False))
+    space = DgSpace(mesh, k)
+    bcs = ops.BoundarySpec({"ymin": ops.DirichletBC(None), "ymax": ops.NeumannBC(None, None)}).resolve(space)
+    g = torch.Generator(device="cuda").manual_seed(k)
+    u = torch.rand(2 * space.n_dofs, dtype=torch.float64, device="cuda", generator=g) - 0.5
+    ne = mesh.n_elements
+    td = torch.rand(ne, dtype=torch.float64, device="cuda", generator=g)
+    tc = torch.rand(2 * ne, dtype=torch.float64, device="cuda", generator=g)
+    calls = (lambda: ops.apply_viscous_helmholtz(space, u, 3.0, 0.2, bcs),
+             lambda: ops.apply_projection_operator(space, u, td, tc),
+             lambda: ops.eval_convective_rhs(space, bcs, [u], (1.0,), (0.0,), 0.0))
+    routed = [f().cpu().numpy() for f in calls]
+    monkeypatch.setenv("DG_2D_GENERIC", "1")
+    generic = [f().cpu().numpy() for f in calls]
+    for a, b in zip(routed, generic):
+        assert relerr(a, b) < 1e-12
