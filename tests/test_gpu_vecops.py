@@ -69,6 +69,9 @@ CASES = [
      {"xmin": "D", "xmax": "N", "ymin": "D", "ymax": "D", "zmin": "N", "zmax": "D"}, None),
     (((0, 2), (-1, 1), (0, 1)), (3, 4, 2), (True, False, True),
      {"ymin": "D", "ymax": "D"}, (0.0, 1.8, 0.0)),
+    # one cell across a periodic axis: every x side is its own neighbour
+    (((0, 1), (0, 1), (0, 2)), (1, 3, 2), (True, False, True),
+     {"ymin": "D", "ymax": "N"}, (0.0, 0.6, 0.0)),
 ]
 
 
