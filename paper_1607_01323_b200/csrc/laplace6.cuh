@@ -42,7 +42,10 @@ struct Lap6Cfg {
   static constexpr int NSLOT = 2 * (NS0 + NS1 + NS2);
   static constexpr int HSIZE = NSLOT * 2 * LPC;           // [slot][v|g][LPC]
   static constexpr int BUF = NC * CS;
-  static constexpr int FBUF = NC * 4 * LPC;                // [cell][v0,g0,v1,g1][LPC]
+  // [cell][v0,g0,v1,g1][LPC], cell stride odd: the threads of a half-warp
+  // (16 cells, same slab index) hit distinct banks
+  static constexpr int FSTR = 4 * LPC + 1;
+  static constexpr int FBUF = NC * FSTR;
   // x/z functionals live in buf0 and y functionals in buf1 whenever they fit
   // (N >= 4; two extra barriers), else in their own regions
   static constexpr bool FX_IN_BUF0 = FBUF <= BUF;
@@ -150,7 +153,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
         B = sg * sfac * hid;
         Dn = sg * sfac * nb.hi;
         if (nb.kind == 0) {
-          off = (d == 1 ? C::OFF_FBY : C::OFF_FBX) + (nb.cb * 4 + (s ? 0 : 2)) * LPC;
+          off = (d == 1 ? C::OFF_FBY : C::OFF_FBX) + nb.cb * C::FSTR + (s ? 0 : 2) * LPC;
         } else {
           const int pos = d == 0 ? jy + BY * jz : (d == 1 ? jx + BX * jz : jx + BX * jy);
           off = C::OFF_HRAW + slot_of<C>(d, s, pos) * 2 * LPC;
@@ -237,8 +240,11 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
 
   // ---- per-thread coordinates ---------------------------------------------
   const bool has = tid < C::NT;
-  const int c = has ? tid / N : 0;
-  const int s = tid - c * N;  // z-slab in the XY phase, y index in the Z phase
+  // slab-major thread order: consecutive threads are different cells with the
+  // same slab index, so the plane loads / stores (cell stride CS = N^3, odd
+  // for odd N) and the functional buffers (odd stride) are bank-conflict free
+  const int c = has ? tid % C::NC : 0;
+  const int s = has ? tid / C::NC : 0;  // z-slab in the XY phase, y index in the Z phase
   // 1D coefficients in registers (indices are compile-time constants)
   double cMe[NE * NE], cMo[HO * HO], cKe[NE * NE], cKo[HO * HO], cLe[NE], cLo[HO];
 #pragma unroll
@@ -270,7 +276,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   };
   // publish the end functionals of the N lines get(l, q) (line l, position q)
   auto publish = [&](double *fb, int t0, auto get) {
-    double *p = fb + c * 4 * LPC + t0;
+    double *p = fb + c * C::FSTR + t0;
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       double v[N], e[NE], o[HO], g0, g1;
