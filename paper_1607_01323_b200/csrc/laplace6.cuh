@@ -55,9 +55,11 @@ struct Lap6Cfg {
   static constexpr int OFF_FBY = FY_IN_BUF1 ? OFF_BUF1 : 2 * BUF + (FX_IN_BUF0 ? 0 : FBUF);
   static constexpr int OFF_HRAW = 2 * BUF + (FX_IN_BUF0 ? 0 : FBUF) + (FY_IN_BUF1 ? 0 : FBUF);
   static constexpr int OFF_ZERO = OFF_HRAW + HSIZE;        // 2*LPC zeros (boundary neighbours)
+  // per-cell tables with odd cell strides (a half-warp reads 16 cells' entries)
+  static constexpr int SSTR = 4 * 6 + 1, CSTR = 5;
   static constexpr int OFF_SIDE = OFF_ZERO + 2 * LPC;      // [cell][side][4]: A, B, Dn, -
-  static constexpr int OFF_CELL = OFF_SIDE + 4 * 6 * NC;   // [cell][4]: s_d Kh scale, |cell|/8
-  static constexpr int OFF_PTR = OFF_CELL + 4 * NC;        // halo sources
+  static constexpr int OFF_CELL = OFF_SIDE + SSTR * NC;    // [cell][4]: s_d Kh scale, |cell|/8
+  static constexpr int OFF_PTR = OFF_CELL + CSTR * NC;     // halo sources
   static constexpr int OFF_BAR = OFF_PTR + NSLOT;
   static constexpr int NDBL = OFF_BAR + 1;
   static constexpr size_t SMEM = sizeof(double) * (size_t)NDBL + sizeof(int) * NC * 6;
@@ -164,7 +166,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
         B = 2.0 * sg * sfac * hid;
       }
     }
-    double *sc = sside + 4 * it;
+    double *sc = sside + C::SSTR * c + 4 * side;
     sc[0] = A;
     sc[1] = B;
     sc[2] = Dn;
@@ -187,7 +189,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       i1 = g.hyi[y0 + jy];
       i2 = g.hzi[z0 + jz];
     }
-    double *ct = scell + 4 * cc;  // (2/h_d) s_d: scale of K along d; cell |J|
+    double *ct = scell + C::CSTR * cc;  // (2/h_d) s_d: scale of K along d; cell |J|
     ct[0] = 0.5 * h1 * h2 * i0;
     ct[1] = 0.5 * h0 * h2 * i1;
     ct[2] = 0.5 * h0 * h1 * i2;
@@ -296,7 +298,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     int o0, o1;
   };
   auto side2 = [&](int side0, int t0) {
-    const double *c0 = sside + 4 * (c * 6 + side0);
+    const double *c0 = sside + C::SSTR * c + 4 * side0;
     Side2 r;
     r.A0 = c0[0]; r.B0 = c0[1]; r.D0 = c0[2];
     r.A1 = c0[4]; r.B1 = c0[5]; r.D1 = c0[6];
@@ -352,7 +354,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   // ---- XY-b: x-sweeps (rows): T = s_x Kh_x u + Lx, P = M_x u ----------------
   if (has) {
     const Side2 sd = side2(0, s * N);
-    const double kx = scell[4 * c + 0];
+    const double kx = scell[C::CSTR * c + 0];
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       double e[NE], o[HO], E[NE], O[HO], g0, g1;
@@ -387,7 +389,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   // ---- XY-c: y-sweeps (columns): G = M_y T + s_y Kh_y P + Ly, Q = M_y P ------
   if (has) {
     const Side2 sd = side2(2, s * N);
-    const double ky = scell[4 * c + 1];
+    const double ky = scell[C::CSTR * c + 1];
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       double v[N], w[N], e[NE], o[HO], te[NE], to[HO], E[NE], O[HO], g0, g1;
@@ -440,7 +442,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   // ---- Z-b: out = M_z G + s_z Kh_z Q + Lz -> buf1 (y = s plane) ------------
   if (has) {
     const Side2 sd = side2(4, s * N);
-    const double kz = scell[4 * c + 2];
+    const double kz = scell[C::CSTR * c + 2];
     double *op = buf1 + c * CS + s * N;
 #pragma unroll
     for (int l = 0; l < N; ++l) {
@@ -497,7 +499,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       double wq = 0.0;
       if (EPI == kEpiDot) {
         const int yy = yx / N, xx = yx - yy * N;
-        wq = scell[4 * cb + 3] * ea.wint[xx] * ea.wint[yy] * ea.wint[z];
+        wq = scell[C::CSTR * cb + 3] * ea.wint[xx] * ea.wint[yy] * ea.wint[z];
       }
       epi_store<EPI, 3, N>(u, out, ea, g0 + w, buf1[si], wq, eacc);
     }
