@@ -47,7 +47,12 @@ struct Geo {
   double ghost_hi[2];
   int exp_flags;             // timing experiments (DG_EXP env); 0 in production
   int bz0;                   // first brick z index of a chunked (z-range) launch, else 0
+  const double *ctab;        // per-cell SIP face coefficients + scales (kCellTab each) or null
 };
+
+// doubles per cell of the Laplace cell table (laplace6.cuh): 6 sides x (A /
+// tau_scale, B, Dn), 3 s_d Kh scales, |cell|/8, one pad (odd stride)
+constexpr int kCellTab = 23;
 
 // 1D reference matrices on [-1,1] for n = k+1 GLL nodes, Gauss rule n_q = n:
 // M = S^T W S, K = D^T W D, endpoint derivative rows.  Passed by value

@@ -42,6 +42,7 @@ struct dg_ctx {
   int64_t partials_n = 0;
   double *d_hin = nullptr, *d_hout = nullptr;   // device staging of dg_laplace_vmult_host
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  double *d_ctab = nullptr;  // Laplace cell table (laplace6.cuh), built on first use
   double *d_trc = nullptr;  // face traces of the Cartesian vector operators (vcart.cu)
   int64_t trc_n = 0;
   std::vector<double *> vwork;  // vector-PCG work vectors (vwork_n doubles each)
@@ -75,6 +76,7 @@ struct dg_ctx {
     }();
     g.exp_flags = exp_flags;
     g.bz0 = 0;
+    g.ctab = d_ctab;
     return g;
   }
 };

@@ -235,6 +235,7 @@ int dg_ctx_destroy(dg_ctx *c) {
   for (double *w : c->work) cudaFree(w);
   cudaFree(c->d_partials);
   cudaFree(c->d_trc);
+  cudaFree(c->d_ctab);
   for (double *w : c->vwork) cudaFree(w);
   cudaFree(c->d_vpart);
   delete c;
@@ -318,6 +319,15 @@ static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_
   if (!attr) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
+  }
+  if (!c->d_ctab) {  // per-cell face coefficients, once per context
+    double *tab = nullptr;
+    DG_CUDA_CHECK(cudaMalloc(&tab, sizeof(double) * kCellTab * (size_t)c->n_cells));
+    const Geo g0 = c->geo();
+    const int64_t items = 7 * c->n_cells;
+    lap6_cell_table_kernel<N><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(g0, tab);
+    DG_LAUNCH_CHECK("lap6_cell_table_kernel");
+    c->d_ctab = tab;
   }
   Geo g = c->geo();
   const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, chunk_bricks_z(c, BZ, g));
@@ -424,6 +434,15 @@ static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau
   if (!attr) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
+  }
+  if (!c->d_ctab) {  // per-cell face coefficients, once per context
+    double *tab = nullptr;
+    DG_CUDA_CHECK(cudaMalloc(&tab, sizeof(double) * kCellTab * (size_t)c->n_cells));
+    const Geo g0 = c->geo();
+    const int64_t items = 7 * c->n_cells;
+    lap6_cell_table_kernel<N><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(g0, tab);
+    DG_LAUNCH_CHECK("lap6_cell_table_kernel");
+    c->d_ctab = tab;
   }
   Geo g = c->geo();
   const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, chunk_bricks_z(c, BZ, g));

@@ -56,14 +56,110 @@ struct Lap6Cfg {
   static constexpr int OFF_HRAW = 2 * BUF + (FX_IN_BUF0 ? 0 : FBUF) + (FY_IN_BUF1 ? 0 : FBUF);
   static constexpr int OFF_ZERO = OFF_HRAW + HSIZE;        // 2*LPC zeros (boundary neighbours)
   // per-cell tables with odd cell strides (a half-warp reads 16 cells' entries)
-  static constexpr int SSTR = 4 * 6 + 1, CSTR = 5;
-  static constexpr int OFF_SIDE = OFF_ZERO + 2 * LPC;      // [cell][side][4]: A, B, Dn, -
-  static constexpr int OFF_CELL = OFF_SIDE + SSTR * NC;    // [cell][4]: s_d Kh scale, |cell|/8
-  static constexpr int OFF_PTR = OFF_CELL + CSTR * NC;     // halo sources
+  // the context's cell table, brick rows as stored in global memory:
+  // [cell][kCellTab] = side coefficients [side][A/tau_scale, B, Dn], then
+  // s_d Kh scales (x, y, z), |cell|/8, pad (odd stride: conflict-free)
+  static constexpr int SSTR = kCellTab;
+  static constexpr int OFF_SIDE = OFF_ZERO + 2 * LPC;
+  static constexpr int OFF_PTR = OFF_SIDE + SSTR * NC;     // halo sources
   static constexpr int OFF_BAR = OFF_PTR + NSLOT;
   static constexpr int NDBL = OFF_BAR + 1;
   static constexpr size_t SMEM = sizeof(double) * (size_t)NDBL + sizeof(int) * NC * 6;
 };
+
+// Global source of halo slot `slot` (neighbour cell across the brick surface)
+// or nullptr when that neighbour is a boundary, lies in the brick (periodic
+// wrap onto the brick itself) or the slot is outside a partial brick.  Pure
+// index arithmetic, the same resolution as resolve_nbr.
+template <class C, int N, int BX, int BY, int BZ>
+__device__ __forceinline__ const double *halo_slot_src(const Geo &g, const double *u, int slot,
+                                                       int x0, int y0, int z0, int ex, int ey,
+                                                       int ez, int &d, int &s) {
+  constexpr int NP = N * N * N;
+  int loc;
+  if (slot < C::SLOT1) { d = 0; loc = slot; }
+  else if (slot < C::SLOT2) { d = 1; loc = slot - C::SLOT1; }
+  else { d = 2; loc = slot - C::SLOT2; }
+  const int ns = d == 0 ? C::NS0 : (d == 1 ? C::NS1 : C::NS2);
+  s = loc >= ns;
+  const int pos = loc - s * ns;
+  int ix, iy, iz;
+  if (d == 0) { iy = pos % BY; iz = pos / BY; if (iy >= ey || iz >= ez) return nullptr; ix = s ? ex - 1 : 0; }
+  else if (d == 1) { ix = pos % BX; iz = pos / BX; if (ix >= ex || iz >= ez) return nullptr; iy = s ? ey - 1 : 0; }
+  else { ix = pos % BX; iy = pos / BX; if (ix >= ex || iy >= ey) return nullptr; iz = s ? ez - 1 : 0; }
+  ix += x0; iy += y0; iz += z0;
+  const int nd = d == 0 ? g.nx : (d == 1 ? g.ny : g.nz);
+  const int lo = d == 0 ? x0 : (d == 1 ? y0 : z0);
+  const int ext = d == 0 ? ex : (d == 1 ? ey : ez);
+  int nc = (d == 0 ? ix : (d == 1 ? iy : iz)) + (s ? 1 : -1);
+  if (nc < 0 || nc >= nd) {
+    const int m = g.mode[2 * d + s];
+    if (m == kGhost) return g.ghost[s] + (size_t)(iy + g.ny * iz) * NP;
+    if (m != kWrap) return nullptr;
+    nc = s ? 0 : nd - 1;
+  }
+  if (nc >= lo && nc < lo + ext) return nullptr;
+  const int cx = d == 0 ? nc : ix, cy = d == 1 ? nc : iy, cz = d == 2 ? nc : iz;
+  return u + ((size_t)cx + (size_t)g.nx * (cy + (size_t)g.ny * cz)) * NP;
+}
+
+// The context's cell table (once per context, one thread per (cell, side) and
+// one per cell for the scales): the face coupling of every (cell, side) as
+// three coefficients, A without tau_scale,
+//   interior (operators.py:217-225): A = max(tau_e, tau_n) s, B = sg s/h, Dn = sg s/h_n
+//   velocity-Neumann (:227-233):    A = 2 tau_e s,         B = 2 sg s/h, Dn = 0
+//   velocity-Dirichlet (:189-193):  0
+// with s the tangential face scale, then the per-cell stiffness scales and
+// |cell|/8.  The vmult copies a brick's rows with its cells (TMA), so its
+// prologue does index arithmetic only.
+template <int N>
+__global__ void lap6_cell_table_kernel(const Geo g, double *tab) {
+  const int64_t ncell = (int64_t)g.nx * g.ny * g.nz;
+  const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (it >= ncell * 7) return;
+  const int64_t e = it / 7;
+  const int side = (int)(it - 7 * e);
+  const int ix = (int)(e % g.nx), iy = (int)((e / g.nx) % g.ny), iz = (int)(e / ((int64_t)g.nx * g.ny));
+  double *row = tab + e * kCellTab;
+  const double h0 = g.hx[ix], h1 = g.hy[iy], h2 = g.hz[iz];
+  if (side == 6) {
+    row[18] = 0.5 * h1 * h2 * g.hxi[ix];
+    row[19] = 0.5 * h0 * h2 * g.hyi[iy];
+    row[20] = 0.5 * h0 * h1 * g.hzi[iz];
+    row[21] = 0.125 * h0 * h1 * h2;
+    row[22] = 0.0;
+    return;
+  }
+  const int d = side >> 1, s = side & 1;
+  const double *dummy = tab;  // resolve_nbr forms (never dereferenced) source pointers
+  NbrInfo nb;
+#define DG_RES(DD, SS) resolve_nbr<DD, SS, 3, N, 1, 1, 1>(g, dummy, ix, iy, iz, 0, 0, 0, 0, 0, 0)
+  switch (side) {
+    case 0: nb = DG_RES(0, 0); break;
+    case 1: nb = DG_RES(0, 1); break;
+    case 2: nb = DG_RES(1, 0); break;
+    case 3: nb = DG_RES(1, 1); break;
+    case 4: nb = DG_RES(2, 0); break;
+    default: nb = DG_RES(2, 1); break;
+  }
+#undef DG_RES
+  const double taue = g.tau[e];
+  const double hid = d == 0 ? g.hxi[ix] : (d == 1 ? g.hyi[iy] : g.hzi[iz]);
+  const double sfac = d == 0 ? 0.25 * h1 * h2 : (d == 1 ? 0.25 * h0 * h2 : 0.25 * h0 * h1);
+  const double sg = s ? -1.0 : 1.0;
+  double A = 0.0, B = 0.0, Dn = 0.0;
+  if (nb.kind <= 1) {
+    A = fmax(taue, nb.tau) * sfac;
+    B = sg * sfac * hid;
+    Dn = sg * sfac * nb.hi;
+  } else if (nb.kind == kBndNeumann) {
+    A = 2.0 * taue * sfac;
+    B = 2.0 * sg * sfac * hid;
+  }
+  row[3 * side] = A;
+  row[3 * side + 1] = B;
+  row[3 * side + 2] = Dn;
+}
 
 // 4 CTAs per SM need <= 168 registers at 96 threads: one more register drops
 // the occupancy to 3 CTAs and costs ~30 % (measured)
@@ -82,7 +178,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   double *fby = smem + C::OFF_FBY;
   double *hraw = smem + C::OFF_HRAW;
   double *sside = smem + C::OFF_SIDE;
-  double *scell = smem + C::OFF_CELL;
+  double *scell = sside + 18;  // per-cell scales at offset 18 of each table row
   const double **hsrc = reinterpret_cast<const double **>(smem + C::OFF_PTR);
   int *soff = reinterpret_cast<int *>(smem + C::NDBL);
 
@@ -103,15 +199,25 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   if (tma) {
     if (tid == 0) {
       mbar_init(bar, 1);
-      mbar_expect_tx(bar, (uint32_t)(ey * ez * ex * NP * sizeof(double)));
+      mbar_expect_tx(bar, (uint32_t)(ey * ez * ex * (NP + C::SSTR) * sizeof(double)));
       for (int r = 0; r < BY * BZ; ++r) {
         const int jy = r % BY, jz = r / BY;
         if (jy >= ey || jz >= ez) continue;
         const size_t e0 = (size_t)x0 + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz));
         bulk_g2s(buf0 + r * ROW, u + e0 * NP, (uint32_t)(ex * NP * sizeof(double)), bar);
+        bulk_g2s(sside + r * BX * C::SSTR, g.ctab + e0 * C::SSTR,
+                 (uint32_t)(ex * C::SSTR * sizeof(double)), bar);
       }
     }
   } else {
+    for (int i = tid; i < C::NC * C::SSTR; i += blockDim.x) {
+      const int cb = i / C::SSTR, w = i - cb * C::SSTR;
+      const int jx = cb % BX, jy = (cb / BX) % BY, jz = cb / (BX * BY);
+      sside[i] = (jx < ex && jy < ey && jz < ez)
+                     ? g.ctab[((size_t)x0 + jx + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz))) *
+                                  C::SSTR + w]
+                     : 0.0;
+    }
     for (int i = tid; i < C::NC * NP; i += blockDim.x) {
       const int r = i / ROW, w = i - r * ROW;
       const int jx = w / NP, o = w - jx * NP;
@@ -124,76 +230,44 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     }
   }
 
-  // ---- setup: per (cell, side) coefficients and neighbour functional offsets
+  // ---- setup: neighbour functional offsets and halo sources (index math only;
+  // the coefficients arrive with the cells from the context's cell table)
   for (int it = tid; it < C::NC * 6; it += blockDim.x) {
     const int c = it / 6, side = it - 6 * c;
     const int d = side >> 1, s = side & 1;
     const int jx = c % BX, jy = (c / BX) % BY, jz = c / (BX * BY);
-    double A = 0.0, B = 0.0, Dn = 0.0;
+    const int pos = d == 0 ? jy + BY * jz : (d == 1 ? jx + BX * jz : jx + BX * jy);
     int off = C::OFF_ZERO;
-    const double *hs = nullptr;
     if (jx < ex && jy < ey && jz < ez) {
-      const int ix = x0 + jx, iy = y0 + jy, iz = z0 + jz;
-      NbrInfo nb;
-#define DG_RES(DD, SS) resolve_nbr<DD, SS, 3, N, BX, BY, BZ>(g, u, ix, iy, iz, x0, y0, z0, ex, ey, ez)
-      switch (side) {
-        case 0: nb = DG_RES(0, 0); break;
-        case 1: nb = DG_RES(0, 1); break;
-        case 2: nb = DG_RES(1, 0); break;
-        case 3: nb = DG_RES(1, 1); break;
-        case 4: nb = DG_RES(2, 0); break;
-        default: nb = DG_RES(2, 1); break;
+      const int nd = d == 0 ? g.nx : (d == 1 ? g.ny : g.nz);
+      const int lo = d == 0 ? x0 : (d == 1 ? y0 : z0);
+      const int ext = d == 0 ? ex : (d == 1 ? ey : ez);
+      int nc = (d == 0 ? x0 + jx : (d == 1 ? y0 + jy : z0 + jz)) + (s ? 1 : -1);
+      int kind = 1;  // 0 in-brick, 1 halo, 2 boundary
+      bool ghost = false;
+      if (nc < 0 || nc >= nd) {
+        const int m = g.mode[2 * d + s];
+        if (m == kWrap) nc = s ? 0 : nd - 1;
+        else if (m == kGhost) ghost = true;
+        else kind = 2;
       }
-#undef DG_RES
-      const double taue = g.tau[(size_t)ix + (size_t)g.nx * (iy + (size_t)g.ny * iz)];
-      const double h0 = g.hx[ix], h1 = g.hy[iy], h2 = g.hz[iz];
-      const double hid = d == 0 ? g.hxi[ix] : (d == 1 ? g.hyi[iy] : g.hzi[iz]);
-      const double sfac = d == 0 ? 0.25 * h1 * h2 : (d == 1 ? 0.25 * h0 * h2 : 0.25 * h0 * h1);
-      const double sg = s ? -1.0 : 1.0;
-      if (nb.kind <= 1) {
-        A = tau_scale * fmax(taue, nb.tau) * sfac;
-        B = sg * sfac * hid;
-        Dn = sg * sfac * nb.hi;
-        if (nb.kind == 0) {
-          off = (d == 1 ? C::OFF_FBY : C::OFF_FBX) + nb.cb * C::FSTR + (s ? 0 : 2) * LPC;
-        } else {
-          const int pos = d == 0 ? jy + BY * jz : (d == 1 ? jx + BX * jz : jx + BX * jy);
-          off = C::OFF_HRAW + slot_of<C>(d, s, pos) * 2 * LPC;
-          hs = nb.src;
-        }
-      } else if (nb.kind == kBndNeumann) {
-        A = 2.0 * tau_scale * taue * sfac;
-        B = 2.0 * sg * sfac * hid;
+      if (kind == 1 && !ghost && nc >= lo && nc < lo + ext) {
+        const int cb = d == 0 ? (nc - x0) + BX * (jy + BY * jz)
+                              : (d == 1 ? jx + BX * ((nc - y0) + BY * jz)
+                                        : jx + BX * (jy + BY * (nc - z0)));
+        off = (d == 1 ? C::OFF_FBY : C::OFF_FBX) + cb * C::FSTR + (s ? 0 : 2) * LPC;
+      } else if (kind == 1) {
+        off = C::OFF_HRAW + slot_of<C>(d, s, pos) * 2 * LPC;
       }
     }
-    double *sc = sside + C::SSTR * c + 4 * side;
-    sc[0] = A;
-    sc[1] = B;
-    sc[2] = Dn;
     soff[it] = off;
     const bool edge = d == 0 ? jx == (s ? ex - 1 : 0)
                              : (d == 1 ? jy == (s ? ey - 1 : 0) : jz == (s ? ez - 1 : 0));
     if (edge) {
-      const int pos = d == 0 ? jy + BY * jz : (d == 1 ? jx + BX * jz : jx + BX * jy);
-      hsrc[slot_of<C>(d, s, pos)] = hs;
+      const int slot = slot_of<C>(d, s, pos);
+      int dd, ss;
+      hsrc[slot] = halo_slot_src<C, N, BX, BY, BZ>(g, u, slot, x0, y0, z0, ex, ey, ez, dd, ss);
     }
-  }
-  for (int cc = tid; cc < C::NC; cc += blockDim.x) {
-    const int jx = cc % BX, jy = (cc / BX) % BY, jz = cc / (BX * BY);
-    double h0 = 1.0, h1 = 1.0, h2 = 1.0, i0 = 1.0, i1 = 1.0, i2 = 1.0;
-    if (jx < ex && jy < ey && jz < ez) {
-      h0 = g.hx[x0 + jx];
-      h1 = g.hy[y0 + jy];
-      h2 = g.hz[z0 + jz];
-      i0 = g.hxi[x0 + jx];
-      i1 = g.hyi[y0 + jy];
-      i2 = g.hzi[z0 + jz];
-    }
-    double *ct = scell + C::CSTR * cc;  // (2/h_d) s_d: scale of K along d; cell |J|
-    ct[0] = 0.5 * h1 * h2 * i0;
-    ct[1] = 0.5 * h0 * h2 * i1;
-    ct[2] = 0.5 * h0 * h1 * i2;
-    ct[3] = 0.125 * h0 * h1 * h2;
   }
   for (int i = tid; i < 2 * LPC; i += blockDim.x) smem[C::OFF_ZERO + i] = 0.0;
   __syncthreads();  // #1 tables, halo pointers
@@ -298,10 +372,10 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     int o0, o1;
   };
   auto side2 = [&](int side0, int t0) {
-    const double *c0 = sside + C::SSTR * c + 4 * side0;
+    const double *c0 = sside + C::SSTR * c + 3 * side0;
     Side2 r;
-    r.A0 = c0[0]; r.B0 = c0[1]; r.D0 = c0[2];
-    r.A1 = c0[4]; r.B1 = c0[5]; r.D1 = c0[6];
+    r.A0 = tau_scale * c0[0]; r.B0 = c0[1]; r.D0 = c0[2];
+    r.A1 = tau_scale * c0[3]; r.B1 = c0[4]; r.D1 = c0[5];
     r.o0 = soff[c * 6 + side0] + t0;
     r.o1 = soff[c * 6 + side0 + 1] + t0;
     return r;
@@ -354,7 +428,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   // ---- XY-b: x-sweeps (rows): T = s_x Kh_x u + Lx, P = M_x u ----------------
   if (has) {
     const Side2 sd = side2(0, s * N);
-    const double kx = scell[C::CSTR * c + 0];
+    const double kx = scell[C::SSTR * c + 0];
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       double e[NE], o[HO], E[NE], O[HO], g0, g1;
@@ -389,7 +463,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   // ---- XY-c: y-sweeps (columns): G = M_y T + s_y Kh_y P + Ly, Q = M_y P ------
   if (has) {
     const Side2 sd = side2(2, s * N);
-    const double ky = scell[C::CSTR * c + 1];
+    const double ky = scell[C::SSTR * c + 1];
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       double v[N], w[N], e[NE], o[HO], te[NE], to[HO], E[NE], O[HO], g0, g1;
@@ -442,7 +516,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   // ---- Z-b: out = M_z G + s_z Kh_z Q + Lz -> buf1 (y = s plane) ------------
   if (has) {
     const Side2 sd = side2(4, s * N);
-    const double kz = scell[C::CSTR * c + 2];
+    const double kz = scell[C::SSTR * c + 2];
     double *op = buf1 + c * CS + s * N;
 #pragma unroll
     for (int l = 0; l < N; ++l) {
@@ -499,7 +573,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       double wq = 0.0;
       if (EPI == kEpiDot) {
         const int yy = yx / N, xx = yx - yy * N;
-        wq = scell[C::CSTR * cb + 3] * ea.wint[xx] * ea.wint[yy] * ea.wint[z];
+        wq = scell[C::SSTR * cb + 3] * ea.wint[xx] * ea.wint[yy] * ea.wint[z];
       }
       epi_store<EPI, 3, N>(u, out, ea, g0 + w, buf1[si], wq, eacc);
     }
