@@ -11,7 +11,7 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libdgmf.so")
+LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdgmf.so")  # DG_LIB: A/B builds
 CSRC = os.path.join(HERE, "csrc")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
