@@ -300,8 +300,12 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
                                : (d == 1 ? slot >= C::SLOT1 + C::NS1 : slot >= C::SLOT2 + C::NS2);
           const int a = t / N, b = t - a * N;
           // x line (y=b, z=a) | y line (x=b, z=a) | z line (x=b, y=a)
-          const double *l = d == 2 ? src + t : src + a * N * N + (d == 0 ? b * N : b);
-          const int qs = d == 0 ? 1 : (d == 1 ? N : N * N);
+          // read the line from its facing end inwards (y[p], p = 0 at the face):
+          // one derivative row for both sides, dR_q = -dL_{N-1-q}
+          const int qs0 = d == 0 ? 1 : (d == 1 ? N : N * N);
+          const int qs = s ? qs0 : -qs0;
+          const double *l = (d == 2 ? src + t : src + a * N * N + (d == 0 ? b * N : b)) +
+                            (s ? 0 : (N - 1) * qs0);
 #pragma unroll
           for (int q = 0; q < N; ++q) x[k][q] = __ldg(l + q * qs);
           dst[k] = slot * 2 * LPC + t;
@@ -313,9 +317,9 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
         if (dst[k] < 0) continue;
         double gs = 0.0;
 #pragma unroll
-        for (int q = 0; q < N; ++q) gs += (sd[k] ? T.dL[q] : T.dR[q]) * x[k][q];
-        hraw[dst[k]] = sd[k] ? x[k][0] : x[k][N - 1];
-        hraw[dst[k] + LPC] = gs;
+        for (int q = 0; q < N; ++q) gs += T.dL[q] * x[k][q];
+        hraw[dst[k]] = x[k][0];
+        hraw[dst[k] + LPC] = sd[k] ? gs : -gs;
       }
     }
   }
