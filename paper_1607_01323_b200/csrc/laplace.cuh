@@ -318,6 +318,45 @@ laplace_vmult_kernel(const R *__restrict__ u, R *__restrict__ out, const Geo g,
   }
   const int tid = threadIdx.x;
 
+  // ---- own cells -> buf0 (issued first: the copy overlaps the setup) ------
+  // rows of x-adjacent cells are contiguous in both
+  // global and (odd N, unpadded) shared memory -> one TMA bulk copy per row
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::BAR_B);
+  constexpr int ROW = BX * NP;
+  const bool tma = std::is_same<R, double>::value && (RP == N) && !(ex & 1) && !(g.nx & 1) &&
+                   ((reinterpret_cast<uintptr_t>(u) & 15) == 0);
+  if (tma) {
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      int rows = 0;
+      for (int r = 0; r < BY * BZ; ++r)
+        if (r % BY < ey && r / BY < ez) ++rows;
+      mbar_expect_tx(bar, (uint32_t)(rows * ex * NP * sizeof(R)));
+      for (int r = 0; r < BY * BZ; ++r) {
+        const int jy = r % BY, jz = r / BY;
+        if (jy >= ey || jz >= ez) continue;
+        const size_t e0 = (size_t)x0 + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz));
+        bulk_g2s(buf0 + r * ROW, u + e0 * NP, (uint32_t)(ex * NP * sizeof(R)), bar);
+      }
+    }
+  } else {
+    for (int i = tid; i < C::NC * NP; i += blockDim.x) {
+      const int r = i / ROW, w = i - r * ROW;
+      const int jx = w / NP, o = w - jx * NP;
+      const int jy = r % BY, jz = r / BY;
+      R v = 0.0;
+      if (jx < ex && jy < ey && jz < ez)
+        v = u[((size_t)x0 + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz))) * NP + w];
+      int so;
+      if (RP == N) {
+        so = o;
+      } else {
+        const int x = o % N, yz = o / N;
+        so = yz * RP + x;
+      }
+      buf0[(r * BX + jx) * CS + so] = v;
+    }
+  }
   // ---- setup: per (cell, side) face coefficients + neighbour data offset ---
   for (int it = tid; it < C::NC * NSIDE; it += blockDim.x) {
     const int c = it / NSIDE, side = it % NSIDE;
@@ -399,44 +438,6 @@ laplace_vmult_kernel(const R *__restrict__ u, R *__restrict__ out, const Geo g,
       ct[2] = 0.0;
     }
   }
-  // ---- own cells -> buf0: rows of x-adjacent cells are contiguous in both
-  // global and (odd N, unpadded) shared memory -> one TMA bulk copy per row
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + C::BAR_B);
-  constexpr int ROW = BX * NP;
-  const bool tma = std::is_same<R, double>::value && (RP == N) && !(ex & 1) && !(g.nx & 1) &&
-                   ((reinterpret_cast<uintptr_t>(u) & 15) == 0);
-  if (tma) {
-    if (tid == 0) {
-      mbar_init(bar, 1);
-      int rows = 0;
-      for (int r = 0; r < BY * BZ; ++r)
-        if (r % BY < ey && r / BY < ez) ++rows;
-      mbar_expect_tx(bar, (uint32_t)(rows * ex * NP * sizeof(R)));
-      for (int r = 0; r < BY * BZ; ++r) {
-        const int jy = r % BY, jz = r / BY;
-        if (jy >= ey || jz >= ez) continue;
-        const size_t e0 = (size_t)x0 + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz));
-        bulk_g2s(buf0 + r * ROW, u + e0 * NP, (uint32_t)(ex * NP * sizeof(R)), bar);
-      }
-    }
-  } else {
-    for (int i = tid; i < C::NC * NP; i += blockDim.x) {
-      const int r = i / ROW, w = i - r * ROW;
-      const int jx = w / NP, o = w - jx * NP;
-      const int jy = r % BY, jz = r / BY;
-      R v = 0.0;
-      if (jx < ex && jy < ey && jz < ez)
-        v = u[((size_t)x0 + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz))) * NP + w];
-      int so;
-      if (RP == N) {
-        so = o;
-      } else {
-        const int x = o % N, yz = o / N;
-        so = yz * RP + x;
-      }
-      buf0[(r * BX + jx) * CS + so] = v;
-    }
-  }
   __syncthreads();  // #1
 
   // ---- halo: raw face functionals of neighbour cells outside the brick ----
@@ -465,6 +466,9 @@ laplace_vmult_kernel(const R *__restrict__ u, R *__restrict__ out, const Geo g,
           if (d == 0) { base = (a * N + b) * N; stride = 1; }     // (z,y) line along x
           else if (d == 1) { base = a * N * N + b; stride = N; }  // (z,x) line along y
           else { base = a * N + b; stride = N * N; }              // (y,x) line along z
+          // read from the facing end inwards: one derivative row for both
+          // sides (dR_q = -dL_{N-1-q})
+          if (!s) { base += (N - 1) * stride; stride = -stride; }
 #pragma unroll
           for (int q = 0; q < N; ++q) x[k][q] = __ldg(src + base + q * stride);
           item[k] = i;
@@ -477,15 +481,10 @@ laplace_vmult_kernel(const R *__restrict__ u, R *__restrict__ out, const Geo g,
       if (item[k] < 0) continue;
       const int slot = item[k] / LPC, p = item[k] - slot * LPC;
       R v, gsum = 0.0;
-      if (sd[k]) {  // neighbour on our hi side faces us with its LEFT end
-        v = x[k][0];
+      v = x[k][0];  // the facing end (hi side: the neighbour's LEFT end)
 #pragma unroll
-        for (int q = 0; q < N; ++q) gsum += T.dL[q] * x[k][q];
-      } else {
-        v = x[k][N - 1];
-#pragma unroll
-        for (int q = 0; q < N; ++q) gsum += T.dR[q] * x[k][q];
-      }
+      for (int q = 0; q < N; ++q) gsum += T.dL[q] * x[k][q];
+      if (!sd[k]) gsum = -gsum;
       hraw[(slot * 2 + 0) * LPC + p] = v;
       hraw[(slot * 2 + 1) * LPC + p] = gsum;
     }
