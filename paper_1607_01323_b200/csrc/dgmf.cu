@@ -88,6 +88,8 @@ int dg_basis_tables(int k, int n_q, double *S, double *D, double *nodes, double 
   return DG_OK;
 }
 
+static int ensure_cell_table(dg_ctx *c, cudaStream_t st);
+
 int dg_ctx_create(const dg_mesh_desc *desc, dg_ctx **out) {
   if (!desc || !out) return inval("null argument");
   *out = nullptr;
@@ -206,6 +208,12 @@ int dg_ctx_create(const dg_mesh_desc *desc, dg_ctx **out) {
   if (cudaMalloc((void **)&c->d_scal, sizeof(double) * 32) != cudaSuccess) goto cfail;
   if (cudaMemset(c->d_scal, 0, sizeof(double) * 32) != cudaSuccess) goto cfail;
   if (cudaMallocHost((void **)&c->h_scal, sizeof(double) * 32) != cudaSuccess) goto cfail;
+  // the Laplace cell table, built here (not lazily: vmults may run under
+  // CUDA-graph capture, where allocation is not allowed)
+  if (c->dim == 3) {
+    if ((rc = ensure_cell_table(c, 0))) goto fail;
+    if (cudaDeviceSynchronize() != cudaSuccess) goto cfail;
+  }
   *out = c;
   return DG_OK;
 cfail:
@@ -310,6 +318,20 @@ static unsigned chunk_bricks_z(const dg_ctx *c, int BZ, Geo &g) {
   return (unsigned)((g.nz + BZ - 1) / BZ);
 }
 
+// the context's Laplace cell table (3D): per-(cell, side) SIP coefficients and
+// stiffness scales, built once on the stream of the first vmult
+static int ensure_cell_table(dg_ctx *c, cudaStream_t st) {
+  if (c->d_ctab) return DG_OK;
+  double *tab = nullptr;
+  DG_CUDA_CHECK(cudaMalloc(&tab, sizeof(double) * kCellTab * (size_t)c->n_cells));
+  const Geo g0 = c->geo();
+  const int64_t items = 7 * c->n_cells;
+  lap6_cell_table_kernel<<<(unsigned)((items + 255) / 256), 256, 0, st>>>(g0, tab);
+  DG_LAUNCH_CHECK("lap6_cell_table_kernel");
+  c->d_ctab = tab;
+  return DG_OK;
+}
+
 template <int DIM, int N, int BX, int BY, int BZ, int EPI = kEpiStore>
 static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                           cudaStream_t st, const EpiArgs &ea = EpiArgs{}) {
@@ -320,15 +342,7 @@ static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
-  if (!c->d_ctab) {  // per-cell face coefficients, once per context
-    double *tab = nullptr;
-    DG_CUDA_CHECK(cudaMalloc(&tab, sizeof(double) * kCellTab * (size_t)c->n_cells));
-    const Geo g0 = c->geo();
-    const int64_t items = 7 * c->n_cells;
-    lap6_cell_table_kernel<N><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(g0, tab);
-    DG_LAUNCH_CHECK("lap6_cell_table_kernel");
-    c->d_ctab = tab;
-  }
+  if (c->dim == 3 && ensure_cell_table(c, st) != DG_OK) return DG_ECUDA;
   Geo g = c->geo();
   const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, chunk_bricks_z(c, BZ, g));
   kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part, ea);
@@ -359,6 +373,7 @@ static int launch_laplace_f(dg_ctx *c, const float *src, float *dst, double tau_
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
+  if (DIM == 3 && ensure_cell_table(c, st) != DG_OK) return DG_ECUDA;
   Geo g = c->geo();
   g.bz0 = 0;
   const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, (g.nz + BZ - 1) / BZ);
@@ -435,15 +450,7 @@ static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
-  if (!c->d_ctab) {  // per-cell face coefficients, once per context
-    double *tab = nullptr;
-    DG_CUDA_CHECK(cudaMalloc(&tab, sizeof(double) * kCellTab * (size_t)c->n_cells));
-    const Geo g0 = c->geo();
-    const int64_t items = 7 * c->n_cells;
-    lap6_cell_table_kernel<N><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(g0, tab);
-    DG_LAUNCH_CHECK("lap6_cell_table_kernel");
-    c->d_ctab = tab;
-  }
+  if (c->dim == 3 && ensure_cell_table(c, st) != DG_OK) return DG_ECUDA;
   Geo g = c->geo();
   const dim3 grid((g.nx + BX - 1) / BX, (g.ny + BY - 1) / BY, chunk_bricks_z(c, BZ, g));
   kern<<<grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale, part, ea);

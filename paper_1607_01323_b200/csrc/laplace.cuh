@@ -172,6 +172,42 @@ __device__ __forceinline__ int slot_of(int d, int s, int pos) {
                 : (d == 1 ? C::SLOT1 + s * C::NS1 + pos : C::SLOT2 + s * C::NS2 + pos);
 }
 
+// Global source of halo slot `slot` (neighbour cell across the brick surface)
+// or nullptr when that neighbour is a boundary, lies in the brick (periodic
+// wrap onto the brick itself) or the slot is outside a partial brick.  Pure
+// index arithmetic, the same resolution as resolve_nbr.
+template <class C, int N, int BX, int BY, int BZ, class R = double>
+__device__ __forceinline__ const R *halo_slot_src(const Geo &g, const R *u, int slot,
+                                                       int x0, int y0, int z0, int ex, int ey,
+                                                       int ez, int &d, int &s) {
+  constexpr int NP = N * N * N;
+  int loc;
+  if (slot < C::SLOT1) { d = 0; loc = slot; }
+  else if (slot < C::SLOT2) { d = 1; loc = slot - C::SLOT1; }
+  else { d = 2; loc = slot - C::SLOT2; }
+  const int ns = d == 0 ? C::NS0 : (d == 1 ? C::NS1 : C::NS2);
+  s = loc >= ns;
+  const int pos = loc - s * ns;
+  int ix, iy, iz;
+  if (d == 0) { iy = pos % BY; iz = pos / BY; if (iy >= ey || iz >= ez) return nullptr; ix = s ? ex - 1 : 0; }
+  else if (d == 1) { ix = pos % BX; iz = pos / BX; if (ix >= ex || iz >= ez) return nullptr; iy = s ? ey - 1 : 0; }
+  else { ix = pos % BX; iy = pos / BX; if (ix >= ex || iy >= ey) return nullptr; iz = s ? ez - 1 : 0; }
+  ix += x0; iy += y0; iz += z0;
+  const int nd = d == 0 ? g.nx : (d == 1 ? g.ny : g.nz);
+  const int lo = d == 0 ? x0 : (d == 1 ? y0 : z0);
+  const int ext = d == 0 ? ex : (d == 1 ? ey : ez);
+  int nc = (d == 0 ? ix : (d == 1 ? iy : iz)) + (s ? 1 : -1);
+  if (nc < 0 || nc >= nd) {
+    const int m = g.mode[2 * d + s];
+    if (m == kGhost) return reinterpret_cast<const R *>(g.ghost[s]) + (size_t)(iy + g.ny * iz) * NP;
+    if (m != kWrap) return nullptr;
+    nc = s ? 0 : nd - 1;
+  }
+  if (nc >= lo && nc < lo + ext) return nullptr;
+  const int cx = d == 0 ? nc : ix, cy = d == 1 ? nc : iy, cz = d == 2 ? nc : iz;
+  return u + ((size_t)cx + (size_t)g.nx * (cy + (size_t)g.ny * cz)) * NP;
+}
+
 // ---- even-odd helpers on register arrays ------------------------------------
 template <int N, class R>
 __device__ __forceinline__ void eo_split(const R *v, R *e, R *o) {
@@ -365,6 +401,52 @@ laplace_vmult_kernel(const R *__restrict__ u, R *__restrict__ out, const Geo g,
     R a_vo = 0.0, a_go = 0.0, a_vn = 0.0, a_gn = 0.0, b_vo = 0.0, b_vn = 0.0;
     int off = C::OFF_FBUF + (c * 4 + (s ? 2 : 0)) * LPC;  // own data (any valid)
     const R *hsrc_cell = nullptr;
+    if (DIM == 3 && g.ctab != nullptr) {
+      // coefficients from the context's cell table (laplace6.cuh), neighbour
+      // kind by index arithmetic: no dependent loads, no divisions
+      if (jx < ex && jy < ey && jz < ez) {
+        const size_t e = (size_t)(x0 + jx) + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz));
+        const double *tr = g.ctab + e * kCellTab + 3 * side;
+        const R A = (R)(tau_scale * tr[0]), B = (R)tr[1], Dn = (R)tr[2];
+        const int nd = d == 0 ? g.nx : (d == 1 ? g.ny : g.nz);
+        const int lo = d == 0 ? x0 : (d == 1 ? y0 : z0);
+        const int ext = d == 0 ? ex : (d == 1 ? ey : ez);
+        int nc = (d == 0 ? x0 + jx : (d == 1 ? y0 + jy : z0 + jz)) + (s ? 1 : -1);
+        int kind = 1;  // 0 in-brick, 1 halo, 2 boundary
+        bool ghost = false;
+        if (nc < 0 || nc >= nd) {
+          const int m = g.mode[2 * d + s];
+          if (m == kWrap) nc = s ? 0 : nd - 1;
+          else if (m == kGhost) ghost = true;
+          else kind = 2;
+        }
+        a_vo = A; a_go = B; b_vo = B;
+        if (kind == 1) {
+          a_vn = -A; a_gn = Dn; b_vn = -B;
+          if (!ghost && nc >= lo && nc < lo + ext) {
+            const int cb = d == 0 ? (nc - x0) + BX * (jy + BY * jz)
+                                  : (d == 1 ? jx + BX * ((nc - y0) + BY * jz)
+                                            : jx + BX * (jy + BY * (nc - z0)));
+            off = C::OFF_FBUF + (cb * 4 + (s ? 0 : 2)) * LPC;
+          } else {
+            const int pos = d == 0 ? jy + BY * jz : (d == 1 ? jx + BX * jz : jx + BX * jy);
+            off = (d == 0 ? C::OFF_HRAW : C::OFF_HBUF) + slot_of<C>(d, s, pos) * 2 * LPC;
+          }
+        }
+      }
+      const bool edge = d == 0 ? jx == (s ? ex - 1 : 0)
+                               : (d == 1 ? jy == (s ? ey - 1 : 0) : jz == (s ? ez - 1 : 0));
+      if (edge) {
+        const int pos = d == 0 ? jy + BY * jz : (d == 1 ? jx + BX * jz : jx + BX * jy);
+        const int slot = slot_of<C>(d, s, pos);
+        int dd, ss;
+        hsrc[slot] = halo_slot_src<C, N, BX, BY, BZ, R>(g, u, slot, x0, y0, z0, ex, ey, ez, dd, ss);
+      }
+      R *sc = sside + C::SIDEC * it;
+      sc[0] = a_vo; sc[1] = a_go; sc[2] = a_vn; sc[3] = a_gn; sc[4] = b_vo; sc[5] = b_vn;
+      soff[it] = off;
+      continue;
+    }
     if (jx < ex && jy < ey && jz < ez) {
       const int ix = x0 + jx, iy = y0 + jy, iz = z0 + jz;
       NbrInfoT<R> nb;
@@ -428,7 +510,17 @@ laplace_vmult_kernel(const R *__restrict__ u, R *__restrict__ out, const Geo g,
       if (DIM == 3) h2 = g.hz[z0 + jz];
     }
     R *ct = scell + 4 * cc;  // (2/h_d) s_d: scale of K along d
-    if (DIM == 3) {
+    if (DIM == 3 && g.ctab != nullptr) {
+      if (jx < ex && jy < ey && jz < ez) {
+        const double *tr =
+            g.ctab + ((size_t)(x0 + jx) + (size_t)g.nx * ((y0 + jy) + (size_t)g.ny * (z0 + jz))) * kCellTab;
+        ct[0] = (R)tr[18];
+        ct[1] = (R)tr[19];
+        ct[2] = (R)tr[20];
+      } else {
+        ct[0] = ct[1] = ct[2] = 0.0;
+      }
+    } else if (DIM == 3) {
       ct[0] = 0.5 * h1 * h2 / h0;
       ct[1] = 0.5 * h0 * h2 / h1;
       ct[2] = 0.5 * h0 * h1 / h2;

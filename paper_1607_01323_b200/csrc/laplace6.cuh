@@ -67,42 +67,6 @@ struct Lap6Cfg {
   static constexpr size_t SMEM = sizeof(double) * (size_t)NDBL + sizeof(int) * NC * 6;
 };
 
-// Global source of halo slot `slot` (neighbour cell across the brick surface)
-// or nullptr when that neighbour is a boundary, lies in the brick (periodic
-// wrap onto the brick itself) or the slot is outside a partial brick.  Pure
-// index arithmetic, the same resolution as resolve_nbr.
-template <class C, int N, int BX, int BY, int BZ>
-__device__ __forceinline__ const double *halo_slot_src(const Geo &g, const double *u, int slot,
-                                                       int x0, int y0, int z0, int ex, int ey,
-                                                       int ez, int &d, int &s) {
-  constexpr int NP = N * N * N;
-  int loc;
-  if (slot < C::SLOT1) { d = 0; loc = slot; }
-  else if (slot < C::SLOT2) { d = 1; loc = slot - C::SLOT1; }
-  else { d = 2; loc = slot - C::SLOT2; }
-  const int ns = d == 0 ? C::NS0 : (d == 1 ? C::NS1 : C::NS2);
-  s = loc >= ns;
-  const int pos = loc - s * ns;
-  int ix, iy, iz;
-  if (d == 0) { iy = pos % BY; iz = pos / BY; if (iy >= ey || iz >= ez) return nullptr; ix = s ? ex - 1 : 0; }
-  else if (d == 1) { ix = pos % BX; iz = pos / BX; if (ix >= ex || iz >= ez) return nullptr; iy = s ? ey - 1 : 0; }
-  else { ix = pos % BX; iy = pos / BX; if (ix >= ex || iy >= ey) return nullptr; iz = s ? ez - 1 : 0; }
-  ix += x0; iy += y0; iz += z0;
-  const int nd = d == 0 ? g.nx : (d == 1 ? g.ny : g.nz);
-  const int lo = d == 0 ? x0 : (d == 1 ? y0 : z0);
-  const int ext = d == 0 ? ex : (d == 1 ? ey : ez);
-  int nc = (d == 0 ? ix : (d == 1 ? iy : iz)) + (s ? 1 : -1);
-  if (nc < 0 || nc >= nd) {
-    const int m = g.mode[2 * d + s];
-    if (m == kGhost) return g.ghost[s] + (size_t)(iy + g.ny * iz) * NP;
-    if (m != kWrap) return nullptr;
-    nc = s ? 0 : nd - 1;
-  }
-  if (nc >= lo && nc < lo + ext) return nullptr;
-  const int cx = d == 0 ? nc : ix, cy = d == 1 ? nc : iy, cz = d == 2 ? nc : iz;
-  return u + ((size_t)cx + (size_t)g.nx * (cy + (size_t)g.ny * cz)) * NP;
-}
-
 // The context's cell table (once per context, one thread per (cell, side) and
 // one per cell for the scales): the face coupling of every (cell, side) as
 // three coefficients, A without tau_scale,
@@ -112,8 +76,7 @@ __device__ __forceinline__ const double *halo_slot_src(const Geo &g, const doubl
 // with s the tangential face scale, then the per-cell stiffness scales and
 // |cell|/8.  The vmult copies a brick's rows with its cells (TMA), so its
 // prologue does index arithmetic only.
-template <int N>
-__global__ void lap6_cell_table_kernel(const Geo g, double *tab) {
+static __global__ void lap6_cell_table_kernel(const Geo g, double *tab) {
   const int64_t ncell = (int64_t)g.nx * g.ny * g.nz;
   const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (it >= ncell * 7) return;
@@ -133,7 +96,7 @@ __global__ void lap6_cell_table_kernel(const Geo g, double *tab) {
   const int d = side >> 1, s = side & 1;
   const double *dummy = tab;  // resolve_nbr forms (never dereferenced) source pointers
   NbrInfo nb;
-#define DG_RES(DD, SS) resolve_nbr<DD, SS, 3, N, 1, 1, 1>(g, dummy, ix, iy, iz, 0, 0, 0, 0, 0, 0)
+#define DG_RES(DD, SS) resolve_nbr<DD, SS, 3, 2, 1, 1, 1>(g, dummy, ix, iy, iz, 0, 0, 0, 0, 0, 0)
   switch (side) {
     case 0: nb = DG_RES(0, 0); break;
     case 1: nb = DG_RES(0, 1); break;
