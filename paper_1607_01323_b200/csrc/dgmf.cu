@@ -464,14 +464,16 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
     const char *v = getenv("DG_LAP_VARIANT");  // brick-shape experiments
     return v ? atoi(v) : 0;
   }();
-  if (c->dim == 3 && variant == 6) {  // register-plane kernel at k = 2, 3 (experiment)
-    if (c->n == 4) return launch_laplace6<4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
-    if (c->n == 3) return launch_laplace6<3, 4, 4, 2>(c, src, dst, tau_scale, part, st);
-  }
+  if (c->dim == 3 && variant == 6 && c->n == 4)  // register-plane kernel at k = 3 (experiment)
+    return launch_laplace6<4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+
   if (c->dim == 3) {
     switch (c->n) {
       case 2: return launch_laplace<3, 2, 8, 4, 4>(c, src, dst, tau_scale, part, st);
-      case 3: return launch_laplace<3, 3, 4, 4, 4>(c, src, dst, tau_scale, part, st);
+      case 3:  // register-plane kernel (64^3 Q2: 69 vs 52 GDoF/s for the v4 bricks;
+               // bricks 4x2x2 66, 8x4x2 65, 4x4x4 59)
+        if (variant == 4) return launch_laplace<3, 3, 4, 4, 4>(c, src, dst, tau_scale, part, st);
+        return launch_laplace6<3, 4, 4, 2>(c, src, dst, tau_scale, part, st);
       case 4: return launch_laplace<3, 4, 4, 4, 2>(c, src, dst, tau_scale, part, st);
       case 5:
         if (variant == 4) return launch_laplace<3, 5, 4, 2, 2>(c, src, dst, tau_scale, part, st);
