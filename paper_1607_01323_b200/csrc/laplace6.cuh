@@ -51,8 +51,12 @@ struct Lap6Cfg {
   static constexpr bool FX_IN_BUF0 = FBUF <= BUF;
   static constexpr bool FY_IN_BUF1 = FBUF <= BUF;
   static constexpr int OFF_BUF1 = BUF;
-  static constexpr int OFF_FBX = FX_IN_BUF0 ? 0 : 2 * BUF;
-  static constexpr int OFF_FBY = FY_IN_BUF1 ? OFF_BUF1 : 2 * BUF + (FX_IN_BUF0 ? 0 : FBUF);
+  // x functionals go to buf1 (free until the G planes), y and z functionals
+  // to buf0 (its planes are in registers by then): publishing the x
+  // functionals needs no barrier after the u planes leave buf0
+  static constexpr int OFF_FBX = FX_IN_BUF0 ? OFF_BUF1 : 2 * BUF;
+  static constexpr int OFF_FBY = FY_IN_BUF1 ? 0 : 2 * BUF + (FX_IN_BUF0 ? 0 : FBUF);
+  static constexpr int OFF_FBZ = FX_IN_BUF0 ? 0 : OFF_FBX;
   static constexpr int OFF_HRAW = 2 * BUF + (FX_IN_BUF0 ? 0 : FBUF) + (FY_IN_BUF1 ? 0 : FBUF);
   static constexpr int OFF_ZERO = OFF_HRAW + HSIZE;        // 2*LPC zeros (boundary neighbours)
   // per-cell tables with odd cell strides (a half-warp reads 16 cells' entries)
@@ -139,6 +143,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   double *buf1 = smem + C::OFF_BUF1;
   double *fbx = smem + C::OFF_FBX;
   double *fby = smem + C::OFF_FBY;
+  double *fbz = smem + C::OFF_FBZ;
   double *hraw = smem + C::OFF_HRAW;
   double *sside = smem + C::OFF_SIDE;
   double *scell = sside + 18;  // per-cell scales at offset 18 of each table row
@@ -218,7 +223,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
         const int cb = d == 0 ? (nc - x0) + BX * (jy + BY * jz)
                               : (d == 1 ? jx + BX * ((nc - y0) + BY * jz)
                                         : jx + BX * (jy + BY * (nc - z0)));
-        off = (d == 1 ? C::OFF_FBY : C::OFF_FBX) + cb * C::FSTR + (s ? 0 : 2) * LPC;
+        off = (d == 0 ? C::OFF_FBX : (d == 1 ? C::OFF_FBY : C::OFF_FBZ)) + cb * C::FSTR + (s ? 0 : 2) * LPC;
       } else if (kind == 1) {
         off = C::OFF_HRAW + slot_of<C>(d, s, pos) * 2 * LPC;
       }
@@ -379,7 +384,6 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
 #pragma unroll
       for (int i = 0; i < N; ++i) P[j][i] = up[j * N + i];
   }
-  if (C::FX_IN_BUF0) __syncthreads();  // #1b: every plane of u is in registers
   if (has) publish(fbx, s * N, [&](int l, int q) { return P[l][q]; });  // x-lines t = z*N + y
   __syncthreads();  // #2
   // halo step A: y/z slots M_x in place (rows along x)
@@ -462,7 +466,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       for (int q = 0; q < N; ++q) P[q][l] = v[q];
     }
   }
-  if (C::FY_IN_BUF1) __syncthreads();  // #3b: y functionals live in buf1
+  if (C::FY_IN_BUF1) __syncthreads();  // #3b: y functionals live in buf0 (Q goes there)
   if (has) {  // Q -> buf0 (z-slab s), G -> buf1
     double *q = buf0 + c * CS + s * PS, *gp = buf1 + c * CS + s * PS;
 #pragma unroll
@@ -486,7 +490,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       }
   }
   if (C::FX_IN_BUF0) __syncthreads();  // #4b: Q and G planes are in registers
-  if (has) publish(fbx, s * N, [&](int l, int q2) { return P[q2][l]; });  // z-lines t = y*N + x
+  if (has) publish(fbz, s * N, [&](int l, int q2) { return P[q2][l]; });  // z-lines t = y*N + x
   __syncthreads();  // #5
   // ---- Z-b: out = M_z G + s_z Kh_z Q + Lz -> buf1 (y = s plane) ------------
   if (has) {
@@ -553,7 +557,7 @@ laplace6_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       epi_store<EPI, 3, N>(u, out, ea, g0 + w, buf1[si], wq, eacc);
     }
   }
-  if (EPI == kEpiDot) epi_reduce(eacc, fbx, ea, bx + gridDim.x * (by + gridDim.y * bz));
+  if (EPI == kEpiDot) epi_reduce(eacc, fbz, ea, bx + gridDim.x * (by + gridDim.y * bz));
 }
 
 }  // namespace dg
