@@ -494,6 +494,52 @@ def main():
                "h2d_bytes_per_step": 8 * total, "d2h_bytes_per_step": 8 * total,
                "ms_per_step": ems / K2, "steps": K2}
 
+    # C5 CG iteration on every rank count: the slab vmult
+    # with its overlapped halo exchange, two inner products all-reduced over
+    # NCCL, vector updates as device ops; unpreconditioned, fixed count
+    cgi = None
+    if not args.no_cg:
+        from paper_1607_01323_b200.parallel import allreduce_sum
+        r = src.clone()
+        p = r.clone()
+        x = torch.zeros_like(r)
+        Ap = torch.empty_like(r)
+        rr = [allreduce_sum(torch.dot(r, r).reshape(1))]
+
+        def cg_iter():
+            op.vmult(p, Ap)
+            pAp = allreduce_sum(torch.dot(p, Ap).reshape(1))
+            alpha = rr[0] / pAp
+            x.addcmul_(p, alpha)
+            r.addcmul_(Ap, alpha, value=-1.0)
+            rn = allreduce_sum(torch.dot(r, r).reshape(1))
+            p.mul_(rn / rr[0]).add_(r)
+            rr[0] = rn
+
+        for _ in range(3):
+            cg_iter()
+        torch.cuda.synchronize()
+        barrier()
+        KC = 20
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(KC):
+            cg_iter()
+        c1.record()
+        torch.cuda.synchronize()
+        cms = c0.elapsed_time(c1)
+        if world > 1:
+            t = torch.tensor([cms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            cms = t.item()
+        cgi = {"config": f"C5: {n}^3 Q{k} walls, CG iteration (unpreconditioned): x-slab vmult "
+                         f"with overlapped halo exchange + 2 all-reduced inner products + "
+                         f"vector updates, {world} GPU(s)",
+               "iterations": KC, "ms_per_iteration": cms / KC,
+               "dof_per_s_per_iteration": total / (cms / KC * 1e-3),
+               "vmult_share": ms_step / (cms / KC)}
+        del r, p, x, Ap
+
     cg = None
     if rank == 0 and world == 1 and not args.no_cg:
         cg = run_cg(False)
@@ -551,6 +597,8 @@ def main():
         }
         if e2e:
             line["e2e"] = e2e
+        if cgi:
+            line["cg_iteration_c5"] = cgi
         if cg:
             line["cg"] = cg
         if step:
