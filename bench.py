@@ -513,7 +513,7 @@ def main():
             x.addcmul_(p, alpha)
             r.addcmul_(Ap, alpha, value=-1.0)
             rn = allreduce_sum(torch.dot(r, r).reshape(1))
-            p.mul_(rn / rr[0]).add_(r)
+            torch.addcmul(r, p, rn / rr[0], out=p)  # p = r + beta p, one pass
             rr[0] = rn
 
         for _ in range(3):
