@@ -146,6 +146,30 @@ def test_config1_vmult():
         assert relerr(got, want) < TOL
 
 
+BRICK_CASES = [
+    # several full bricks per axis of every kernel's tiling, bench BCs (walls
+    # everywhere, velocity-Dirichlet kind), the NeumannBC kind, grading, and
+    # partial bricks / partial z-columns
+    ((16, 8, 8), (False, False, False), "D", None),
+    ((16, 8, 8), (False, False, False), "N", (0.6, 1.2, 0.9)),
+    ((12, 10, 9), (True, False, True), "D", (0.0, 1.8, 0.0)),
+    ((8, 12, 20), (True, True, False), "N", None),
+]
+
+
+@pytest.mark.parametrize("case", range(len(BRICK_CASES)))
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+def test_vmult_multibrick_matches_oracle(case, k):
+    counts, per, kind, grading = BRICK_CASES[case]
+    kinds = {t: kind for t in O.TAG_NAMES}
+    ext = ((0, 1), (0, 2), (0, 1))
+    osp, obcs, gsp, gbcs = oracle_and_gpu_3d(ext, counts, k, per, kinds, grading)
+    p = np.random.default_rng(11 * case + k).uniform(-1, 1, osp.field_shape())
+    want = O.apply_pressure_laplace(osp, p, obcs).ravel()
+    got = host(ops.apply_pressure_laplace(gsp, dev(p), gbcs))
+    assert relerr(got, want) < TOL, relerr(got, want)
+
+
 @pytest.mark.parametrize("k,nx", [(3, 8), (4, 6)])
 def test_pcg_histories_match_reference_2d(k, nx):
     """Fused device PCG vs the reference's own solves (golden): Chebyshev(5,20)

@@ -93,8 +93,6 @@ def host(t):
 @pytest.mark.parametrize("variant", ["V3c", "V4", "VHW"])
 @pytest.mark.parametrize("fused", [False, True])
 def test_two_steps_match_oracle(name, variant, fused):
-    if fused and variant != "V4":
-        pytest.skip("fused pressure solve checked on V4")
     osp, ospec, gsp, gspec = setups(name)
     bf = force if name == "outflow" else None
     ocfg = OS.StepConfig(dt=1e-3, nu=1 / 180, variant=OS.Variant(variant), body_force=bf)
@@ -108,24 +106,23 @@ def test_two_steps_match_oracle(name, variant, fused):
     ow = O.compute_vorticity(osp[-1], u0)
     ou, op_, ow_h = [u0, u0], [], [ow, ow]
     gu, gp_, gw_h = [dev(u0), dev(u0)], [], [dev(ow), dev(ow)]
-    tol = 1e-9 if not fused else 1e-6
+    # the fused path (device MG-PCG on the correction, device vector PCG)
+    # keeps the exact counts and the plain path's bar (profiles/r02/step_counts.py)
+    tol = 1e-9 if not fused else 1e-10
     for n in range(2):
         t = n * 1e-3
         ro = ovc.step(ou, op_, ow_h, t)
         rg = gvc.step(gu, gp_, gw_h, t)
         assert relerr(host(rg.uhat), ro.uhat.ravel()) < 1e-11, "uhat"
-        if not fused:
-            assert rg.iters["pressure"] == ro.iters["pressure"]
-        else:
-            assert abs(rg.iters["pressure"] - ro.iters["pressure"]) <= 1
+        assert rg.iters["pressure"] == ro.iters["pressure"]
         p_ref = ro.p.ravel()
         assert relerr(host(rg.p), p_ref) < tol, ("p", relerr(host(rg.p), p_ref))
         if variant == "V3c":
             assert abs(rg.iters["projection"] - ro.iters["projection"]) <= 2
         else:
-            assert rg.iters["projection"] == ro.iters["projection"] or fused
+            assert rg.iters["projection"] == ro.iters["projection"]
         assert relerr(host(rg.uhh), ro.uhh.ravel()) < tol, "uhh"
-        assert abs(rg.iters["viscous"] - ro.iters["viscous"]) <= (0 if not fused else 1)
+        assert rg.iters["viscous"] == ro.iters["viscous"]
         assert relerr(host(rg.u), ro.u.ravel()) < tol, "u"
         assert relerr(host(rg.w), ro.w.ravel()) < tol * 10, "w"
         ou, op_, ow_h = [ro.u, ou[0]], [ro.p] + op_[:1], [ro.w, ow_h[0]]
