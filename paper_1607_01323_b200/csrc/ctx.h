@@ -29,6 +29,8 @@ struct dg_ctx {
   std::vector<double> ghost_tau_h[2];
   double *d_hx = nullptr, *d_hy = nullptr, *d_hz = nullptr, *d_tau = nullptr;
   double *d_hinv = nullptr;  // [1/hx | 1/hy | 1/hz]
+  double *d_axis = nullptr;  // per-axis [h, 1/h, tau part, 0] incl. one neighbour per side
+  int64_t axis_off[3] = {0, 0, 0};
   double *d_ghost_tau[2] = {nullptr, nullptr};
   const double *d_recv[2] = {nullptr, nullptr};  // caller-owned ghost layers
   int64_t halo_count = 0;
@@ -77,6 +79,7 @@ struct dg_ctx {
     g.exp_flags = exp_flags;
     g.bz0 = 0;
     g.ctab = d_ctab;
+    for (int d = 0; d < 3; ++d) g.ax[d] = d_axis ? d_axis + axis_off[d] : nullptr;
     return g;
   }
 };

@@ -10,6 +10,7 @@
 #include "ctx.h"
 #include "laplace.cuh"
 #include "laplace6.cuh"
+#include "laplace7.cuh"
 #include "mg.cuh"
 #include "tables.h"
 #include "tensor.cuh"
@@ -38,26 +39,44 @@ using namespace dg;
 
 // tau_e of GLOBAL cell (gx, gy, gz), Eq. 18 (geometry.py:90-108): every
 // boundary face counts in A_bnd (also walls without a pressure term),
-// periodic faces count as interior.
-static double tau_global(const dg_ctx *c, int gx, int gy, int gz) {
-  const int gi[3] = {gx, gy, gz};
-  double h[3] = {1.0, 1.0, 1.0};
-  for (int d = 0; d < c->dim; ++d) h[d] = c->gvert[d][gi[d] + 1] - c->gvert[d][gi[d]];
-  double vol = 1.0;
-  for (int d = 0; d < c->dim; ++d) vol *= h[d];
-  double aint = 0.0, abnd = 0.0;
-  for (int d = 0; d < c->dim; ++d) {
-    double area = 1.0;
-    for (int dd = 0; dd < c->dim; ++dd)
-      if (dd != d) area *= h[dd];
-    for (int s = 0; s < 2; ++s) {
-      const bool edge = s ? (gi[d] == c->gcounts[d] - 1) : (gi[d] == 0);
-      if (edge && !c->periodic[d]) abnd += area;
-      else aint += area;
-    }
+// periodic faces count as interior.  On Cartesian cells A/V separates per
+// axis, tau_e = (k+1)^2 sum_d (w_lo + w_hi) / h_d with w = 1 on a boundary
+// side and 1/2 otherwise; the sum is taken in the fixed order (x + y) + z,
+// the order in which the Laplace column kernel (laplace7.cuh) forms it from
+// the per-axis terms, so tau is bitwise the same everywhere.
+static double tau_axis(const dg_ctx *c, int d, int gi) {
+  const double h = c->gvert[d][gi + 1] - c->gvert[d][gi];
+  double w = 0.0;
+  for (int s = 0; s < 2; ++s) {
+    const bool edge = s ? (gi == c->gcounts[d] - 1) : (gi == 0);
+    w += (edge && !c->periodic[d]) ? 1.0 : 0.5;
   }
   const double kp = (double)(c->k + 1);
-  return kp * kp * (0.5 * aint + abnd) / vol;
+  return kp * kp * w / h;
+}
+
+static double tau_global(const dg_ctx *c, int gx, int gy, int gz) {
+  double t = tau_axis(c, 0, gx) + tau_axis(c, 1, gy);
+  if (c->dim == 3) t += tau_axis(c, 2, gz);
+  return t;
+}
+
+// per-axis cell data of the owned index range extended by one cell per side
+// (the periodic wrap or x-slab ghost neighbour; a copy of the end cell on a
+// boundary): [i + 1][h, 1/h, tau_axis, 0] for local i in [-1, n_d]
+static std::vector<double> axis_table(const dg_ctx *c, int d) {
+  const int n = c->counts[d], off = d == 0 ? c->slab_begin : 0, gn = c->gcounts[d];
+  std::vector<double> t(4 * (size_t)(n + 2), 0.0);
+  for (int i = -1; i <= n; ++i) {
+    int gi = off + i;
+    if (gi < 0) gi = c->periodic[d] ? gn - 1 : 0;
+    if (gi >= gn) gi = c->periodic[d] ? 0 : gn - 1;
+    double *e = &t[4 * (size_t)(i + 1)];
+    e[0] = c->gvert[d][gi + 1] - c->gvert[d][gi];
+    e[1] = 1.0 / e[0];
+    e[2] = d < c->dim ? tau_axis(c, d, gi) : 0.0;
+  }
+  return t;
 }
 
 template <typename T>
@@ -204,6 +223,15 @@ int dg_ctx_create(const dg_mesh_desc *desc, dg_ctx **out) {
     if ((rc = upload(&c->d_hinv, hinv))) goto fail;
   }
   if ((rc = upload(&c->d_tau, c->tau))) goto fail;
+  {
+    std::vector<double> ax;
+    for (int d = 0; d < 3; ++d) {
+      c->axis_off[d] = (int64_t)ax.size() + 4;  // entry of local index 0
+      const std::vector<double> t = axis_table(c, d);
+      ax.insert(ax.end(), t.begin(), t.end());
+    }
+    if ((rc = upload(&c->d_axis, ax))) goto fail;
+  }
   if (cudaMalloc((void **)&c->d_red, sizeof(double) * (kRedBlocks + 64)) != cudaSuccess) goto cfail;
   if (cudaMalloc((void **)&c->d_scal, sizeof(double) * 32) != cudaSuccess) goto cfail;
   if (cudaMemset(c->d_scal, 0, sizeof(double) * 32) != cudaSuccess) goto cfail;
@@ -234,6 +262,7 @@ int dg_ctx_destroy(dg_ctx *c) {
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   cudaFree(c->d_tau);
+  cudaFree(c->d_axis);
   for (int s = 0; s < 2; ++s) {
     cudaFree(c->d_ghost_tau[s]);
   }
@@ -458,12 +487,73 @@ static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau
   return DG_OK;
 }
 
+// z-marching column kernel (laplace7.cuh): units = TX x TY tiles x z-chunks,
+// the chunk length chosen so that ~4 waves of CTAs fill the GPU
+template <int N, int TX, int TY, int NRING, int MINB, bool STAGE = false>
+static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
+                           cudaStream_t st) {
+  using C = Lap7Cfg<N, TX, TY, NRING>;
+  auto kern = laplace7_kernel<N, TX, TY, NRING, MINB, STAGE>;
+  static int nsm = 0, occ = 1;
+  if (!nsm) {
+    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    int dev = 0;
+    DG_CUDA_CHECK(cudaGetDevice(&dev));
+    DG_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    DG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM));
+    if (occ < 1) occ = 1;
+  }
+  const Geo g = c->geo();
+  int zlo = 0, zhi = g.nz;
+  if (t_chunk.z1 > 0) {
+    zlo = t_chunk.z0;
+    zhi = t_chunk.z1;
+  }
+  const int ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY;
+  const int cols = ntx * nty, nz = zhi - zlo;
+  const int want = (4 * nsm * occ + cols - 1) / cols;  // chunks per column
+  int lc = std::max(8, (nz + want - 1) / want);
+  lc = std::min(std::min(lc, nz), C::LCMAX);
+  const int nch = (nz + lc - 1) / lc;
+  kern<<<(unsigned)(cols * nch), C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis),
+                                                            tau_scale, part, zlo, zhi, lc, ntx, nty);
+  DG_LAUNCH_CHECK("laplace7_kernel");
+  return DG_OK;
+}
+
+// tile / ring configuration of the column kernel (DG_L7CFG: experiments)
+static int l7_cfg() {
+  const char *e = getenv("DG_L7CFG");  // read per call: A/B within one process
+  return e ? atoi(e) : 0;
+}
+
 static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                             cudaStream_t st) {
-  static const int variant = [] {
-    const char *v = getenv("DG_LAP_VARIANT");  // brick-shape experiments
-    return v ? atoi(v) : 0;
-  }();
+  // DG_LAP_VARIANT (read per call, A/B experiments): 4 = v4 bricks, 6 = the
+  // round-1 register-plane bricks, 7 = column kernel with tile config DG_L7CFG
+  const char *vv = getenv("DG_LAP_VARIANT");
+  const int variant = vv ? atoi(vv) : 0;
+  if (c->dim == 3 && variant == 7) {
+    const int cfg = l7_cfg();
+    if (c->n == 4) {
+      if (cfg == 1) return launch_laplace7<4, 8, 4, 3, 2>(c, src, dst, tau_scale, part, st);
+      if (cfg == 2) return launch_laplace7<4, 4, 4, 3, 5>(c, src, dst, tau_scale, part, st);
+    }
+    if (c->n == 5) {
+      if (cfg == 1) return launch_laplace7<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
+      if (cfg == 2) return launch_laplace7<5, 4, 4, 3, 2>(c, src, dst, tau_scale, part, st);
+      if (cfg == 3) return launch_laplace7<5, 8, 4, 3, 1>(c, src, dst, tau_scale, part, st);
+    }
+    if (c->n == 6 && cfg == 1) return launch_laplace7<6, 4, 4, 3, 1>(c, src, dst, tau_scale, part, st);
+    if (c->n == 3) return launch_laplace7<3, 8, 4, 3, 2>(c, src, dst, tau_scale, part, st);
+  }
+  // default 3D Q3-Q5: the z-marching column kernel (laplace7.cuh); tile, ring
+  // depth and CTAs/SM measured per degree (profiles/r02/NOTES.md)
+  if (c->dim == 3 && variant != 4 && variant != 6) {
+    if (c->n == 4) return launch_laplace7<4, 4, 4, 4, 4>(c, src, dst, tau_scale, part, st);
+    if (c->n == 5) return launch_laplace7<5, 4, 4, 4, 2>(c, src, dst, tau_scale, part, st);
+    if (c->n == 6) return launch_laplace7<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+  }
   if (c->dim == 3 && variant == 6 && c->n == 4)  // register-plane kernel at k = 3 (experiment)
     return launch_laplace6<4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
 

@@ -1,0 +1,6 @@
+export DG_LAP_VARIANT=7
+for cfg in 0 1 2; do DG_L7CFG=$cfg timeout 600 python -m pytest -x -q -m gpu tests/test_gpu_laplace.py -k "3d or multibrick or config1 or slab or periodic or host_buffer" > gpurun_out/r2d_pytest_$cfg.log 2>&1; tail -2 gpurun_out/r2d_pytest_$cfg.log; done
+unset DG_LAP_VARIANT
+timeout 300 python profiles/r02/vmult_ab.py 128,4 64,4 64,3 96,3 > gpurun_out/r2d_ab0.log 2>&1
+for cfg in 0 1 2; do DG_LAP_VARIANT=7 DG_L7CFG=$cfg timeout 300 python profiles/r02/vmult_ab.py 128,4 64,4 64,3 96,3 > gpurun_out/r2d_ab7_$cfg.log 2>&1; done
+cat gpurun_out/r2d_ab*.log
