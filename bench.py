@@ -494,37 +494,25 @@ def main():
                "h2d_bytes_per_step": 8 * total, "d2h_bytes_per_step": 8 * total,
                "ms_per_step": ems / K2, "steps": K2}
 
-    # C5 CG iteration on every rank count: the slab vmult
-    # with its overlapped halo exchange, two inner products all-reduced over
-    # NCCL, vector updates as device ops; unpreconditioned, fixed count
+    # C5 CG iteration on every rank count: parallel.SlabPCG
+    # (the reference pcg with point-Jacobi preconditioning, pure-Neumann
+    # projected operator as the walls make it): slab vmult with overlapped
+    # halo exchange, dg_cg_dots, NCCL all-reduce, fused x/r/z update with r.z,
+    # NCCL all-reduce, host stop test, p update -- fixed iteration count
     cgi = None
     if not args.no_cg:
-        from paper_1607_01323_b200.parallel import allreduce_sum
-        r = src.clone()
-        p = r.clone()
-        x = torch.zeros_like(r)
-        Ap = torch.empty_like(r)
-        rr = [allreduce_sum(torch.dot(r, r).reshape(1))]
-
-        def cg_iter():
-            op.vmult(p, Ap)
-            pAp = allreduce_sum(torch.dot(p, Ap).reshape(1))
-            alpha = rr[0] / pAp
-            x.addcmul_(p, alpha)
-            r.addcmul_(Ap, alpha, value=-1.0)
-            rn = allreduce_sum(torch.dot(r, r).reshape(1))
-            torch.addcmul(r, p, rn / rr[0], out=p)  # p = r + beta p, one pass
-            rr[0] = rn
-
+        from paper_1607_01323_b200.parallel import SlabPCG
+        solver = SlabPCG(op, op.diagonal(), cheb=None, project_dual=True)
+        solver.start(src, rel_tol=0.0)
         for _ in range(3):
-            cg_iter()
+            solver.step()
         torch.cuda.synchronize()
         barrier()
         KC = 20
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         c0.record()
         for _ in range(KC):
-            cg_iter()
+            solver.step()
         c1.record()
         torch.cuda.synchronize()
         cms = c0.elapsed_time(c1)
@@ -532,13 +520,15 @@ def main():
             t = torch.tensor([cms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             cms = t.item()
-        cgi = {"config": f"C5: {n}^3 Q{k} walls, CG iteration (unpreconditioned): x-slab vmult "
-                         f"with overlapped halo exchange + 2 all-reduced inner products + "
-                         f"vector updates, {world} GPU(s)",
+        cgi = {"config": f"C5: {n}^3 Q{k} walls, Jacobi-PCG iteration (parallel.SlabPCG): x-slab "
+                         f"vmult with overlapped face-trace halo exchange + 2 NCCL all-reduces + "
+                         f"fused vector kernels + host stop test, {world} GPU(s)",
                "iterations": KC, "ms_per_iteration": cms / KC,
                "dof_per_s_per_iteration": total / (cms / KC * 1e-3),
+               "bytes_per_dof_algorithmic": 96,
+               "hbm_frac_of_96B_per_dof": total * 96 / (cms / KC * 1e-3) / 1e9 / hbm_peak()[0],
                "vmult_share": ms_step / (cms / KC)}
-        del r, p, x, Ap
+        del solver
 
     cg = None
     if rank == 0 and world == 1 and not args.no_cg:

@@ -346,12 +346,16 @@ int dg_g2_transfer(int k, int prolong, int64_t n_fine, const int64_t *parent,
 int dg_g2_laplace_diagonal(dg_g2 *g, double tau_scale, const int *kind,
                            double *diag, void *stream);
 
-/* ---- multi-GPU x-slabs (ghost cell layers) ------------------------------ */
-/* doubles in one ghost layer: ny*nz cells of one component (n^dim each),
- * ordered by (iz, iy) -- the size of every send/recv buffer below */
+/* ---- multi-GPU x-slabs (ghost layers) ----------------------------------- */
+/* doubles in one ghost layer, ny*nz cells ordered by (iz, iy) -- the size of
+ * every send/recv buffer below.  3D Q3-Q5 (the column kernel): owner-computed
+ * face traces, per cell [z][y][value | x-derivative] at the facing end
+ * (2 n^2 doubles: the face data of kernels.py:119-156); other degrees: whole
+ * cells (n^dim doubles). */
 int dg_halo_count(const dg_ctx *ctx, int64_t *count);
 /* pack the first/last owned x-layer of src into caller-owned device buffers
- * send_lo / send_hi (either may be NULL) */
+ * send_lo / send_hi (either may be NULL): traces of the left end (value,
+ * dL . line) for send_lo, of the right end (value, dR . line) for send_hi */
 int dg_halo_pack(dg_ctx *ctx, const double *src, double *send_lo,
                  double *send_hi, void *stream);
 /* attach caller-owned device buffers holding the neighbours' layers; they
@@ -361,6 +365,35 @@ int dg_halo_attach(dg_ctx *ctx, const double *recv_lo, const double *recv_hi);
  *       2 = only cells touching a ghost layer (needs recv_* filled) */
 int dg_laplace_vmult_part(dg_ctx *ctx, const double *src, double *dst,
                           double tau_scale, int part, void *stream);
+
+/* ---- sharded (x-slab) PCG building blocks (parallel.SlabPCG) ------------
+ * The reference pcg (solvers.py:30-73) on x-slab contexts: every call works
+ * on this rank's slab; the caller all-reduces the partial sums between calls
+ * (one all-reduce per CG sync point) and the updates read the REDUCED device
+ * scalars scal[8]: [0] r.z, [1] p.Lp, [2] sum(Lp), [3] p.w, [4] r.z new.
+ * out3 = partial [p.Lp, sum(Lp), p.w] (w = dual weights; deterministic). */
+int dg_cg_dots(dg_ctx *ctx, const double *p, const double *Lp, double *out3,
+               void *stream);
+/* alpha = scal[0] / pAp, pAp = p.Lp - (sum(Lp)/|Omega|) p.w (project_dual:
+ * op = zero_mean_project_dual o L, solvers.py:187-198) or p.Lp; no update
+ * when pAp <= 0 (breakdown, the caller stops).  x += alpha p ;
+ * r -= alpha (Lp - c w) ; diag != NULL (Jacobi): z = r / diag and
+ * out_rz = partial r.z (device).  Vector updates round like numpy. */
+int dg_cg_update(dg_ctx *ctx, double *x, double *r, const double *p,
+                 const double *Lp, const double *scal, int project_dual,
+                 const double *diag, double *z, double *out_rz, void *stream);
+/* p = z + (scal[4] / scal[0]) p ; then scal[0] = scal[4] */
+int dg_cg_pupdate(dg_ctx *ctx, double *p, const double *z, double *scal,
+                  void *stream);
+/* Chebyshev (solvers.py:93-129) vector parts: init from x = 0
+ * (d = (r/diag)/theta ; x = d ; rc = r) and one step after the caller's
+ * L d_old (rc -= Ld ; d_new = a d_old + b rc/diag ; x += d_new) */
+int dg_cheb_vec_init(dg_ctx *ctx, const double *r, const double *diag,
+                     double *rc, double *d, double *x, double theta,
+                     void *stream);
+int dg_cheb_vec_step(dg_ctx *ctx, double *rc, const double *Ld,
+                     const double *d_old, double *d_new, const double *diag,
+                     double *x, double a, double b, void *stream);
 
 #ifdef __cplusplus
 }

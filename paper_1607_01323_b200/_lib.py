@@ -125,6 +125,11 @@ PROTOTYPES = {
     "dg_basis_tables": [_I, _I, _DP, _DP, _DP, _DP, _DP, _DP, _DP],
     "dg_laplace_vmult": [_P, _P, _P, _D, _P],
     "dg_laplace_vmult_part": [_P, _P, _P, _D, _I, _P],
+    "dg_cg_dots": [_P, _P, _P, _P, _P],
+    "dg_cg_update": [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P],
+    "dg_cg_pupdate": [_P, _P, _P, _P, _P],
+    "dg_cheb_vec_init": [_P, _P, _P, _P, _P, _P, _D, _P],
+    "dg_cheb_vec_step": [_P, _P, _P, _P, _P, _P, _P, _D, _D, _P],
     "dg_laplace_vmult_host": [_P, _P, _P, _D, _I, _P],
     "dg_laplace_diagonal": [_P, _P, _D, _P],
     "dg_mass": [_P, _P, _P, _I, _P],

@@ -48,7 +48,8 @@ struct Geo {
   int exp_flags;             // timing experiments (DG_EXP env); 0 in production
   int bz0;                   // first brick z index of a chunked (z-range) launch, else 0
   const double *ctab;        // per-cell SIP face coefficients + scales (kCellTab each) or null
-  const double *ax[3];       // per-axis [h, 1/h, tau part, 0] at local index i (i = -1..n: neighbours)
+  const double *ax[3];
+  int ghost_traces;          // ghost layers hold face traces [cell][z][y][v|g], not cells       // per-axis [h, 1/h, tau part, 0] at local index i (i = -1..n: neighbours)
 };
 
 // doubles per cell of the Laplace cell table (laplace6.cuh): 6 sides x (A /

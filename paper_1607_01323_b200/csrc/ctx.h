@@ -37,6 +37,9 @@ struct dg_ctx {
   int64_t n_cells = 0, n_dofs = 0, np = 0;
   double volume = 0.0;  // |Omega| of the GLOBAL mesh
   double *d_red = nullptr;     // reduction partials (kRedBlocks) + scalars
+  double *d_red3 = nullptr;    // 3 x kRedBlocks partials (sharded CG dots)
+  double *d_hcell = nullptr;   // per-cell dual-weight factor hx hy hz / 8 (3D)
+  int halo_traces = 0;         // ghost layers carry face traces (column kernel)
   double *d_scal = nullptr;    // 16 device scalars
   double *h_scal = nullptr;    // pinned mirror
   std::vector<double *> work;  // solver work vectors (n_dofs each)
@@ -78,6 +81,7 @@ struct dg_ctx {
     }();
     g.exp_flags = exp_flags;
     g.bz0 = 0;
+    g.ghost_traces = halo_traces;
     g.ctab = d_ctab;
     for (int d = 0; d < 3; ++d) g.ax[d] = d_axis ? d_axis + axis_off[d] : nullptr;
     return g;

@@ -11,6 +11,7 @@
 #include "laplace.cuh"
 #include "laplace6.cuh"
 #include "laplace7.cuh"
+#include "laplace8.cuh"
 #include "mg.cuh"
 #include "tables.h"
 #include "tensor.cuh"
@@ -197,7 +198,9 @@ int dg_ctx_create(const dg_mesh_desc *desc, dg_ctx **out) {
   for (int d = 0; d < c->dim; ++d) c->volume *= (c->gvert[d].back() - c->gvert[d].front());
   // ghost layers
   const int64_t layer = (int64_t)c->counts[1] * c->counts[2];
-  c->halo_count = layer * c->np;
+  // 3D Q3-Q5 run the column kernel, whose halo consumes face traces
+  c->halo_traces = (c->dim == 3 && c->n >= 4 && c->n <= 6) ? 1 : 0;
+  c->halo_count = layer * (c->halo_traces ? 2 * c->n * c->n : c->np);
   int rc = 0;
   for (int s = 0; s < 2; ++s) {
     int gx;
@@ -263,6 +266,8 @@ int dg_ctx_destroy(dg_ctx *c) {
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   cudaFree(c->d_tau);
   cudaFree(c->d_axis);
+  cudaFree(c->d_red3);
+  cudaFree(c->d_hcell);
   for (int s = 0; s < 2; ++s) {
     cudaFree(c->d_ghost_tau[s]);
   }
@@ -521,6 +526,39 @@ static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau
   return DG_OK;
 }
 
+// half-plane column kernel (laplace8.cuh)
+template <int N, int TX, int TY, int NRING, int MINB>
+static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
+                           cudaStream_t st) {
+  using C = Lap8Cfg<N, TX, TY, NRING>;
+  auto kern = laplace8_kernel<N, TX, TY, NRING, MINB>;
+  static int nsm = 0, occ = 1;
+  if (!nsm) {
+    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    int dev = 0;
+    DG_CUDA_CHECK(cudaGetDevice(&dev));
+    DG_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    DG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM));
+    if (occ < 1) occ = 1;
+  }
+  const Geo g = c->geo();
+  int zlo = 0, zhi = g.nz;
+  if (t_chunk.z1 > 0) {
+    zlo = t_chunk.z0;
+    zhi = t_chunk.z1;
+  }
+  const int ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY;
+  const int cols = ntx * nty, nz = zhi - zlo;
+  const int want = (4 * nsm * occ + cols - 1) / cols;
+  int lc = std::max(8, (nz + want - 1) / want);
+  lc = std::min(std::min(lc, nz), C::LCMAX);
+  const int nch = (nz + lc - 1) / lc;
+  kern<<<(unsigned)(cols * nch), C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis),
+                                                            tau_scale, part, zlo, zhi, lc, ntx, nty);
+  DG_LAUNCH_CHECK("laplace8_kernel");
+  return DG_OK;
+}
+
 // tile / ring configuration of the column kernel (DG_L7CFG: experiments)
 static int l7_cfg() {
   const char *e = getenv("DG_L7CFG");  // read per call: A/B within one process
@@ -532,7 +570,21 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
   // DG_LAP_VARIANT (read per call, A/B experiments): 4 = v4 bricks, 6 = the
   // round-1 register-plane bricks, 7 = column kernel with tile config DG_L7CFG
   const char *vv = getenv("DG_LAP_VARIANT");
-  const int variant = vv ? atoi(vv) : 0;
+  int variant = vv ? atoi(vv) : 0;
+  // ghost layers in the trace format are read by the column kernels only
+  if (c->halo_traces && (c->mode[0] == kGhost || c->mode[1] == kGhost) && variant != 8) variant = 0;
+  if (c->dim == 3 && variant == 8) {
+    const int cfg = l7_cfg();
+    if (c->n == 4) {
+      if (cfg == 1) return launch_laplace8<4, 4, 4, 4, 3>(c, src, dst, tau_scale, part, st);
+      if (cfg == 2) return launch_laplace8<4, 8, 4, 3, 2>(c, src, dst, tau_scale, part, st);
+      return launch_laplace8<4, 4, 4, 4, 4>(c, src, dst, tau_scale, part, st);
+    }
+    if (c->n == 5) {
+      return launch_laplace8<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
+    }
+    if (c->n == 6) return launch_laplace8<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+  }
   if (c->dim == 3 && variant == 7) {
     const int cfg = l7_cfg();
     if (c->n == 4) {
@@ -612,6 +664,28 @@ __device__ __forceinline__ double dual_weight(const Geo &g, int dim, int n, cons
   double v = 0.5 * g.hx[ix] * wi.w[x] * 0.5 * g.hy[iy] * wi.w[y];
   if (dim == 3) v *= 0.5 * g.hz[iz] * wi.w[z];
   return v;
+}
+
+// face traces of the first (side 0: value, dL . line) or last (side 1:
+// value, dR . line) x-layer: one thread per (cell (iy, iz), y, z), the x-line
+// of that cell; out[cell][z][y][v|g] (the ghost layout of laplace7.cuh)
+struct HaloTab {
+  double dL[kMaxN], dR[kMaxN];
+};
+__global__ void halo_trace_kernel(const double *__restrict__ src, double *__restrict__ out,
+                                  int nx, int n, int64_t items, int side, HaloTab t) {
+  const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (it >= items) return;
+  const int64_t nn = (int64_t)n * n;
+  const int64_t cell = it / nn;  // iy + ny * iz
+  const int zy = (int)(it - cell * nn), z = zy / n, y = zy - z * n;
+  const int64_t e = (int64_t)(side ? nx - 1 : 0) + (int64_t)nx * cell;
+  const double *l = src + e * nn * n + (int64_t)z * nn + (int64_t)y * n;
+  double g = 0.0;
+  for (int q = 0; q < n; ++q) g += (side ? t.dR[q] : t.dL[q]) * l[q];
+  double *o = out + (cell * nn + (int64_t)z * n + y) * 2;
+  o[0] = side ? l[n - 1] : l[0];
+  o[1] = g;
 }
 
 __global__ void wdot_partial_kernel(const double *__restrict__ p, int64_t n, Geo g, int dim,
@@ -795,6 +869,19 @@ int dg_halo_attach(dg_ctx *c, const double *recv_lo, const double *recv_hi) {
 int dg_halo_pack(dg_ctx *c, const double *src, double *send_lo, double *send_hi, void *stream) {
   if (!c || !src) return inval("null argument");
   cudaStream_t st = (cudaStream_t)stream;
+  if (c->halo_traces) {  // owner-computed face traces of the first / last x-layer
+    const int64_t items = (int64_t)c->counts[1] * c->counts[2] * c->n * c->n;
+    HaloTab t;
+    for (int i = 0; i < c->n; ++i) {
+      t.dL[i] = c->basis.ld[i];
+      t.dR[i] = c->basis.rd[i];
+    }
+    const unsigned gb = (unsigned)((items + 255) / 256);
+    if (send_lo) halo_trace_kernel<<<gb, 256, 0, st>>>(src, send_lo, c->counts[0], c->n, items, 0, t);
+    if (send_hi) halo_trace_kernel<<<gb, 256, 0, st>>>(src, send_hi, c->counts[0], c->n, items, 1, t);
+    DG_LAUNCH_CHECK("halo_trace_kernel");
+    return DG_OK;
+  }
   const size_t row = sizeof(double) * c->np;
   const size_t pitch = row * c->counts[0];
   const size_t rows = (size_t)c->counts[1] * c->counts[2];
@@ -952,6 +1039,29 @@ int dg_laplace_diagonal(dg_ctx *c, double *diag, double tau_scale, void *stream)
 }  // extern "C"
 
 #include "pcg.inc"
+
+// per-cell dual-weight factor hx hy hz / 8 (3D), built on first use
+__global__ void hcell_kernel(Geo g, double *hc) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)g.nx * g.ny * g.nz) return;
+  const int ix = (int)(e % g.nx), iy = (int)((e / g.nx) % g.ny), iz = (int)(e / ((int64_t)g.nx * g.ny));
+  hc[e] = 0.125 * g.hx[ix] * g.hy[iy] * g.hz[iz];
+}
+static int ensure_hcell(dg_ctx *c) {
+  if (c->d_hcell) return DG_OK;
+  DG_CUDA_CHECK(cudaMalloc((void **)&c->d_hcell, sizeof(double) * (c->n_cells > 0 ? c->n_cells : 1)));
+  hcell_kernel<<<(unsigned)((c->n_cells + 255) / 256), 256>>>(c->geo(), c->d_hcell);
+  DG_LAUNCH_CHECK("hcell_kernel");
+  DG_CUDA_CHECK(cudaDeviceSynchronize());
+  return DG_OK;
+}
+
+static int ensure_red3(dg_ctx *c) {
+  if (c->d_red3) return DG_OK;
+  DG_CUDA_CHECK(cudaMalloc((void **)&c->d_red3, sizeof(double) * 3 * kRedBlocks));
+  return DG_OK;
+}
+#include "slabcg.inc"
 
 // The quadrature-point operators (Helmholtz, projection, convective, the
 // once-per-step right-hand sides, element-local PCG) are in vecops.cu.

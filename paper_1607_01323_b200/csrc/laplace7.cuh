@@ -319,7 +319,9 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     hrow = rem / N;
     hpos = rem - hrow * N;
   }
+  int htrace = 0;
   auto halo_src = [&](int lay) -> const double * {
+    htrace = 0;
     if (hit >= C::HITEMS || lay < 0) return nullptr;
     if (hx_item) {
       if (hrow >= ey) return nullptr;
@@ -328,7 +330,10 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       if (nc < 0 || nc >= g.nx) {
         const int m = g.mode[hside];
         if (m == kWrap) nc = hside ? 0 : g.nx - 1;
-        else if (m == kGhost) return g.ghost[hside] + ((size_t)yy + (size_t)g.ny * lay) * NP;
+        else if (m == kGhost) {  // remote neighbour: its face traces (or whole cells)
+          htrace = g.ghost_traces;
+          return g.ghost[hside] + ((size_t)yy + (size_t)g.ny * lay) * (htrace ? 2 * N2 : NP);
+        }
         else return nullptr;
       }
       if (nc >= x0 && nc < x0 + ex) return nullptr;  // wraps onto the tile itself
@@ -350,6 +355,14 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   auto halo_load = [&](int lay) {
     hsrc = halo_src(lay);
     if (!hsrc) return;
+    if (htrace) {  // [z][y][v|g] of the facing end, raw (M_z below)
+#pragma unroll
+      for (int z = 0; z < N; ++z) {
+        hreg[z][0] = __ldg(hsrc + (z * N + hpos) * 2);
+        hreg[z][1] = __ldg(hsrc + (z * N + hpos) * 2 + 1);
+      }
+      return;
+    }
 #pragma unroll
     for (int z = 0; z < N; ++z)
 #pragma unroll
@@ -366,8 +379,8 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       eo_split<N>(hreg[z], e, o);
       l7_ends<N>(T, e, o, g0, g1);
       // lower side (hside 0): the neighbour's upper end faces the tile
-      v[z] = hside ? hreg[z][0] : hreg[z][N - 1];
-      gg[z] = hside ? g0 : g1;
+      v[z] = htrace ? hreg[z][0] : (hside ? hreg[z][0] : hreg[z][N - 1]);
+      gg[z] = htrace ? hreg[z][1] : (hside ? g0 : g1);
     }
     l7_mass<N>(T, v, mv);
     l7_mass<N>(T, gg, mg);

@@ -225,16 +225,18 @@ def test_generic_pcg_callables_match_fused():
     assert relerr(host(x1), host(x2)) < 1e-9
 
 
-def test_slab_split_equals_full_on_one_gpu():
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+def test_slab_split_equals_full_on_one_gpu(k):
     """x-slab decomposition path (ghost layers + interior/boundary parts) on
     one GPU: slab contexts whose ghost buffers are filled by device copies
-    (standing in for the NCCL exchange) reproduce the single-context vmult."""
+    (standing in for the NCCL exchange) reproduce the single-context vmult.
+    k = 3..5: face-trace ghost payload (column kernel); k = 2: ghost cells."""
     import ctypes
     from paper_1607_01323_b200 import _lib
     from paper_1607_01323_b200.parallel import SlabPartition, slab_of
     from paper_1607_01323_b200.spaces import DeviceContext
     from paper_1607_01323_b200.operators import ctypes_ptr, _stream
-    ext, counts, k = ((0, 1),) * 3, (8, 4, 3), 4
+    ext, counts = ((0, 1),) * 3, (8, 4, 3)
     for nranks in (2, 3):
         for per in ((False, False, True), (True, False, True)):
             mesh = M.build_box_mesh(ext, counts, periodic=per, grading=(0.0, 0.9, 0.0))
