@@ -15,7 +15,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .mesh import BoxMesh, TAG_NAMES
+from .mesh import BoxMesh, TAG_NAMES, box_from_reference
 
 
 def _torch():
@@ -71,11 +71,32 @@ class DeviceContext:
 
 
 class DgSpace:
-    def __init__(self, mesh: BoxMesh, k: int, n_q_over=None):
+    """DG Q_k space (reference spaces.py:61-81) on a box mesh.
+
+    Drop-in for the reference's ``DgSpace(mesh, k)``: ``mesh`` may be this
+    package's BoxMesh or the reference's own ``Mesh`` object.  A reference
+    mesh that is an axis-aligned box (build_box_mesh) becomes the Cartesian
+    context (mesh.box_from_reference); any other reference mesh (curved,
+    cylinder, refined hierarchies) yields the general-geometry space
+    general.GeneralSpace2D, which the same operator calls dispatch on."""
+
+    def __new__(cls, mesh, k: int, n_q_over=None):
+        if not isinstance(mesh, BoxMesh) and hasattr(mesh, "elem_vertices"):
+            if box_from_reference(mesh) is None:
+                from .general import GeneralSpace2D
+                return GeneralSpace2D(mesh, k)
+        return super().__new__(cls)
+
+    def __init__(self, mesh, k: int, n_q_over=None):
         if k < 1:
             raise ValueError(f"polynomial degree must be >= 1, got k={k}")
         if k > 7:
             raise ValueError("the device path supports k <= 7")
+        if not isinstance(mesh, BoxMesh):
+            box = box_from_reference(mesh)
+            if box is None:
+                raise ValueError("DgSpace: not a box mesh (use general.GeneralSpace2D)")
+            mesh = box
         self.mesh = mesh
         self.dim = mesh.dim
         self.k = k

@@ -100,3 +100,25 @@ def map_tau_c(space, z, key):
         lut[(int(em), int(sm))] = t
         lut[(int(ep), int(sp))] = t
     return np.array([lut[(int(e), int(s))] for e, s in zip(space.f_em, space.f_sm)])
+
+
+MESHES = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref2d_meshes.npz")
+
+
+def reference_mesh(name):
+    """A reference-built Mesh (tests/golden/make_golden_meshes.py) as an
+    object with the reference Mesh's attribute names (pkg/src/dgins/mesh.py:
+    72-90): what a reference caller passes to DgSpace(mesh, k)."""
+    from types import SimpleNamespace
+    z = np.load(MESHES)
+    g = lambda f: z[f"{name}_{f}"]
+    return SimpleNamespace(
+        vertices=g("vertices"), elem_vertices=g("elem_vertices"),
+        geom_degree=int(g("geom_degree")), geom_nodes=g("geom_nodes"),
+        interior=SimpleNamespace(em=g("if_em"), sm=g("if_sm"), ep=g("if_ep"), sp=g("if_sp"),
+                                 flip=g("if_flip")),
+        boundary=SimpleNamespace(elem=g("bf_elem"), slot=g("bf_slot"), tag=g("bf_tag")),
+        tag_names=[str(t) for t in g("tag_names")],
+        periodic_spec={int(a): None for a in g("periodic_axes")},
+        periodic_pairs=[], curved={}, parent=None, quadrant=None, coarser=None,
+        n_elements=int(g("elem_vertices").shape[0]))
