@@ -114,15 +114,27 @@ def hbm_peak():
         return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
-def ncu_summary(k):
+def ncu_summary(k, kernel):
     """Committed ncu --set full summary of the headline vmult kernel at degree
-    k (profiles/ncu_laplace.json): kernel name, DRAM bytes per launch, fp64
-    instruction counts per DoF; {} if absent."""
+    k (profiles/ncu_laplace.json, written by profiles/r02/ncu_to_summary.py):
+    DRAM bytes per launch, fp64 instruction counts per DoF.  Used only if it
+    was captured on the kernel this run launches (``kernel`` =
+    dg_laplace_kernel_name); otherwise {} -- a stale capture is never reported."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_laplace.json")) as f:
-            return json.load(f).get(f"k{k}", {})
+            e = json.load(f).get(f"k{k}", {})
     except Exception:
         return {}
+    return e if e.get("kernel") == kernel else {}
+
+
+def fp64_peak_measured():
+    """Measured fp64 DFMA peak (profiles/fp64_peak.cu -> fp64_peak.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            return float(json.load(f)["dfma_tflops"]), "measured DFMA peak (profiles/fp64_peak.json)"
+    except Exception:
+        return None, None
 
 
 def oracle_sample(k, cells, threads_all):
@@ -181,22 +193,28 @@ def run_reference(args, rank, world):
 
 
 def cpu_baseline(k):
-    """Oracle port on 1 core, ~10-20 s of CPU work."""
-    try:
-        import threadpoolctl
-        threadpoolctl.threadpool_limits(1)
-    except Exception:
-        pass
+    """Oracle port (restated reference algorithm) on the host: 1 BLAS thread
+    (the reference tests' setting) and all host threads, ~10 s each."""
+    import threadpoolctl
     from oracle import dg_oracle as O
     cells = 24 if k <= 4 else 16
     sp, b, p = oracle_sample(k, cells, False)
-    reps, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < 10.0:
-        O.apply_pressure_laplace(sp, p, b)
-        reps += 1
-    dt = time.perf_counter() - t0
-    return {"value": p.size * reps / dt, "unit": "DoF/s", "cores": 1, "kind": "port",
-            "sample": f"{cells}^3 cells Q{k} walls vmult x {reps} (numpy port, 1 thread)"}
+    res = {}
+    for label, threads in (("one", 1), ("all", len(os.sched_getaffinity(0)))):
+        with threadpoolctl.threadpool_limits(threads):
+            O.apply_pressure_laplace(sp, p, b)
+            reps, t0 = 0, time.perf_counter()
+            while time.perf_counter() - t0 < 10.0:
+                O.apply_pressure_laplace(sp, p, b)
+                reps += 1
+            res[label] = (p.size * reps / (time.perf_counter() - t0), threads, reps)
+    v1, _, r1 = res["one"]
+    va, ca, ra = res["all"]
+    return {"value": v1, "unit": "DoF/s", "cores": 1, "kind": "port",
+            "sample": f"{cells}^3 cells Q{k} walls vmult x {r1} (numpy port, 1 thread)",
+            "all_cores": {"value": va, "unit": "DoF/s", "cores": ca,
+                          "sample": f"{cells}^3 cells Q{k} walls vmult x {ra} (numpy port, "
+                                    f"{ca} BLAS threads)"}}
 
 
 def run_c4_step(nsteps=5):
@@ -548,15 +566,22 @@ def main():
         cpu = cpu_baseline(k)
 
     if rank == 0:
+        import ctypes
         peak, peak_kind = hbm_peak()
         per_rank_dofs = nd
         achieved = per_rank_dofs * BYTES_PER_DOF / (ms_step * 1e-3) / 1e9
         clocks = clk.summary()
-        prof = ncu_summary(k)
+        kbuf = ctypes.create_string_buffer(128)
+        _lib.call("dg_laplace_kernel_name", op.ctx.handle, kbuf, 128)
+        kernel = kbuf.value.decode()
+        prof = ncu_summary(k, kernel)
         fma = FMA_PER_DOF.get(k + 1)
         flop = prof.get("flop_per_dof") or (2 * fma if fma else None)
         sm_mhz = clocks["sm_mhz"] or 1965.0
-        fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+        fp64_peak, fp64_kind = fp64_peak_measured()
+        if fp64_peak is None:
+            fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+            fp64_kind = "nominal 64 DFMA/clk/SM x 148 SMs x median SM clock"
         fp64_ach = per_rank_dofs * flop / (ms_step * 1e-3) / 1e12 if flop else None
         line = {
             "metric": "SIP Laplace vmult DoF/s (fp64)",
@@ -571,17 +596,22 @@ def main():
                        "l2": "inputs (8 B/DoF x dofs) larger than L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": prof.get("dram_bytes_per_launch") if n == 128 else None,
+                         "traffic": (prof.get("dram_bytes_per_launch") / world
+                                     if prof and n == 128 and world == 1 else None),
+                         "traffic_source": (prof.get("source") if prof else
+                                            "no ncu capture of this kernel committed"),
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_dof": BYTES_PER_DOF,
-                         "kernel": prof.get("kernel", "laplace_vmult_kernel")},
+                         "kernel": kernel},
             "fp64": {"flop_per_dof": flop,
-                     "flop_source": ("ncu sass dfma/dadd/dmul counts (profiles/ncu_laplace.json)"
+                     "fp64_inst_per_dof": prof.get("fp64_inst_per_dof"),
+                     "flop_source": ("ncu sass dfma/dadd/dmul counts of this kernel "
+                                     "(profiles/ncu_laplace.json)"
                                      if prof.get("flop_per_dof") else "model 2 x (7n + 18)"),
                      "achieved_tflops": fp64_ach,
-                     "peak_tflops_at_clock": fp64_peak,
+                     "peak_tflops": fp64_peak,
                      "frac": (fp64_ach / fp64_peak) if flop else None,
-                     "peak_kind": "nominal 64 DFMA/clk/SM x 148 SMs x median SM clock"},
+                     "peak_kind": fp64_kind},
             "gpu_launches": args.steps * (1 if world == 1 else 2),
             "clocks": clocks,
         }

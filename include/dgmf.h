@@ -361,6 +361,9 @@ int dg_halo_pack(dg_ctx *ctx, const double *src, double *send_lo,
 /* attach caller-owned device buffers holding the neighbours' layers; they
  * are read by subsequent vmults on the sides that have a remote neighbour */
 int dg_halo_attach(dg_ctx *ctx, const double *recv_lo, const double *recv_hi);
+/* identifier of the kernel dg_laplace_vmult launches on this context,
+ * "name<template args>" (bench / profile bookkeeping) */
+int dg_laplace_kernel_name(dg_ctx *ctx, char *buf, int len);
 /* part: 0 = all cells, 1 = cells not touching a ghost layer,
  *       2 = only cells touching a ghost layer (needs recv_* filled) */
 int dg_laplace_vmult_part(dg_ctx *ctx, const double *src, double *dst,

@@ -39,6 +39,7 @@ struct dg_ctx {
   double *d_red = nullptr;     // reduction partials (kRedBlocks) + scalars
   double *d_red3 = nullptr;    // 3 x kRedBlocks partials (sharded CG dots)
   double *d_hcell = nullptr;   // per-cell dual-weight factor hx hy hz / 8 (3D)
+  unsigned *d_counter = nullptr;  // work counter of the persistent warp-column kernel
   int halo_traces = 0;         // ghost layers carry face traces (column kernel)
   double *d_scal = nullptr;    // 16 device scalars
   double *h_scal = nullptr;    // pinned mirror

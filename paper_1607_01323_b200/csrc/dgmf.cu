@@ -1,5 +1,6 @@
 // C-ABI implementation of the B200 matrix-free DG library (include/dgmf.h).
 #include <cmath>
+#include <initializer_list>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -12,6 +13,7 @@
 #include "laplace6.cuh"
 #include "laplace7.cuh"
 #include "laplace8.cuh"
+#include "laplace9.cuh"
 #include "mg.cuh"
 #include "tables.h"
 #include "tensor.cuh"
@@ -268,6 +270,7 @@ int dg_ctx_destroy(dg_ctx *c) {
   cudaFree(c->d_axis);
   cudaFree(c->d_red3);
   cudaFree(c->d_hcell);
+  cudaFree(c->d_counter);
   for (int s = 0; s < 2; ++s) {
     cudaFree(c->d_ghost_tau[s]);
   }
@@ -333,6 +336,20 @@ static LapTab<N> lap_tab(const Basis1D &b) {
   return t;
 }
 
+// dg_laplace_kernel_name: when set, the launchers below record the kernel
+// they would launch ("name<template args>") instead of launching it
+static thread_local std::string *t_kname = nullptr;
+static std::string kname(const char *base, std::initializer_list<int> args) {
+  std::string s = std::string(base) + "<";
+  bool first = true;
+  for (int a : args) {
+    if (!first) s += ",";
+    s += std::to_string(a);
+    first = false;
+  }
+  return s + ">";
+}
+
 // z-range of cell layers [z0, z1) of the vmult being launched by this host
 // thread (the pipelined host-buffer path; z1 <= 0: whole mesh).  Thread-local,
 // so concurrent calls on other threads are unaffected.
@@ -369,6 +386,10 @@ static int ensure_cell_table(dg_ctx *c, cudaStream_t st) {
 template <int DIM, int N, int BX, int BY, int BZ, int EPI = kEpiStore>
 static int launch_laplace(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                           cudaStream_t st, const EpiArgs &ea = EpiArgs{}) {
+  if (t_kname) {
+    *t_kname = kname("laplace_vmult_kernel", {DIM, N, BX, BY, BZ, EPI});
+    return DG_OK;
+  }
   using C = LapCfg<DIM, N, BX, BY, BZ>;
   auto kern = laplace_vmult_kernel<DIM, N, BX, BY, BZ, EPI>;
   static bool attr = false;
@@ -477,6 +498,10 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
 template <int N, int BX, int BY, int BZ, int EPI>
 static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea) {
+  if (t_kname) {
+    *t_kname = kname("laplace6_kernel", {N, BX, BY, BZ, EPI});
+    return DG_OK;
+  }
   using C = Lap6Cfg<N, BX, BY, BZ>;
   auto kern = laplace6_kernel<N, BX, BY, BZ, EPI>;
   static bool attr = false;
@@ -497,6 +522,10 @@ static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau
 template <int N, int TX, int TY, int NRING, int MINB, bool STAGE = false>
 static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st) {
+  if (t_kname) {
+    *t_kname = kname("laplace7_kernel", {N, TX, TY, NRING, MINB, (int)STAGE});
+    return DG_OK;
+  }
   using C = Lap7Cfg<N, TX, TY, NRING>;
   auto kern = laplace7_kernel<N, TX, TY, NRING, MINB, STAGE>;
   static int nsm = 0, occ = 1;
@@ -530,6 +559,10 @@ static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau
 template <int N, int TX, int TY, int NRING, int MINB>
 static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st) {
+  if (t_kname) {
+    *t_kname = kname("laplace8_kernel", {N, TX, TY, NRING, MINB});
+    return DG_OK;
+  }
   using C = Lap8Cfg<N, TX, TY, NRING>;
   auto kern = laplace8_kernel<N, TX, TY, NRING, MINB>;
   static int nsm = 0, occ = 1;
@@ -559,6 +592,50 @@ static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau
   return DG_OK;
 }
 
+// warp-column kernel (laplace9.cuh): persistent CTAs, warps pull units
+// (tile x z-chunk) from a counter reset before the launch
+template <int N, int TX, int TY, int NRING, int WPB>
+static int launch_laplace9(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
+                           cudaStream_t st) {
+  if (t_kname) {
+    *t_kname = kname("laplace9_kernel", {N, TX, TY, NRING, WPB});
+    return DG_OK;
+  }
+  using C = Lap9Cfg<N, TX, TY, NRING, WPB>;
+  auto kern = laplace9_kernel<N, TX, TY, NRING, WPB>;
+  static int nsm = 0, occ = 1;
+  if (!nsm) {
+    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    int dev = 0;
+    DG_CUDA_CHECK(cudaGetDevice(&dev));
+    DG_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    DG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM));
+    if (occ < 1) occ = 1;
+  }
+  if (!c->d_counter) DG_CUDA_CHECK(cudaMalloc((void **)&c->d_counter, 64));
+  const Geo g = c->geo();
+  int zlo = 0, zhi = g.nz;
+  if (t_chunk.z1 > 0) {
+    zlo = t_chunk.z0;
+    zhi = t_chunk.z1;
+  }
+  const int ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY;
+  const int cols = ntx * nty, nz = zhi - zlo;
+  const int warps = nsm * occ * WPB;
+  const int want = (4 * warps + cols - 1) / cols;  // ~4 units per warp
+  int lc = std::max(4, (nz + want - 1) / want);
+  lc = std::min(std::min(lc, nz), C::LCMAX);
+  const int nch = (nz + lc - 1) / lc;
+  const int nunits = cols * nch;
+  const int grid = std::min(nsm * occ, (nunits + WPB - 1) / WPB);
+  DG_CUDA_CHECK(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), st));
+  kern<<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis), tau_scale,
+                                                    part, zlo, zhi, lc, ntx, nty, nunits,
+                                                    c->d_counter);
+  DG_LAUNCH_CHECK("laplace9_kernel");
+  return DG_OK;
+}
+
 // tile / ring configuration of the column kernel (DG_L7CFG: experiments)
 static int l7_cfg() {
   const char *e = getenv("DG_L7CFG");  // read per call: A/B within one process
@@ -572,7 +649,19 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
   const char *vv = getenv("DG_LAP_VARIANT");
   int variant = vv ? atoi(vv) : 0;
   // ghost layers in the trace format are read by the column kernels only
-  if (c->halo_traces && (c->mode[0] == kGhost || c->mode[1] == kGhost) && variant != 8) variant = 0;
+  if (c->halo_traces && (c->mode[0] == kGhost || c->mode[1] == kGhost) && variant != 8 && variant != 9)
+    variant = 0;
+  if (c->dim == 3 && variant == 9) {
+    const int cfg = l7_cfg();
+    if (c->n == 4) {
+      if (cfg == 1) return launch_laplace9<4, 2, 4, 3, 6>(c, src, dst, tau_scale, part, st);
+      return launch_laplace9<4, 2, 4, 2, 8>(c, src, dst, tau_scale, part, st);
+    }
+    if (c->n == 5) {
+      if (cfg == 1) return launch_laplace9<5, 2, 3, 3, 6>(c, src, dst, tau_scale, part, st);
+      return launch_laplace9<5, 2, 3, 2, 8>(c, src, dst, tau_scale, part, st);
+    }
+  }
   if (c->dim == 3 && variant == 8) {
     const int cfg = l7_cfg();
     if (c->n == 4) {
@@ -595,6 +684,7 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
       if (cfg == 1) return launch_laplace7<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
       if (cfg == 2) return launch_laplace7<5, 4, 4, 3, 2>(c, src, dst, tau_scale, part, st);
       if (cfg == 3) return launch_laplace7<5, 8, 4, 3, 1>(c, src, dst, tau_scale, part, st);
+      if (cfg == 4) return launch_laplace7<5, 4, 4, 4, 2>(c, src, dst, tau_scale, part, st);
     }
     if (c->n == 6 && cfg == 1) return launch_laplace7<6, 4, 4, 3, 1>(c, src, dst, tau_scale, part, st);
     if (c->n == 3) return launch_laplace7<3, 8, 4, 3, 2>(c, src, dst, tau_scale, part, st);
@@ -603,7 +693,9 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
   // depth and CTAs/SM measured per degree (profiles/r02/NOTES.md)
   if (c->dim == 3 && variant != 4 && variant != 6) {
     if (c->n == 4) return launch_laplace7<4, 4, 4, 4, 4>(c, src, dst, tau_scale, part, st);
-    if (c->n == 5) return launch_laplace7<5, 4, 4, 4, 2>(c, src, dst, tau_scale, part, st);
+    // Q4: the half-plane variant (laplace8.cuh, 8x4 tile, 10 warps) -- +3..7 %
+    // over laplace7<5,4,4,4,2> from 48^3 to 160^3 (profiles/r02/NOTES.md)
+    if (c->n == 5) return launch_laplace8<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
     if (c->n == 6) return launch_laplace7<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
   }
   if (c->dim == 3 && variant == 6 && c->n == 4)  // register-plane kernel at k = 3 (experiment)
@@ -820,6 +912,17 @@ int dg_laplace_vmult_part(dg_ctx *c, const double *src, double *dst, double tau_
       ((c->mode[0] == kGhost && !c->d_recv[0]) || (c->mode[1] == kGhost && !c->d_recv[1])))
     return inval("x-slab context: attach ghost layers (dg_halo_attach) first");
   return laplace_dispatch(c, src, dst, tau_scale, part, (cudaStream_t)stream);
+}
+
+int dg_laplace_kernel_name(dg_ctx *c, char *buf, int len) {
+  if (!c || !buf || len < 1) return inval("null argument");
+  std::string name;
+  t_kname = &name;
+  const int rc = laplace_dispatch(c, nullptr, nullptr, 1.0, 0, nullptr);
+  t_kname = nullptr;
+  if (rc) return rc;
+  std::snprintf(buf, (size_t)len, "%s", name.c_str());
+  return DG_OK;
 }
 
 int dg_dot(dg_ctx *c, const double *x, const double *y, int64_t n, double *out_dev,
