@@ -517,6 +517,14 @@ static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau
   return DG_OK;
 }
 
+// shortest z-chunk of the column kernels: each chunk re-reads the layers
+// below and above it, so short chunks only pay on meshes too small to fill
+// the GPU otherwise (DG_L7_LCMIN: experiments)
+static int l7_lcmin(int dflt) {
+  const char *e = getenv("DG_L7_LCMIN");
+  return e ? std::max(1, atoi(e)) : dflt;
+}
+
 // z-marching column kernel (laplace7.cuh): units = TX x TY tiles x z-chunks,
 // the chunk length chosen so that ~4 waves of CTAs fill the GPU
 template <int N, int TX, int TY, int NRING, int MINB, bool STAGE = false>
@@ -546,7 +554,7 @@ static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau
   const int ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY;
   const int cols = ntx * nty, nz = zhi - zlo;
   const int want = (4 * nsm * occ + cols - 1) / cols;  // chunks per column
-  int lc = std::max(8, (nz + want - 1) / want);
+  int lc = std::max(l7_lcmin(4), (nz + want - 1) / want);  // measured: 32^3 Q3 54 -> 78 GDoF/s
   lc = std::min(std::min(lc, nz), C::LCMAX);
   const int nch = (nz + lc - 1) / lc;
   kern<<<(unsigned)(cols * nch), C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis),
@@ -583,7 +591,7 @@ static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau
   const int ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY;
   const int cols = ntx * nty, nz = zhi - zlo;
   const int want = (4 * nsm * occ + cols - 1) / cols;
-  int lc = std::max(8, (nz + want - 1) / want);
+  int lc = std::max(l7_lcmin(8), (nz + want - 1) / want);
   lc = std::min(std::min(lc, nz), C::LCMAX);
   const int nch = (nz + lc - 1) / lc;
   kern<<<(unsigned)(cols * nch), C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis),
