@@ -46,6 +46,7 @@ struct dg_ctx {
   std::vector<double *> work;  // solver work vectors (n_dofs each)
   double *d_partials = nullptr;  // per-brick partial sums of the fused vmult epilogue
   int64_t partials_n = 0;
+  int64_t epi_nparts = 0;  // partial-sum slots written by the last fused-dot vmult
   double *d_hin = nullptr, *d_hout = nullptr;   // device staging of dg_laplace_vmult_host
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   double *d_ctab = nullptr;  // Laplace cell table (laplace6.cuh), built on first use

@@ -480,8 +480,23 @@ static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau
                            cudaStream_t st, const EpiArgs &ea = EpiArgs{});
 
 // fused-epilogue vmults for the CG / Chebyshev loop (default bricks, k = 2..5)
+template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore>
+static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
+                           cudaStream_t st, const EpiArgs &ea = EpiArgs{});
+
 static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, double tau_scale,
                                 int epi, const EpiArgs &ea, cudaStream_t st) {
+  c->epi_nparts = laplace_bricks(c);
+  // DG_EPI_COL=1: the column kernel's cooperative epilogue at Q4 (measured
+  // slower: C2 PCG 0.91 vs 0.57 ms per iteration -- a barrier per layer and
+  // the epilogue vectors streamed by one 320-thread CTA per SM); the v4
+  // bricks' 416-thread CTAs stream them better
+  static const bool col = getenv("DG_EPI_COL") != nullptr;
+  if (col && c->dim == 3 && c->n == 5 && c->n_cells >= 16384 && c->mode[0] != kGhost &&
+      c->mode[1] != kGhost) {
+    if (epi == kEpiCheb) return launch_laplace8<5, 8, 4, 4, 1, kEpiCheb>(c, src, dst, tau_scale, 0, st, ea);
+    if (epi == kEpiDot) return launch_laplace8<5, 8, 4, 4, 1, kEpiDot>(c, src, dst, tau_scale, 0, st, ea);
+  }
 #define DG_E(D, NN, X, Y, Z)                                                                     \
   if (c->dim == D && c->n == NN) {                                                               \
     if (epi == kEpiCheb) return launch_laplace<D, NN, X, Y, Z, kEpiCheb>(c, src, dst, tau_scale, 0, st, ea); \
@@ -564,15 +579,15 @@ static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau
 }
 
 // half-plane column kernel (laplace8.cuh)
-template <int N, int TX, int TY, int NRING, int MINB>
+template <int N, int TX, int TY, int NRING, int MINB, int EPI>
 static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
-                           cudaStream_t st) {
+                           cudaStream_t st, const EpiArgs &ea) {
   if (t_kname) {
-    *t_kname = kname("laplace8_kernel", {N, TX, TY, NRING, MINB});
+    *t_kname = kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI});
     return DG_OK;
   }
   using C = Lap8Cfg<N, TX, TY, NRING>;
-  auto kern = laplace8_kernel<N, TX, TY, NRING, MINB>;
+  auto kern = laplace8_kernel<N, TX, TY, NRING, MINB, EPI>;
   static int nsm = 0, occ = 1;
   if (!nsm) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -594,8 +609,13 @@ static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau
   int lc = std::max(l7_lcmin(8), (nz + want - 1) / want);
   lc = std::min(std::min(lc, nz), C::LCMAX);
   const int nch = (nz + lc - 1) / lc;
+  if (EPI == kEpiDot) {
+    if (4 * (int64_t)cols * nch > c->partials_n) return inval("laplace8 epilogue: partials buffer");
+    c->epi_nparts = (int64_t)cols * nch;
+  }
   kern<<<(unsigned)(cols * nch), C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis),
-                                                            tau_scale, part, zlo, zhi, lc, ntx, nty);
+                                                            tau_scale, part, zlo, zhi, lc, ntx, nty,
+                                                            ea);
   DG_LAUNCH_CHECK("laplace8_kernel");
   return DG_OK;
 }

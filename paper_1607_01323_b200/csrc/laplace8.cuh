@@ -44,11 +44,15 @@ __device__ __forceinline__ int l8_role(int w) {
   return w;
 }
 
-template <int N, int TX, int TY, int NRING, int MINB>
+// EPI: kEpiStore (out by TMA bulk stores) or a CG / Chebyshev epilogue
+// (laplace.cuh epi_store) applied cooperatively to each finished layer of
+// the tile; kEpiDot leaves one partial-sum triple per CTA in ea.partials.
+template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore>
 __global__ void __launch_bounds__(Lap8Cfg<N, TX, TY, NRING>::THREADS, MINB)
 laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g,
                 const __grid_constant__ LapTab<N> T, const double ts, const int part,
-                const int zlo, const int zhi, const int lc, const int ntx, const int nty) {
+                const int zlo, const int zhi, const int lc, const int ntx, const int nty,
+                const EpiArgs ea = EpiArgs{}) {
   using C = Lap8Cfg<N, TX, TY, NRING>;
   constexpr int NCT = C::NCT, NP = C::NP, CSTR = C::CSTR, H = N / 2, NE = (N + 1) / 2;
   constexpr int HO = H > 0 ? H : 1;
@@ -73,11 +77,16 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   const int x0 = tix * TX, y0 = tiy * TY;
   const int ex = min(TX, g.nx - x0), ey = min(TY, g.ny - y0);
   const int z0 = zlo + chunk * lc, z1 = min(zhi, z0 + lc);
-  if (z0 >= z1) return;
+  bool skip = z0 >= z1;
   if (part != 0) {
     const bool touches = (g.mode[0] == kGhost && x0 == 0) || (g.mode[1] == kGhost && x0 + ex == g.nx);
-    if ((part == 1 && touches) || (part == 2 && !touches)) return;
+    if ((part == 1 && touches) || (part == 2 && !touches)) skip = true;
   }
+  if (skip) {
+    if (EPI == kEpiDot && threadIdx.x < 3) ea.partials[(size_t)blockIdx.x * 4 + threadIdx.x] = 0.0;
+    return;
+  }
+  double eacc[3] = {0.0, 0.0, 0.0};  // kEpiDot partial sums of this CTA
   const int nlay = z1 - z0;
   const size_t nxy = (size_t)g.nx * g.ny;
 
@@ -468,9 +477,25 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
         }
       }
     }
-    if (tma) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (tma && EPI == kEpiStore) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();  // B_b: out complete in the slot
-    if (tma) {
+    if (EPI != kEpiStore) {
+      // epilogue on this layer's cells: out / Chebyshev vectors / partial sums
+      const double hzl = hz;
+      for (int i = tid; i < ex * ey * NP; i += C::THREADS) {
+        const int cl = i / NP, w = i - cl * NP;
+        const int xx = cl % ex, yy = cl / ex;
+        const size_t gi = ((size_t)x0 + xx + (size_t)g.nx * (y0 + yy) + nxy * iz) * NP + w;
+        double wq = 0.0;
+        if (EPI == kEpiDot) {
+          const int qx = w % N, qy = (w / N) % N, qz = w / N2;
+          wq = 0.5 * g.ax[0][4 * (x0 + xx)] * ea.wint[qx] * 0.5 * g.ax[1][4 * (y0 + yy)] *
+               ea.wint[qy] * 0.5 * hzl * ea.wint[qz];
+        }
+        epi_store<EPI, 3, N>(u, out, ea, gi, slot[(xx + TX * yy) * CSTR + w], wq, eacc);
+      }
+      __syncthreads();  // the slot is refilled by a later z phase
+    } else if (tma) {
       if (tid < 32) {
         const int nitem = (N & 1) ? ey : ex * ey;
         for (int i = tid; i < nitem; i += 32) {
@@ -490,7 +515,8 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       __syncthreads();
     }
   }
-  if (tid < 32 && tma) bulk_wait_read();
+  if (EPI == kEpiDot) epi_reduce(eacc, rbuf, ea, blockIdx.x);
+  if (tid < 32 && tma && EPI == kEpiStore) bulk_wait_read();
 }
 
 }  // namespace dg
