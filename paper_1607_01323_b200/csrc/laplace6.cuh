@@ -46,8 +46,9 @@ struct Lap6Cfg {
   // (16 cells, same slab index) hit distinct banks
   static constexpr int FSTR = 4 * LPC + 1;
   static constexpr int FBUF = NC * FSTR;
-  // x/z functionals live in buf0 and y functionals in buf1 whenever they fit
-  // (N >= 4; two extra barriers), else in their own regions
+  // whenever they fit (N >= 4): x functionals in buf1 (free until the G
+  // planes), y and z functionals in buf0 (its planes are in registers by
+  // then), the dot-product reduction scratch in fbz; else their own regions
   static constexpr bool FX_IN_BUF0 = FBUF <= BUF;
   static constexpr bool FY_IN_BUF1 = FBUF <= BUF;
   static constexpr int OFF_BUF1 = BUF;
@@ -69,6 +70,10 @@ struct Lap6Cfg {
   static constexpr int OFF_BAR = OFF_PTR + NSLOT;
   static constexpr int NDBL = OFF_BAR + 1;
   static constexpr size_t SMEM = sizeof(double) * (size_t)NDBL + sizeof(int) * NC * 6;
+  // the TMA row copies (PS == N*N) need 16-byte aligned shared addresses and
+  // sizes: cell-table rows, brick rows and the table offset in doubles even
+  static_assert(PS != N * N || (OFF_SIDE % 2 == 0 && (BX * SSTR) % 2 == 0 && (BX * NP) % 2 == 0),
+                "TMA alignment of the brick rows");
 };
 
 // The context's cell table (once per context, one thread per (cell, side) and
