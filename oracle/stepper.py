@@ -11,7 +11,11 @@ Helmholtz solve with inverse-mass preconditioning; solver initial guesses
 are order-J extrapolations (Section 5.1).  Built only from the
 oracle's operators and solvers (oracle/dg_oracle.py, oracle/multigrid.py),
 so each substep's parity with the device step reduces to the already
-pinned operators.  V2 (the HONS path) is not restated.
+pinned operators.  V2 (the HONS path, Eqs. 26-28 / SPEC.md
+advance_step): the convective step yields u^_dt = M^-1 conv, the Poisson
+right-hand side is the divergence of u^_dt alone (the 1/dt divergence of the
+BDF history is dropped), and u^ = dt/gamma0 u^_dt + sum alpha_i/gamma0 u^{n-i}
+is reconstructed for the projection.
 """
 
 from dataclasses import dataclass, field
@@ -34,12 +38,12 @@ def bdf_ex_constants(J):
     raise ValueError(f"unsupported BDF order J={J}")
 
 
-VARIANTS = ("VHW", "V1", "V3a", "V3b", "V3c", "V4")
+VARIANTS = ("VHW", "V1", "V2", "V3a", "V3b", "V3c", "V4")
 
 
 @dataclass
 class Variant:
-    """operators.py:31-75 (V2 excluded)."""
+    """operators.py:29-75."""
     variant: str = "V3c"
     zeta_d_star: float = 1.0
     zeta_c_star: float = 1.0
@@ -101,10 +105,17 @@ class VelocityCorrection:
         it = {}
         # (a) convective step (Eq. 37)
         conv = O.eval_convective_rhs(sp, bcs, hist_u[:J], be, times, t_np1, cfg.body_force)
-        uhat = sum(al[i] * hist_u[i] for i in range(J)) + dt * O.inverse_mass_apply(sp, conv)
-        uhat = uhat / g0
-        # (b) pressure Poisson (Eq. 38)
-        rhs = O.eval_divergence_rhs(sp, uhat, bcs, g0 / dt, cfg.variant.a_form)
+        if cfg.variant.variant == "V2":
+            # HONS (Eqs. 26-28): u^_dt (Eq. 26), Poisson rhs -div u^_dt (Eq. 27),
+            # u^ reconstructed from u^_dt and the BDF history (Eq. 28)
+            udt = O.inverse_mass_apply(sp, conv)
+            uhat = (dt / g0) * udt + sum((al[i] / g0) * hist_u[i] for i in range(J))
+            rhs = O.eval_divergence_rhs(sp, udt, bcs, 1.0, cfg.variant.a_form)
+        else:
+            uhat = sum(al[i] * hist_u[i] for i in range(J)) + dt * O.inverse_mass_apply(sp, conv)
+            uhat = uhat / g0
+            # (b) pressure Poisson (Eq. 38)
+            rhs = O.eval_divergence_rhs(sp, uhat, bcs, g0 / dt, cfg.variant.a_form)
         rhs = rhs + O.eval_pressure_neumann_rhs(sp, bcs, hist_u[:J], hist_w[:J], be, nu, t_np1,
                                                 cfg.body_force)
         rhs = rhs + O.gp_dirichlet_rhs(sp, bcs, t_np1, self.tau_scale)

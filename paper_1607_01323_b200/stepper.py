@@ -14,8 +14,10 @@ side and solver it is made of is a pinned row of this package:
 
 Solver initial guesses are order-J extrapolations (Section 5.1).
 Vectors are device tensors (element-major); per-substep fields and solver
-iteration counts are returned for parity checks and timing.  V2 (HONS) is
-not provided.
+iteration counts are returned for parity checks and timing.  V2 (HONS,
+PAPER.md Eqs. 26-28): (a) yields u^_dt = M^-1 conv, (b) takes the divergence
+of u^_dt alone (no 1/dt divergence of the BDF history), and u^ = dt/gamma0
+u^_dt + sum alpha_i/gamma0 u^{n-i} is reconstructed before (c).
 """
 
 import time
@@ -27,7 +29,7 @@ from . import solvers as sol
 from . import multigrid as MG
 from .spaces import _torch
 
-VARIANTS = ("VHW", "V1", "V3a", "V3b", "V3c", "V4")
+VARIANTS = ("VHW", "V1", "V2", "V3a", "V3b", "V3c", "V4")
 
 
 def bdf_ex_constants(J):
@@ -76,7 +78,7 @@ class VelocityCorrection:
 
     def __init__(self, mg_spaces, bc_spec, cfg: StepConfig, fused: bool = True):
         if cfg.variant.variant not in VARIANTS:
-            raise ValueError(f"unsupported variant {cfg.variant.variant!r} (V2 is not provided)")
+            raise ValueError(f"unsupported variant {cfg.variant.variant!r}")
         self.space = mg_spaces[-1]
         self.cfg, self.fused = cfg, fused
         self.bcs = bc_spec.resolve(self.space)
@@ -118,11 +120,19 @@ class VelocityCorrection:
         t0 = clock()
         # (a) convective step
         conv = ops.eval_convective_rhs(sp, bcs, hist_u[:J], be, times, t_np1, cfg.body_force)
-        uhat = sum(al[i] * hist_u[i] for i in range(J)) + dt * ops.inverse_mass_apply(sp, conv)
-        uhat = uhat / g0
+        v2 = cfg.variant.variant == "V2"
+        if v2:
+            udt = ops.inverse_mass_apply(sp, conv)
+            uhat = (dt / g0) * udt + sum((al[i] / g0) * hist_u[i] for i in range(J))
+        else:
+            uhat = sum(al[i] * hist_u[i] for i in range(J)) + dt * ops.inverse_mass_apply(sp, conv)
+            uhat = uhat / g0
         t0 = mark("convective", t0)
         # (b) pressure Poisson
-        rhs = ops.eval_divergence_rhs(sp, uhat, bcs, g0 / dt, cfg.variant.a_form)
+        if v2:
+            rhs = ops.eval_divergence_rhs(sp, udt, bcs, 1.0, cfg.variant.a_form)
+        else:
+            rhs = ops.eval_divergence_rhs(sp, uhat, bcs, g0 / dt, cfg.variant.a_form)
         if bcs.dirichlet:
             rhs = rhs + ops.eval_pressure_neumann_rhs(sp, bcs, hist_u[:J], hist_w[:J], be, nu,
                                                       t_np1, cfg.body_force)

@@ -90,7 +90,7 @@ def host(t):
 
 
 @pytest.mark.parametrize("name", list(CASES))
-@pytest.mark.parametrize("variant", ["V3c", "V4", "VHW"])
+@pytest.mark.parametrize("variant", ["V3c", "V4", "VHW", "V2"])
 @pytest.mark.parametrize("fused", [False, True])
 def test_two_steps_match_oracle(name, variant, fused):
     osp, ospec, gsp, gspec = setups(name)
