@@ -461,7 +461,13 @@ static int laplace_dispatch_f(dg_ctx *c, const float *src, float *dst, double ta
 
 // number of CTAs (bricks) of the default Laplace configuration: the size of
 // the kEpiDot partial-sum array
+// Q3 meshes of at most 2048 cells run the v4 kernel with one cell per CTA:
+// graph-replayed vmults at 4x2x2 / 8x4x4 / 16x8x8 cells take 4.6 / 4.7 / 5.1 us
+// against 5.6 / 6.9 / 6.9 us with 4x4x2 bricks (profiles/r02/small_ab.py)
+static bool tiny_q3(const dg_ctx *c) { return c->dim == 3 && c->n == 4 && c->n_cells <= 2048; }
+
 static int64_t laplace_bricks(const dg_ctx *c) {
+  if (tiny_q3(c)) return c->n_cells;
   int bx = 0, by = 0, bz = 1;
   if (c->dim == 3) {
     static const int B[9][3] = {{0, 0, 0}, {0, 0, 0}, {8, 4, 4}, {4, 4, 4}, {4, 4, 2},
@@ -504,6 +510,10 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
   }
   // v4 bricks here also for k = 4: its 416-thread CTAs stream the CG vectors of
   // the epilogue faster than the 96-thread register-plane CTAs
+  if (tiny_q3(c)) {
+    if (epi == kEpiCheb) return launch_laplace<3, 4, 1, 1, 1, kEpiCheb>(c, src, dst, tau_scale, 0, st, ea);
+    if (epi == kEpiDot) return launch_laplace<3, 4, 1, 1, 1, kEpiDot>(c, src, dst, tau_scale, 0, st, ea);
+  }
   DG_E(3, 3, 4, 4, 4) DG_E(3, 4, 4, 4, 2) DG_E(3, 5, 4, 2, 2) DG_E(3, 6, 2, 2, 1)
   DG_E(2, 3, 16, 8, 1) DG_E(2, 4, 16, 8, 1) DG_E(2, 5, 8, 8, 1) DG_E(2, 6, 8, 8, 1)
 #undef DG_E
@@ -670,6 +680,8 @@ static int l7_cfg() {
   return e ? atoi(e) : 0;
 }
 
+constexpr int64_t kSmallMesh = 16384;
+
 static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                             cudaStream_t st) {
   // DG_LAP_VARIANT (read per call, A/B experiments): 4 = v4 bricks, 6 = the
@@ -719,6 +731,11 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
   }
   // default 3D Q3-Q5: the z-marching column kernel (laplace7.cuh); tile, ring
   // depth and CTAs/SM measured per degree (profiles/r02/NOTES.md)
+  // small meshes (multigrid coarse levels): the column kernel's z march is a
+  // serial chain per CTA (a 16x8x8 level takes ~20 us at any tile), the v4
+  // bricks run all bricks at once (~9 us; profiles/r02/NOTES.md)
+  const bool traced = c->halo_traces && (c->mode[0] == kGhost || c->mode[1] == kGhost);
+  if (c->dim == 3 && variant == 0 && !traced && c->n_cells < kSmallMesh) variant = 4;
   if (c->dim == 3 && variant != 4 && variant != 6) {
     if (c->n == 4) return launch_laplace7<4, 4, 4, 4, 4>(c, src, dst, tau_scale, part, st);
     // Q4: the half-plane variant (laplace8.cuh, 8x4 tile, 10 warps) -- +3..7 %
@@ -729,6 +746,8 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
   if (c->dim == 3 && variant == 6 && c->n == 4)  // register-plane kernel at k = 3 (experiment)
     return launch_laplace6<4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
 
+  // tiny Q3 meshes (the coarsest multigrid levels): one cell per CTA
+  if (tiny_q3(c) && variant == 4) return launch_laplace<3, 4, 1, 1, 1>(c, src, dst, tau_scale, part, st);
   if (c->dim == 3) {
     switch (c->n) {
       case 2: return launch_laplace<3, 2, 8, 4, 4>(c, src, dst, tau_scale, part, st);

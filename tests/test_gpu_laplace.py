@@ -106,9 +106,24 @@ CASES_3D = [
 ]
 
 
+# "auto": the production dispatch (meshes this small run the v4 bricks, the
+# multigrid coarse-level rule); "column": DG_LAP_VARIANT=7 forces the z-marching
+# column kernels (laplace7 / laplace8) whatever the mesh size
+PATHS = {"auto": None, "column": "7"}
+
+
+@pytest.fixture(params=list(PATHS))
+def kernel_path(request, monkeypatch):
+    if PATHS[request.param] is None:
+        monkeypatch.delenv("DG_LAP_VARIANT", raising=False)
+    else:
+        monkeypatch.setenv("DG_LAP_VARIANT", PATHS[request.param])
+    return request.param
+
+
 @pytest.mark.parametrize("case", range(len(CASES_3D)))
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6, 7])
-def test_3d_laplace_matches_oracle(case, k):
+def test_3d_laplace_matches_oracle(case, k, kernel_path):
     ext, counts, per, kinds, grading = CASES_3D[case]
     osp, obcs, gsp, gbcs = oracle_and_gpu_3d(ext, counts, k, per, kinds, grading)
     np.testing.assert_allclose(gsp.ctx(gbcs.kinds).tau(), osp.tau_e, rtol=1e-13)
@@ -132,7 +147,7 @@ def test_3d_laplace_matches_oracle(case, k):
                   O.zero_mean_project_dual(osp, p).ravel()) < TOL
 
 
-def test_config1_vmult():
+def test_config1_vmult(kernel_path):
     """BASELINE config 1: 8^3 unit cube, Q3, walls, uniform[-1,1] seed 0 --
     both wall kinds (velocity-Dirichlet semantics and the NeumannBC kind
     that exercises the pressure-Dirichlet face branch)."""
@@ -159,7 +174,7 @@ BRICK_CASES = [
 
 @pytest.mark.parametrize("case", range(len(BRICK_CASES)))
 @pytest.mark.parametrize("k", [2, 3, 4, 5])
-def test_vmult_multibrick_matches_oracle(case, k):
+def test_vmult_multibrick_matches_oracle(case, k, kernel_path):
     counts, per, kind, grading = BRICK_CASES[case]
     kinds = {t: kind for t in O.TAG_NAMES}
     ext = ((0, 1), (0, 2), (0, 1))
