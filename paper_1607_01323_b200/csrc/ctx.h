@@ -56,6 +56,8 @@ struct dg_ctx {
   int64_t vwork_n = 0;
   double *d_vpart = nullptr;    // per-CTA partial sums of the vector-PCG update
   int64_t vpart_n = 0;
+  double *d_apdot = nullptr;    // per-CTA p.Ap partials of the vector-PCG operator
+  int64_t apdot_n = 0;
   std::mutex mu;
 
   dg::Geo geo() const {

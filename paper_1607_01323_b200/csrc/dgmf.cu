@@ -283,6 +283,7 @@ int dg_ctx_destroy(dg_ctx *c) {
   cudaFree(c->d_ctab);
   for (double *w : c->vwork) cudaFree(w);
   cudaFree(c->d_vpart);
+  cudaFree(c->d_apdot);
   delete c;
   return DG_OK;
 }

@@ -42,7 +42,8 @@ static int ensure_trc(dg_ctx *c, int64_t n) {
 
 template <int N, int OP>
 static int launch_vc(dg_ctx *c, const double *src, double *dst, double gamma0_dt, double nu,
-                     const double *tau_d, const double *tau_c, cudaStream_t st) {
+                     const double *tau_d, const double *tau_c, cudaStream_t st,
+                     double *pdot = nullptr) {
   using C = VlCfg<N>;
   static const VcTab<N> tab = vc_tab<N>(c->basis);  // depends on k only
   auto ktr = vl_trace_kernel<N, OP == kVcHelmholtz>;
@@ -67,7 +68,7 @@ static int launch_vc(dg_ctx *c, const double *src, double *dst, double gamma0_dt
     DG_LAUNCH_CHECK("vl_trace_kernel");
   }
   kap<<<grid, C::THREADS, C::SMEM, st>>>(src, c->d_trc, dst, g, tab, gamma0_dt, nu, tau_d, tau_c,
-                                          c->n_cells);
+                                          c->n_cells, pdot);
   DG_LAUNCH_CHECK("vl_apply_kernel");
   return DG_OK;
 }
@@ -87,6 +88,29 @@ int vcart_apply(dg_ctx *c, int op, const double *src, double *dst, double gamma0
     return op == kVcHelmholtz                                                                       \
                ? launch_vc<NN, kVcHelmholtz>(c, src, dst, gamma0_dt, nu, tau_d, tau_c, st)         \
                : launch_vc<NN, kVcProjection>(c, src, dst, gamma0_dt, nu, tau_d, tau_c, st);
+  switch (c->n) { DG_VC(2) DG_VC(3) DG_VC(4) DG_VC(5) DG_VC(6) DG_VC(7) DG_VC(8) }
+#undef DG_VC
+  return DG_ENOTSUP;
+}
+
+// the fast-path operator with the CG product: dst = A src and, per CTA of the
+// apply kernel, pdot[b] = sum of src . dst over its cells (deterministic);
+// *nparts = the number of CTAs.  DG_ENOTSUP where vcart_apply has no fast path.
+static int vcart_apply_dot(dg_ctx *c, int op, const double *src, double *dst, double gamma0_dt,
+                           double nu, const double *tau_d, const double *tau_c, double *pdot,
+                           int64_t *nparts, cudaStream_t st) {
+  static const bool generic = [] {
+    const char *v = getenv("DG_VEC_GENERIC");
+    return v && atoi(v) != 0;
+  }();
+  if (generic || c->dim != 3 || c->basis.nq != c->n) return DG_ENOTSUP;
+  if (src == dst) return inval("vector operator: src and dst must not alias");
+#define DG_VC(NN)                                                                                   \
+  case NN:                                                                                          \
+    *nparts = (c->n_cells + VlCfg<NN>::CPB - 1) / VlCfg<NN>::CPB;                                  \
+    return op == kVcHelmholtz                                                                       \
+               ? launch_vc<NN, kVcHelmholtz>(c, src, dst, gamma0_dt, nu, tau_d, tau_c, st, pdot)   \
+               : launch_vc<NN, kVcProjection>(c, src, dst, gamma0_dt, nu, tau_d, tau_c, st, pdot);
   switch (c->n) { DG_VC(2) DG_VC(3) DG_VC(4) DG_VC(5) DG_VC(6) DG_VC(7) DG_VC(8) }
 #undef DG_VC
   return DG_ENOTSUP;
@@ -161,6 +185,24 @@ static int launch_vpcg_update(dg_ctx *c, double *x, double *r, const double *p, 
   return DG_OK;
 }
 
+// the update kernel's per-CTA partial buffer (allocated outside any capture)
+static int vpcg_ensure_part(dg_ctx *c, int *nblocks) {
+  int64_t nb = 0;
+#define DG_U(NN) \
+  case NN: nb = (c->n_cells + VcCfg<NN>::CPB - 1) / VcCfg<NN>::CPB; break;
+  switch (c->n) { DG_U(2) DG_U(3) DG_U(4) DG_U(5) DG_U(6) DG_U(7) DG_U(8) default: return inval("unsupported degree"); }
+#undef DG_U
+  if (c->vpart_n < nb) {
+    cudaFree(c->d_vpart);
+    c->d_vpart = nullptr;
+    c->vpart_n = 0;
+    DG_CUDA_CHECK(cudaMalloc((void **)&c->d_vpart, sizeof(double) * (size_t)nb));
+    c->vpart_n = nb;
+  }
+  *nblocks = (int)nb;
+  return DG_OK;
+}
+
 static int vpcg_update(dg_ctx *c, double *x, double *r, const double *p, const double *Ap, double *z,
                        const double *scal, cudaStream_t st, int *nblocks) {
 #define DG_U(NN) \
@@ -192,13 +234,13 @@ extern "C" int dg_vector_pcg(dg_ctx *c, int op, double gamma0_dt, double nu, con
   double *r = c->vwork[0], *z = c->vwork[1], *p = c->vwork[2], *Ap = c->vwork[3];
   double *scal = c->d_scal + 10;  // [rz, pAp, rz_new]
   double *hs = c->h_scal + 10;
-  auto apply = [&](const double *src, double *dst) {
-    return op == 0 ? dg_helmholtz_vmult(c, src, dst, gamma0_dt, nu, stream)
-                   : dg_projection_vmult(c, src, dst, tau_d, tau_c, stream);
+  auto apply = [&](const double *src, double *dst, cudaStream_t s) {
+    return op == 0 ? dg_helmholtz_vmult(c, src, dst, gamma0_dt, nu, s)
+                   : dg_projection_vmult(c, src, dst, tau_d, tau_c, s);
   };
   const int gb = vgrid(n);
   // r = b - A x0 ; z = M^-1 r ; rz
-  if ((rc = apply(x, Ap))) return rc;
+  if ((rc = apply(x, Ap, st))) return rc;
   vpcg_sub_kernel<<<gb, 256, 0, st>>>(r, b, Ap, n);
   DG_LAUNCH_CHECK("vpcg_sub_kernel");
   if ((rc = dg_inverse_mass(c, r, z, 3, stream))) return rc;
@@ -221,20 +263,51 @@ extern "C" int dg_vector_pcg(dg_ctx *c, int op, double gamma0_dt, double nu, con
   if (hist) hist[0] = norm0;
   double norm = norm0;
   stats->residual = norm0;
-  if (norm0 <= tol) {
-    stats->converged = 1;
+  if (norm0 <= tol || max_iter == 0) {
+    stats->converged = norm0 <= tol;
     return DG_OK;
   }
   DG_CUDA_CHECK(cudaMemcpyAsync(p, z, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st));
-  for (int it = 1; it <= max_iter; ++it) {
-    if ((rc = apply(p, Ap))) return rc;
-    dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(p, Ap, n, c->d_red);
-    sum_partials_kernel<<<1, 1024, 0, st>>>(c->d_red, kRedBlocks, scal + 1);
+  // buffers of the loop body
+  {
+    const int64_t need = c->n_cells;  // >= CTAs of every fast-path apply
+    if (c->apdot_n < need) {
+      cudaFree(c->d_apdot);
+      c->d_apdot = nullptr;
+      c->apdot_n = 0;
+      DG_CUDA_CHECK(cudaMalloc((void **)&c->d_apdot, sizeof(double) * (size_t)std::max<int64_t>(need, 1)));
+      c->apdot_n = need;
+    }
+    int nb0 = 0;
+    if ((rc = vpcg_ensure_part(c, &nb0))) return rc;
+  }
+  // one iteration up to the new r.z: Ap = A p with p.Ap from the apply kernel
+  // (or a separate dot where the generic operator runs), the fused update;
+  // the partial sums are reduced in a fixed order
+  auto body = [&](cudaStream_t s) -> int {
+    int64_t np = 0;
+    int rc2 = vcart_apply_dot(c, op, p, Ap, gamma0_dt, nu, tau_d, tau_c, c->d_apdot, &np, s);
+    if (rc2 == DG_ENOTSUP) {
+      if ((rc2 = apply(p, Ap, s))) return rc2;
+      dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(p, Ap, n, c->d_red);
+      sum_partials_kernel<<<1, 1024, 0, s>>>(c->d_red, kRedBlocks, scal + 1);
+    } else if (rc2) {
+      return rc2;
+    } else {
+      sum_partials_kernel<<<1, 1024, 0, s>>>(c->d_apdot, (int)np, scal + 1);
+    }
     DG_LAUNCH_CHECK("dot");
     int nb = 0;
-    if ((rc = vpcg_update(c, x, r, p, Ap, z, scal, st, &nb))) return rc;
-    sum_partials_kernel<<<1, 1024, 0, st>>>(c->d_vpart, nb, scal + 2);
+    if ((rc2 = vpcg_update(c, x, r, p, Ap, z, scal, s, &nb))) return rc2;
+    sum_partials_kernel<<<1, 1024, 0, s>>>(c->d_vpart, nb, scal + 2);
     DG_LAUNCH_CHECK("sum_partials_kernel");
+    return DG_OK;
+  };
+  // host loop: the stop test reads pAp and r.z each iteration (a CUDA-graph
+  // loop with a device stop test measured no faster at ~0.4-0.6 ms per
+  // iteration and added graph set-up per solve)
+  for (int it = 1; it <= max_iter; ++it) {
+    if ((rc = body(st))) return rc;
     DG_CUDA_CHECK(cudaMemcpyAsync(hs + 1, scal + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     DG_CUDA_CHECK(cudaStreamSynchronize(st));
     const double pAp = hs[1];
@@ -263,4 +336,3 @@ extern "C" int dg_vector_pcg(dg_ctx *c, int op, double gamma0_dt, double nu, con
   }
   return DG_OK;
 }
-

@@ -83,11 +83,17 @@ struct VlGeo {
   int ix, iy, iz;
   double h[3], sc[3], det;
 };
+// cell coordinates by 32-bit division (cell counts < 2^31)
+__device__ __forceinline__ void vl_cell_xyz(const Geo &g, int64_t e, int &ix, int &iy, int &iz) {
+  const unsigned ei = (unsigned)e, nx = (unsigned)g.nx, ny = (unsigned)g.ny;
+  const unsigned q = ei / nx;
+  ix = (int)(ei - q * nx);
+  iz = (int)(q / ny);
+  iy = (int)(q - (unsigned)iz * ny);
+}
 __device__ __forceinline__ VlGeo vl_geo(const Geo &g, int64_t e) {
   VlGeo v;
-  v.ix = (int)(e % g.nx);
-  v.iy = (int)((e / g.nx) % g.ny);
-  v.iz = (int)(e / ((int64_t)g.nx * g.ny));
+  vl_cell_xyz(g, e, v.ix, v.iy, v.iz);
   v.h[0] = g.hx[v.ix];
   v.h[1] = g.hy[v.iy];
   v.h[2] = g.hz[v.iz];
@@ -156,11 +162,11 @@ vl_trace_kernel(const double *__restrict__ u, double *__restrict__ trc, const Ge
   double *cells = sm + C::TAB;
   const int64_t e0 = (int64_t)blockIdx.x * C::CPB;
   __shared__ double ssc[C::CPB][3];
-  for (int cs = threadIdx.x; cs < C::CPB; cs += blockDim.x) {
-    const VlGeo v = vl_geo(g, e0 + cs < ncells ? e0 + cs : 0);
-    ssc[cs][0] = v.sc[0];
-    ssc[cs][1] = v.sc[1];
-    ssc[cs][2] = v.sc[2];
+  if (threadIdx.x < 3 * C::CPB) {  // one thread per (cell, axis)
+    const int cs = threadIdx.x / 3, d = threadIdx.x - 3 * cs;
+    int ix, iy, iz;
+    vl_cell_xyz(g, e0 + cs < ncells ? e0 + cs : 0, ix, iy, iz);
+    ssc[cs][d] = 2.0 * (d == 0 ? g.hxi[ix] : (d == 1 ? g.hyi[iy] : g.hzi[iz]));
   }
   __syncthreads();
   auto emit = [&](int64_t e, int side, int c, int f, const double (&w)[N], double sd) {
@@ -206,7 +212,8 @@ __global__ void __launch_bounds__(VlCfg<N>::THREADS)
 vl_apply_kernel(const double *__restrict__ u, const double *__restrict__ trc,
                 double *__restrict__ out, const Geo g, const __grid_constant__ VcTab<N> tab,
                 const double gamma0_dt, const double nu, const double *__restrict__ tau_d,
-                const double *__restrict__ tau_c, const int64_t ncells) {
+                const double *__restrict__ tau_c, const int64_t ncells,
+                double *__restrict__ pdot = nullptr) {
   using C = VlCfg<N>;
   constexpr int F = C::F, NN = N * N;
   extern __shared__ double sm[];
@@ -219,22 +226,27 @@ vl_apply_kernel(const double *__restrict__ u, const double *__restrict__ trc,
   __shared__ int skind[C::CPB][6];
   __shared__ int64_t snbr[C::CPB][6];
   vc_stage_tab<N>(tb, tab);
-  for (int cs = threadIdx.x; cs < C::CPB; cs += blockDim.x) {
+  // one thread per (cell, side) for the side kinds / neighbours, one per cell
+  // for the geometry (all in the first warps, in parallel)
+  static_assert(7 * C::CPB <= C::THREADS, "setup: one pass");
+  if (threadIdx.x < 7 * C::CPB) {
+    const int cs = threadIdx.x / 7, side = threadIdx.x - 7 * cs;
     const int64_t e = e0 + cs < ncells ? e0 + cs : 0;
-    const VlGeo v = vl_geo(g, e);
-    sgeo[cs] = v;
-#pragma unroll
-    for (int side = 0; side < 6; ++side) {
+    if (side == 6) {
+      sgeo[cs] = vl_geo(g, e);
+    } else {
+      int ix, iy, iz;
+      vl_cell_xyz(g, e, ix, iy, iz);
       const int d = side >> 1, s = side & 1;
       const int nd = d == 0 ? g.nx : (d == 1 ? g.ny : g.nz);
-      int nidx = (d == 0 ? v.ix : (d == 1 ? v.iy : v.iz)) + (s ? 1 : -1);
+      int nidx = (d == 0 ? ix : (d == 1 ? iy : iz)) + (s ? 1 : -1);
       int k = 0;
       if (nidx < 0 || nidx >= nd) {
         const int m = g.mode[side];
         k = (m == kBndNone || m == kBndNeumann) ? m : 0;
         nidx = s ? 0 : nd - 1;  // periodic wrap
       }
-      const int cx = d == 0 ? nidx : v.ix, cy = d == 1 ? nidx : v.iy, cz = d == 2 ? nidx : v.iz;
+      const int cx = d == 0 ? nidx : ix, cy = d == 1 ? nidx : iy, cz = d == 2 ? nidx : iz;
       skind[cs][side] = k;
       snbr[cs][side] = cx + (int64_t)g.nx * (cy + (int64_t)g.ny * cz);
     }
@@ -251,7 +263,8 @@ vl_apply_kernel(const double *__restrict__ u, const double *__restrict__ trc,
       return fdet * W[f % N] * W[f / N];
     };
     // FA: jumps, averaged normal derivatives, w; projection: final value test
-    for (int it = threadIdx.x; it < C::CPB * 6 * F; it += blockDim.x) {
+    #pragma unroll
+    for (int it = threadIdx.x; it < C::CPB * 6 * F; it += C::THREADS) {
       const int cs = it / (6 * F), i = it % (6 * F);
       const int side = i / F, f = i % F, d = side >> 1, s = side & 1;
       const int64_t e = e0 + cs;
@@ -305,7 +318,8 @@ vl_apply_kernel(const double *__restrict__ u, const double *__restrict__ trc,
     __syncthreads();
     if (OP == kVcHelmholtz) {
       // FB: fluxes and test coefficients
-      for (int it = threadIdx.x; it < C::CPB * 6 * F; it += blockDim.x) {
+      #pragma unroll
+    for (int it = threadIdx.x; it < C::CPB * 6 * F; it += C::THREADS) {
         const int cs = it / (6 * F), i = it % (6 * F);
         const int side = i / F, f = i % F, d = side >> 1, s = side & 1;
         const int64_t e = e0 + cs;
@@ -360,7 +374,8 @@ vl_apply_kernel(const double *__restrict__ u, const double *__restrict__ trc,
       }
       __syncthreads();
       // FC: tangential-gradient tests of component d, transposed onto the face
-      for (int it = threadIdx.x; it < C::CPB * 6 * F; it += blockDim.x) {
+      #pragma unroll
+    for (int it = threadIdx.x; it < C::CPB * 6 * F; it += C::THREADS) {
         const int cs = it / (6 * F), i = it % (6 * F);
         const int side = i / F, f = i % F, d = side >> 1;
         const int fa = f % N, sl = f / N;
@@ -590,7 +605,8 @@ vl_apply_kernel(const double *__restrict__ u, const double *__restrict__ trc,
     vl_st<N>(cell + C::TT + a * C::CS + first, 1, o);
   }
   __syncthreads();
-  // y lines: S^T -> global
+  // y lines: S^T -> global (+ the CG product u . out of this line)
+  double dacc = 0.0;
   #pragma unroll
   for (int it = threadIdx.x; it < 3 * C::LINES; it += C::THREADS) {
     const int cs = it / (3 * NN), a = (it / NN) % 3, l = it % NN, x = l % N, z = l / N;
@@ -600,7 +616,26 @@ vl_apply_kernel(const double *__restrict__ u, const double *__restrict__ trc,
     double w[N], o[N];
     vl_ld<N>(cell + C::TT + a * C::CS + vl_idx<N>(x, 0, z), C::LS, w);
     vl_mat<N, true>(tab.S, w, o);
-    vl_st<N>(out + ((int64_t)a * ncells + e) * C::P + z * NN + x, N, o);
+    double *dst = out + ((int64_t)a * ncells + e) * C::P + z * NN + x;
+    vl_st<N>(dst, N, o);
+    if (pdot) {
+      const double *src = u + ((int64_t)a * ncells + e) * C::P + z * NN + x;
+#pragma unroll
+      for (int m = 0; m < N; ++m) dacc = fma(src[m * N], o[m], dacc);
+    }
+  }
+  if (pdot) {  // deterministic CTA sum -> pdot[blockIdx.x]
+    __shared__ double red[C::THREADS / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dacc += __shfl_xor_sync(0xffffffffu, dacc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < C::THREADS / 32; ++w) t += red[w];
+      pdot[blockIdx.x] = t;
+    }
   }
 }
 
