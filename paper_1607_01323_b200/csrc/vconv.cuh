@@ -29,11 +29,13 @@
 
 namespace dg {
 
-template <int N, int NQ>
+// TV / MB: threads per CTA and the CTAs per SM the register budget must
+// allow (0: the defaults below; other values are A/B experiments)
+template <int N, int NQ, int TV = 0, int MB = 0>
 struct CvCfg {
   static constexpr int NP = N * N * N, QP = NQ * NQ * NQ, FQ = NQ * NQ, FN = N * N;
-  static constexpr int T = QP <= 64 ? 64 : 128;
-  static constexpr int MINB = N >= 5 ? 3 : 4;  // CTAs per SM the register budget must allow
+  static constexpr int T = TV ? TV : (QP <= 64 ? 64 : 128);
+  static constexpr int MINB = MB ? MB : (N >= 5 ? 3 : 4);
   static constexpr int TAB = NQ;  // Gauss weights (runtime-indexed)
   static constexpr int mx(int a, int b) { return a > b ? a : b; }
   // regions (doubles)
@@ -77,6 +79,75 @@ __device__ __forceinline__ void cv_line(const double *tab, const double (&x)[Cc]
     y[r] = a;
   }
 }
+// Even-odd (flip-symmetric) form of an R x C matrix A with
+// A[R-1-r][C-1-c] = SIG A[r][c] (SIG = +1: the GLL -> Gauss interpolation S
+// and S^T; -1: the derivative D and D^T): with xs = x[c] + x[C-1-c],
+// xd = x[c] - x[C-1-c] (c < C/2), E = (A[r][c] + A[r][C-1-c]) / 2 and
+// O = (A[r][c] - A[r][C-1-c]) / 2, the rows r and R-1-r are ye +- yo with
+// ye = E xs (+ A[r][C/2] x[C/2]), yo = O xd: about half the FMAs of y = A x.
+template <int R, int C>
+struct EoTab {
+  static constexpr int RH = R / 2, CH = C / 2;
+  double E[RH > 0 ? RH : 1][CH > 0 ? CH : 1];
+  double O[RH > 0 ? RH : 1][CH > 0 ? CH : 1];
+  double Mc[RH > 0 ? RH : 1];  // A[r][C/2], odd C
+  double Mr[CH > 0 ? CH : 1];  // A[R/2][c], odd R
+  double MM;                   // A[R/2][C/2], odd R and C
+};
+
+template <int R, int C>
+static EoTab<R, C> eo_tab(const double *A) {  // A row-major R x C
+  EoTab<R, C> t{};
+  constexpr int RH = R / 2, CH = C / 2;
+  for (int r = 0; r < RH; ++r) {
+    for (int c = 0; c < CH; ++c) {
+      t.E[r][c] = 0.5 * (A[r * C + c] + A[r * C + C - 1 - c]);
+      t.O[r][c] = 0.5 * (A[r * C + c] - A[r * C + C - 1 - c]);
+    }
+    if (C & 1) t.Mc[r] = A[r * C + CH];
+  }
+  if (R & 1) {
+    for (int c = 0; c < CH; ++c) t.Mr[c] = A[RH * C + c];
+    if (C & 1) t.MM = A[RH * C + CH];
+  }
+  return t;
+}
+
+template <int R, int C, int SIG>
+__device__ __forceinline__ void eo_line(const EoTab<R, C> &t, const double (&x)[C], double (&y)[R]) {
+  constexpr int RH = R / 2, CH = C / 2;
+  double xs[CH > 0 ? CH : 1], xd[CH > 0 ? CH : 1];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    xs[c] = x[c] + x[C - 1 - c];
+    xd[c] = x[c] - x[C - 1 - c];
+  }
+#pragma unroll
+  for (int r = 0; r < RH; ++r) {
+    double ye = (C & 1) ? t.Mc[r] * x[CH] : 0.0, yo = 0.0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      ye = fma(t.E[r][c], xs[c], ye);
+      yo = fma(t.O[r][c], xd[c], yo);
+    }
+    y[r] = ye + yo;
+    y[R - 1 - r] = SIG > 0 ? ye - yo : yo - ye;
+  }
+  if (R & 1) {
+    double ym = (SIG > 0 && (C & 1)) ? t.MM * x[CH] : 0.0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) ym = fma(t.Mr[c], SIG > 0 ? xs[c] : xd[c], ym);
+    y[RH] = ym;
+  }
+}
+
+// the four 1D operators of the convective kernel in even-odd form
+template <int N, int NQ>
+struct CvEo {
+  EoTab<NQ, N> S, D;    // nodes -> Gauss points: values, derivatives
+  EoTab<N, NQ> St, Dt;  // their transposes (the tests)
+};
+
 template <int Cc>
 __device__ __forceinline__ void cv_load(const double *p, int stride, double (&x)[Cc]) {
 #pragma unroll
@@ -88,11 +159,11 @@ __device__ __forceinline__ void cv_store(double *p, int stride, const double (&y
   for (int r = 0; r < R; ++r) p[r * stride] = y[r];
 }
 
-template <int N, int NQ>
-__global__ void __launch_bounds__(CvCfg<N, NQ>::T, CvCfg<N, NQ>::MINB)
+template <int N, int NQ, int TV = 0, int MB = 0>
+__global__ void __launch_bounds__(CvCfg<N, NQ, TV, MB>::T, CvCfg<N, NQ, TV, MB>::MINB)
 vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ QuadTab<N, NQ> tab,
-             const VecParams prm, const int64_t ncells) {
-  using C = CvCfg<N, NQ>;
+             const __grid_constant__ CvEo<N, NQ> eo, const VecParams prm, const int64_t ncells) {
+  using C = CvCfg<N, NQ, TV, MB>;
   constexpr int NP = C::NP, QP = C::QP, FQ = C::FQ, FN = C::FN, T = C::T;
   constexpr int NQ2 = NQ * NQ;
   extern __shared__ double sm[];
@@ -100,7 +171,6 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
   __shared__ double p_beta[kMaxHist];
   __shared__ int kind[6];
   __shared__ int64_t nbr[6];
-  const double *S = tab.S, *D = tab.D;
   double *W = sm;
   double *su = sm + C::U, *so = sm + C::OUT, *snb = sm + C::NB, *ra = sm + C::RA, *rb = sm + C::RB;
   const int tid = threadIdx.x;
@@ -159,7 +229,7 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
     for (int l = tid; l < 3 * N * N; l += T) {  // x lines: x1[c][z][y][qx]
       double xi[N], yo[NQ];
       cv_load<N>(su + l * N, 1, xi);
-      cv_line<NQ, N, N, false>(S, xi, yo);
+      eo_line<NQ, N, 1>(eo.S, xi, yo);
       cv_store<NQ>(x1 + l * NQ, 1, yo);
     }
     __syncthreads();
@@ -167,7 +237,7 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
       const int cz = l / NQ, qx = l % NQ;
       double xi[N], yo[NQ];
       cv_load<N>(x1 + cz * N * NQ + qx, NQ, xi);
-      cv_line<NQ, N, N, false>(S, xi, yo);
+      eo_line<NQ, N, 1>(eo.S, xi, yo);
       cv_store<NQ>(x2 + cz * NQ2 + qx, NQ, yo);
     }
     __syncthreads();
@@ -176,7 +246,7 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
       const int c = l / NQ2, qxy = l % NQ2;
       double xi[N], yo[NQ];
       cv_load<N>(x2 + c * N * NQ2 + qxy, NQ2, xi);
-      cv_line<NQ, N, N, false>(S, xi, yo);
+      eo_line<NQ, N, 1>(eo.S, xi, yo);
       cv_store<NQ>(ra + c * QP + qxy, NQ2, yo);
     }
     __syncthreads();
@@ -195,8 +265,8 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
       cv_load<NQ>(ra + b * QP + qxy, NQ2, ub);
 #pragma unroll
       for (int q = 0; q < NQ; ++q) gz[q] = ua[q] * ub[q] * (wxy * tab.w[q]);
-      if (dz) cv_line<N, NQ, N, true>(D, gz, zo);
-      else cv_line<N, NQ, N, true>(S, gz, zo);
+      if (dz) eo_line<N, NQ, -1>(eo.Dt, gz, zo);
+      else eo_line<N, NQ, 1>(eo.St, gz, zo);
       // destination (r, t) = test direction t for component r: dz -> (a, 2);
       // S jobs: 0 (0,0) 1 (1,1) 3 (0,1)+(1,0) 5 (2,0) 7 (2,1)
       const int r = dz ? a : (job == 5 || job == 7 ? 2 : a);
@@ -220,9 +290,9 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
       cv_load<NQ>(zb, NQ, z0);
       cv_load<NQ>(zb + N * NQ2, NQ, z1);
       cv_load<NQ>(zb + 2 * N * NQ2, NQ, z2);
-      cv_line<N, NQ, N, true>(S, z2, ya);
-      cv_line<N, NQ, N, true>(D, z1, yd);
-      cv_line<N, NQ, N, true>(S, z0, yb);
+      eo_line<N, NQ, 1>(eo.St, z2, ya);
+      eo_line<N, NQ, -1>(eo.Dt, z1, yd);
+      eo_line<N, NQ, 1>(eo.St, z0, yb);
 #pragma unroll
       for (int y = 0; y < N; ++y) ya[y] += yd[y];
       cv_store<N>(ra + ((a * 2 + 0) * N + z) * N * NQ + qx, NQ, ya);
@@ -235,8 +305,8 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
       double xa[NQ], xb[NQ], oa[N], ob[N];
       cv_load<NQ>(ra + ((a * 2 + 0) * N * N + zy) * NQ, 1, xa);
       cv_load<NQ>(ra + ((a * 2 + 1) * N * N + zy) * NQ, 1, xb);
-      cv_line<N, NQ, N, true>(S, xa, oa);
-      cv_line<N, NQ, N, true>(D, xb, ob);
+      eo_line<N, NQ, 1>(eo.St, xa, oa);
+      eo_line<N, NQ, -1>(eo.Dt, xb, ob);
       double *o = so + a * NP + zy * N;
 #pragma unroll
       for (int x = 0; x < N; ++x) o[x] += oa[x] + ob[x];
@@ -250,7 +320,7 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
       double xi[N], yo[NQ];
       if (o == 0) cv_load<N>(su + c * NP + cv_end_node<N>(d, side & 1, sl, 0), d == 0 ? N : 1, xi);
       else cv_load<N>(snb + (side * 3 + c) * FN + sl * N, 1, xi);
-      cv_line<NQ, N, N, false>(S, xi, yo);
+      eo_line<NQ, N, 1>(eo.S, xi, yo);
       cv_store<NQ>(ra + l * NQ, 1, yo);
     }
     __syncthreads();
@@ -259,7 +329,7 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
       const int osc = l / NQ, qfa = l % NQ;
       double xi[N], yo[NQ];
       cv_load<N>(ra + osc * N * NQ + qfa, NQ, xi);
-      cv_line<NQ, N, N, false>(S, xi, yo);
+      eo_line<NQ, N, 1>(eo.S, xi, yo);
       cv_store<NQ>(rb + osc * FQ + qfa, NQ, yo);
     }
     __syncthreads();
@@ -302,7 +372,7 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
     for (int l = tid; l < 18 * NQ; l += T) {
       double xi[NQ], yo[N];
       cv_load<NQ>(vf + l * NQ, 1, xi);
-      cv_line<N, NQ, N, true>(S, xi, yo);
+      eo_line<N, NQ, 1>(eo.St, xi, yo);
       cv_store<N>(ra + l * N, 1, yo);
     }
     __syncthreads();
@@ -311,7 +381,7 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
       const int sa = l / N, fa = l % N;
       double xi[NQ], yo[N];
       cv_load<NQ>(ra + sa * NQ * N + fa, N, xi);
-      cv_line<N, NQ, N, true>(S, xi, yo);
+      eo_line<N, NQ, 1>(eo.St, xi, yo);
       cv_store<N>(rb + sa * FN + fa, N, yo);
     }
     __syncthreads();
@@ -341,7 +411,7 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
       double xi[NQ], yo[N];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) xi[q] = fd[q * NQ2] * (wxy * tab.w[q]);
-      cv_line<N, NQ, N, true>(S, xi, yo);
+      eo_line<N, NQ, 1>(eo.St, xi, yo);
       cv_store<N>(rb + a * N * NQ2 + qxy, NQ2, yo);
     }
     __syncthreads();
@@ -349,14 +419,14 @@ vconv_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Quad
       const int az = l / NQ, qx = l % NQ;
       double xi[NQ], yo[N];
       cv_load<NQ>(rb + az * NQ2 + qx, NQ, xi);
-      cv_line<N, NQ, N, true>(S, xi, yo);
+      eo_line<N, NQ, 1>(eo.St, xi, yo);
       cv_store<N>(ra + az * N * NQ + qx, NQ, yo);
     }
     __syncthreads();
     for (int l = tid; l < 3 * N * N; l += T) {
       double xi[NQ], yo[N];
       cv_load<NQ>(ra + l * NQ, 1, xi);
-      cv_line<N, NQ, N, true>(S, xi, yo);
+      eo_line<N, NQ, 1>(eo.St, xi, yo);
       double *o = so + l * N;
 #pragma unroll
       for (int x = 0; x < N; ++x) o[x] += yo[x];
