@@ -80,6 +80,10 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ const double *p_hist[kMaxHist], *p_gh[kMaxHist][6];
   __shared__ double p_beta[kMaxHist];
+  // side kinds / neighbour cells of the items two apart share a slot: slot
+  // (w & 1) holds item w's, written by threads 0-5 during item w - 2 (w >= 2)
+  __shared__ int skind[2][6];
+  __shared__ int64_t snbr[2][6];
   double *W = sm;
   double *so = sm + C::OUT, *snb = sm + C::NB, *ra = sm + C::RA, *rb = sm + C::RB;
   const int tid = threadIdx.x;
@@ -102,11 +106,21 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
   }
   __syncthreads();
 
+  // item w = k nh + lev: cell blockIdx.x + k gridDim.x, history level lev
   auto item_cell = [&](int64_t w) { return (int64_t)blockIdx.x + (w / nh) * gridDim.x; };
+  auto side_info = [&](int64_t w) {  // threads 0-5
+    if (tid < 6) {
+      int ix, iy, iz;
+      cv2_xyz(g, item_cell(w), ix, iy, iz);
+      int64_t nb;
+      skind[w & 1][tid] = cv2_side(g, ix, iy, iz, tid, nb);
+      snbr[w & 1][tid] = nb;
+    }
+  };
   // TMA of item w's own cell into buffer w & 1 (one thread)
   auto issue_own = [&](int64_t w) {
     const int64_t e = item_cell(w);
-    const double *src = p_hist[(int)(w % nh)];
+    const double *src = p_hist[(int)(w % nh)];  // one thread, once per item
     double *dst = sm + ((w & 1) ? C::SU1 : C::SU0);
     uint64_t *bar = &bars[w & 1];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -116,20 +130,17 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
       bulk_g2s(dst + c * NP, src + ((int64_t)c * ncells + e) * NP, (uint32_t)(NP * sizeof(double)), bar);
   };
   // neighbour end-layer values of item w held by this thread
-  auto load_nbr = [&](int64_t w, double (&nv)[KNB]) {
-    const int64_t e = item_cell(w);
-    const double *src = p_hist[(int)(w % nh)];
-    int ix, iy, iz;
-    cv2_xyz(g, e, ix, iy, iz);
+  auto load_nbr = [&](int64_t w, int lv, double (&nv)[KNB]) {
+    const double *src = p_hist[lv];
+    const int sl = (int)(w & 1);
 #pragma unroll
     for (int j = 0; j < KNB; ++j) {
       const int i = tid + j * T;
       double v = 0.0;
       if (i < 18 * FN) {
         const int side = i / (3 * FN), c = (i / FN) % 3, f = i % FN;
-        int64_t nb;
-        if (cv2_side(g, ix, iy, iz, side, nb) == 0)
-          v = src[((int64_t)c * ncells + nb) * NP +
+        if (skind[sl][side] == 0)
+          v = src[((int64_t)c * ncells + snbr[sl][side]) * NP +
                   cv_end_node<N>(side >> 1, (side & 1) ^ 1, f / N, f % N)];
       }
       nv[j] = v;
@@ -143,25 +154,29 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
     }
   };
 
-  // prologue: item 0
+  // prologue: item 0 (own cell, neighbour layers), side info of items 0, 1
   if (tid == 0) issue_own(0);
+  side_info(0);
+  if (nitems > 1) side_info(1);
+  __syncthreads();
   {
     double nv[KNB];
-    load_nbr(0, nv);
+    load_nbr(0, 0, nv);
     park_nbr(nv);
   }
   __syncthreads();
 
+  int64_t e = blockIdx.x;
+  int lev = 0;
   for (int64_t w = 0; w < nitems; ++w) {
-    const int64_t e = item_cell(w);
-    const int lev = (int)(w % nh);
     const double beta = p_beta[lev];
     const bool has_next = w + 1 < nitems;
+    const int lev_next = lev + 1 == nh ? 0 : lev + 1;
     if (has_next && tid == 0) issue_own(w + 1);
     double nv[KNB];
-    if (has_next) load_nbr(w + 1, nv);
+    if (has_next) load_nbr(w + 1, lev_next, nv);
     int ix, iy, iz;
-    cv2_xyz(g, e, ix, iy, iz);
+    cv2_xyz(g, e, ix, iy, iz);  // 32-bit divisions, once per item
     const double h[3] = {g.hx[ix], g.hy[iy], g.hz[iz]};
     const double sc[3] = {2.0 * g.hxi[ix], 2.0 * g.hyi[iy], 2.0 * g.hzi[iz]};
     const double det = 0.125 * h[0] * h[1] * h[2];
@@ -282,8 +297,7 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
     double *vf = ra;
     for (int i = tid; i < 6 * FQ; i += T) {
       const int side = i / FQ, f = i % FQ, d = side >> 1, s = side & 1;
-      int64_t nbdummy;
-      const int k = cv2_side(g, ix, iy, iz, side, nbdummy);
+      const int k = skind[w & 1][side];
       const double nsgn = s ? 1.0 : -1.0;
       const double fdet = d == 0 ? 0.25 * h[1] * h[2] : (d == 1 ? 0.25 * h[0] * h[2] : 0.25 * h[0] * h[1]);
       const double sj = fdet * W[f % NQ] * W[f / NQ];
@@ -332,21 +346,18 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
       cv_store<N>(ra + sa * FN + fa, N, yo);
     }
     __syncthreads();
-    // gather the lifted sides onto the end nodes
-    for (int i = tid; i < 3 * NP; i += T) {
-      const int a = i / NP, r = i % NP;
-      const int x = r % N, y = (r / N) % N, z = r / (N * N);
-      double add = 0.0;
-      if (x == 0) add += ra[(0 * 3 + a) * FN + z * N + y];
-      if (x == N - 1) add += ra[(1 * 3 + a) * FN + z * N + y];
-      if (y == 0) add += ra[(2 * 3 + a) * FN + z * N + x];
-      if (y == N - 1) add += ra[(3 * 3 + a) * FN + z * N + x];
-      if (z == 0) add += ra[(4 * 3 + a) * FN + y * N + x];
-      if (z == N - 1) add += ra[(5 * 3 + a) * FN + y * N + x];
-      so[i] += add;
+    // add the lifted sides onto their end nodes, one axis at a time (the two
+    // sides of an axis touch disjoint nodes; edges / corners get one side per
+    // phase)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      for (int i = tid; i < 6 * FN; i += T) {  // [s][a][sl][fa]
+        const int sa = i / FN, f = i % FN, s = sa / 3, a = sa % 3;
+        const int side = 2 * d + s;
+        so[a * NP + cv_end_node<N>(d, s, f / N, f % N)] += ra[(side * 3 + a) * FN + f];
+      }
+      __syncthreads();
     }
-    __syncthreads();
-
     if (lev == nh - 1) {
       if (prm.vol_data != nullptr) {
         // (v, f) with the body force at the quadrature points, z, y, x
@@ -383,7 +394,14 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
         const int c = i / NP, o = i % NP;
         out[((int64_t)c * ncells + e) * NP + o] = so[i];
       }
-      __syncthreads();  // so is rewritten by the next cell's first level
+    }
+    // side info of item w + 2 into this item's slot (read by the LF phase
+    // above and by the prefetch at the start of this item: both done)
+    if (w + 2 < nitems) side_info(w + 2);
+    __syncthreads();  // so / skind are rewritten by the next items
+    if (++lev == nh) {
+      lev = 0;
+      e += gridDim.x;
     }
   }
 }
