@@ -4,11 +4,10 @@
 // * one CTA per SM slot loops over cells (e = blockIdx.x + k gridDim.x) and
 //   over the history levels of each cell; the own-cell nodal values of the
 //   NEXT (cell, level) item are fetched by TMA bulk copies into the second of
-//   two buffers while the current item is computed, the neighbours' end
-//   layers of the next item are loaded into registers at the start of the
-//   current item and parked in shared memory once the current item's face
-//   sweep has consumed its own -- the one-CTA-per-cell kernel stalled on
-//   exactly these loads at the start of every cell;
+//   two buffers while the current item is computed, and the neighbours' end
+//   layers of the next item by cp.async into a second shared buffer -- the
+//   one-CTA-per-cell kernel stalled on exactly these loads at the start of
+//   every cell;
 // * lines that one thread writes (reads) contiguously and its neighbours
 //   read (write) across use an odd pitch NQ + 1, so the line-per-thread
 //   phases are free of the 8-way shared-memory bank conflicts of pitch NQ;
@@ -19,27 +18,27 @@
 
 namespace dg {
 
-template <int N, int NQ>
+template <int N, int NQ, int TV = 0, int MB = 0>
 struct Cv2Cfg {
   static constexpr int NP = N * N * N, QP = NQ * NQ * NQ, FQ = NQ * NQ, FN = N * N;
-  static constexpr int T = QP <= 64 ? 64 : 128;
-  static constexpr int MINB = N >= 5 ? 3 : 4;
+  static constexpr int T = TV ? TV : (QP <= 64 ? 64 : 128);
+  static constexpr int MINB = MB ? MB : (N >= 5 ? 3 : 4);
   static constexpr int P1 = NQ + 1;  // odd pitch of NQ-long lines
   static constexpr int mx(int a, int b) { return a > b ? a : b; }
   static constexpr int WR = (NQ + 1) & ~1;        // Gauss weights (keeps the TMA buffers 16 B aligned)
   static constexpr int SU0 = WR, SU1 = SU0 + 3 * NP;  // own nodal cell, two buffers
   static constexpr int OUT = SU1 + 3 * NP;        // accumulator
-  static constexpr int NB = OUT + 3 * NP;         // neighbour end layers [side][c][sl][fa]
-  static constexpr int RA = NB + 18 * FN;
-  // RA: x1 (3 N N P1) | u_q (3 QP) | A, B (6 N N P1) | fast sweep (36 N P1) |
-  //     LF values (18 NQ P1) | lift 2 (18 FN) | body force (3 N N P1)
-  static constexpr int SZA = mx(mx(3 * QP, 6 * N * N * P1), mx(36 * N * P1, 18 * NQ * P1));
+  static constexpr int NB = OUT + 3 * NP;         // neighbour end layers [2][side][c][sl][fa]
+  static constexpr int RA = NB + 36 * FN;
+  // RA: x1 (3 N N P1) | u_q (3 QP) | A, B (6 N N P1) | traces (36 FQ) |
+  //     lift 1 (18 NQ N) | body force (3 N N P1)
+  static constexpr int SZA = mx(mx(3 * QP, 6 * N * N * P1), 36 * FQ);
   static constexpr int RB = RA + SZA;
-  // RB: x2 (3 N NQ NQ) | Z (9 N NQ NQ) | traces (36 FQ) | lift 1 (18 NQ N) | body force
-  static constexpr int SZB = mx(9 * N * FQ, 36 * FQ);
+  // RB: x2 (3 N NQ NQ) | Z (9 N NQ NQ) | fast sweep (36 N P1) | LF values
+  //     (18 NQ P1) | body force (3 N NQ NQ)
+  static constexpr int SZB = mx(9 * N * FQ, mx(36 * N * P1, 18 * NQ * P1));
   static constexpr int NDBL = RB + SZB;
   static constexpr size_t SMEM = sizeof(double) * NDBL;
-  static constexpr int KNB = (18 * FN + T - 1) / T;  // neighbour values per thread
   static_assert((SU0 % 2) == 0 && (NP % 2) == 0, "TMA destinations 16 B aligned");
 };
 
@@ -61,6 +60,13 @@ __device__ __forceinline__ int cv2_side(const Geo &g, int ix, int iy, int iz, in
   return k;
 }
 
+// 8-byte asynchronous global -> shared copy (zero fill when !valid)
+__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+
 __device__ __forceinline__ void cv2_xyz(const Geo &g, int64_t e, int &ix, int &iy, int &iz) {
   const unsigned ei = (unsigned)e, nx = (unsigned)g.nx, ny = (unsigned)g.ny;
   const unsigned q = ei / nx;
@@ -69,13 +75,13 @@ __device__ __forceinline__ void cv2_xyz(const Geo &g, int64_t e, int &ix, int &i
   iy = (int)(q - (unsigned)iz * ny);
 }
 
-template <int N, int NQ>
-__global__ void __launch_bounds__(Cv2Cfg<N, NQ>::T, Cv2Cfg<N, NQ>::MINB)
+template <int N, int NQ, int TV = 0, int MB = 0>
+__global__ void __launch_bounds__(Cv2Cfg<N, NQ, TV, MB>::T, Cv2Cfg<N, NQ, TV, MB>::MINB)
 vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ QuadTab<N, NQ> tab,
               const __grid_constant__ CvEo<N, NQ> eo, const VecParams prm, const int64_t ncells) {
-  using C = Cv2Cfg<N, NQ>;
+  using C = Cv2Cfg<N, NQ, TV, MB>;
   constexpr int NP = C::NP, QP = C::QP, FQ = C::FQ, FN = C::FN, T = C::T, P1 = C::P1;
-  constexpr int NQ2 = NQ * NQ, KNB = C::KNB;
+  constexpr int NQ2 = NQ * NQ;
   extern __shared__ __align__(16) double sm[];
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ const double *p_hist[kMaxHist], *p_gh[kMaxHist][6];
@@ -85,7 +91,7 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
   __shared__ int skind[2][6];
   __shared__ int64_t snbr[2][6];
   double *W = sm;
-  double *so = sm + C::OUT, *snb = sm + C::NB, *ra = sm + C::RA, *rb = sm + C::RB;
+  double *so = sm + C::OUT, *ra = sm + C::RA, *rb = sm + C::RB;
   const int tid = threadIdx.x;
   const int nh = prm.n_hist;
   const int64_t ncta = (ncells - blockIdx.x + gridDim.x - 1) / gridDim.x;  // cells of this CTA
@@ -129,41 +135,29 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
     for (int c = 0; c < 3; ++c)
       bulk_g2s(dst + c * NP, src + ((int64_t)c * ncells + e) * NP, (uint32_t)(NP * sizeof(double)), bar);
   };
-  // neighbour end-layer values of item w held by this thread
-  auto load_nbr = [&](int64_t w, int lv, double (&nv)[KNB]) {
+  // neighbour end layers of item w -> snb buffer w & 1, by cp.async (this
+  // thread's copies; waited for before the barrier that ends item w - 1)
+  auto load_nbr = [&](int64_t w, int lv) {
     const double *src = p_hist[lv];
     const int sl = (int)(w & 1);
-#pragma unroll
-    for (int j = 0; j < KNB; ++j) {
-      const int i = tid + j * T;
-      double v = 0.0;
-      if (i < 18 * FN) {
-        const int side = i / (3 * FN), c = (i / FN) % 3, f = i % FN;
-        if (skind[sl][side] == 0)
-          v = src[((int64_t)c * ncells + snbr[sl][side]) * NP +
-                  cv_end_node<N>(side >> 1, (side & 1) ^ 1, f / N, f % N)];
-      }
-      nv[j] = v;
+    double *snb = sm + C::NB + sl * 18 * FN;
+    for (int i = tid; i < 18 * FN; i += T) {
+      const int side = i / (3 * FN), c = (i / FN) % 3, f = i % FN;
+      const bool in = skind[sl][side] == 0;
+      const double *p = in ? src + ((int64_t)c * ncells + snbr[sl][side]) * NP +
+                                 cv_end_node<N>(side >> 1, (side & 1) ^ 1, f / N, f % N)
+                           : src;
+      cp_async8(snb + i, p, in);
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  auto park_nbr = [&](const double (&nv)[KNB]) {
-#pragma unroll
-    for (int j = 0; j < KNB; ++j) {
-      const int i = tid + j * T;
-      if (i < 18 * FN) snb[i] = nv[j];
-    }
-  };
-
   // prologue: item 0 (own cell, neighbour layers), side info of items 0, 1
   if (tid == 0) issue_own(0);
   side_info(0);
   if (nitems > 1) side_info(1);
   __syncthreads();
-  {
-    double nv[KNB];
-    load_nbr(0, 0, nv);
-    park_nbr(nv);
-  }
+  load_nbr(0, 0);
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 
   int64_t e = blockIdx.x;
@@ -173,8 +167,8 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
     const bool has_next = w + 1 < nitems;
     const int lev_next = lev + 1 == nh ? 0 : lev + 1;
     if (has_next && tid == 0) issue_own(w + 1);
-    double nv[KNB];
-    if (has_next) load_nbr(w + 1, lev_next, nv);
+    if (has_next) load_nbr(w + 1, lev_next);
+    const double *snb = sm + C::NB + (w & 1) * 18 * FN;
     int ix, iy, iz;
     cv2_xyz(g, e, ix, iy, iz);  // 32-bit divisions, once per item
     const double h[3] = {g.hx[ix], g.hy[iy], g.hz[iz]};
@@ -252,49 +246,50 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
       cv_store<N>(ra + (((a * 2 + 1) * N + z) * N) * P1 + qx, P1, yb);
     }
     __syncthreads();
-    // x lines: out_a (=, first level; += later) S^T A_a + D^T B_a
-    for (int l = tid; l < 3 * N * N; l += T) {
-      const int a = l / (N * N), zy = l % (N * N);
-      double xa[NQ], xb[NQ], oa[N], ob[N];
-      cv_load<NQ>(ra + ((a * 2 + 0) * N * N + zy) * P1, 1, xa);
-      cv_load<NQ>(ra + ((a * 2 + 1) * N * N + zy) * P1, 1, xb);
-      eo_line<N, NQ, 1>(eo.St, xa, oa);
-      eo_line<N, NQ, -1>(eo.Dt, xb, ob);
-      double *o = so + a * NP + zy * N;
-      if (lev == 0) {
+    // x lines: out_a (=, first level; += later) S^T A_a + D^T B_a, and (same
+    // phase, independent) the fast tangential sweep of the own / neighbour end
+    // layers -> rb[o side c sl][qfa] (pitch P1; Z is dead)
+    for (int l = tid; l < 3 * N * N + 36 * N; l += T) {
+      if (l < 3 * N * N) {
+        const int a = l / (N * N), zy = l % (N * N);
+        double xa[NQ], xb[NQ], oa[N], ob[N];
+        cv_load<NQ>(ra + ((a * 2 + 0) * N * N + zy) * P1, 1, xa);
+        cv_load<NQ>(ra + ((a * 2 + 1) * N * N + zy) * P1, 1, xb);
+        eo_line<N, NQ, 1>(eo.St, xa, oa);
+        eo_line<N, NQ, -1>(eo.Dt, xb, ob);
+        double *o = so + a * NP + zy * N;
+        if (lev == 0) {
 #pragma unroll
-        for (int x = 0; x < N; ++x) o[x] = oa[x] + ob[x];
+          for (int x = 0; x < N; ++x) o[x] = oa[x] + ob[x];
+        } else {
+#pragma unroll
+          for (int x = 0; x < N; ++x) o[x] += oa[x] + ob[x];
+        }
       } else {
-#pragma unroll
-        for (int x = 0; x < N; ++x) o[x] += oa[x] + ob[x];
+        const int m = l - 3 * N * N;
+        const int o = m / (18 * N), side = (m / (3 * N)) % 6, c = (m / N) % 3, sl = m % N;
+        const int d = side >> 1;
+        double xi[N], yo[NQ];
+        if (o == 0) cv_load<N>(su + c * NP + cv_end_node<N>(d, side & 1, sl, 0), d == 0 ? N : 1, xi);
+        else cv_load<N>(snb + (side * 3 + c) * FN + sl * N, 1, xi);
+        eo_line<NQ, N, 1>(eo.S, xi, yo);
+        cv_store<NQ>(rb + m * P1, 1, yo);
       }
     }
     __syncthreads();
     // ---- faces ----------------------------------------------------------------
-    // fast tangential sweep of own / neighbour end layers: ra[o side c sl][qfa] (pitch P1)
-    for (int l = tid; l < 36 * N; l += T) {
-      const int o = l / (18 * N), side = (l / (3 * N)) % 6, c = (l / N) % 3, sl = l % N;
-      const int d = side >> 1;
-      double xi[N], yo[NQ];
-      if (o == 0) cv_load<N>(su + c * NP + cv_end_node<N>(d, side & 1, sl, 0), d == 0 ? N : 1, xi);
-      else cv_load<N>(snb + (side * 3 + c) * FN + sl * N, 1, xi);
-      eo_line<NQ, N, 1>(eo.S, xi, yo);
-      cv_store<NQ>(ra + l * P1, 1, yo);
-    }
-    __syncthreads();
-    // the next item's neighbour layers (snb is free from here on)
-    if (has_next) park_nbr(nv);
-    // slow sweep: traces rb[o][side][c][qsl][qfa]
+    // slow sweep: traces ra[o][side][c][qsl][qfa]
+    double *tr = ra;
     for (int l = tid; l < 36 * NQ; l += T) {
       const int osc = l / NQ, qfa = l % NQ;
       double xi[N], yo[NQ];
-      cv_load<N>(ra + osc * N * P1 + qfa, P1, xi);
+      cv_load<N>(rb + osc * N * P1 + qfa, P1, xi);
       eo_line<NQ, N, 1>(eo.S, xi, yo);
-      cv_store<NQ>(rb + osc * FQ + qfa, NQ, yo);
+      cv_store<NQ>(tr + osc * FQ + qfa, NQ, yo);
     }
     __syncthreads();
-    // Lax-Friedrichs flux at the face Gauss points -> vf[side a qsl][qfa] (ra, pitch P1)
-    double *vf = ra;
+    // Lax-Friedrichs flux at the face Gauss points -> vf[side a qsl][qfa] (rb, pitch P1)
+    double *vf = rb;
     for (int i = tid; i < 6 * FQ; i += T) {
       const int side = i / FQ, f = i % FQ, d = side >> 1, s = side & 1;
       const int k = skind[w & 1][side];
@@ -304,8 +299,8 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
       double uo[3], up[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        uo[c] = rb[(side * 3 + c) * FQ + f];
-        up[c] = rb[(18 + side * 3 + c) * FQ + f];
+        uo[c] = tr[(side * 3 + c) * FQ + f];
+        up[c] = tr[(18 + side * 3 + c) * FQ + f];
       }
       if (k != 0) {  // mirror state 2 g - u with the level's Dirichlet data
         const double *gd = p_gh[lev][side];
@@ -329,35 +324,30 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
       }
     }
     __syncthreads();
-    // lift, fast: rb[side a qsl][fa] = S^T along the fast face axis
+    // lift, fast: ra[side a qsl][fa] = S^T along the fast face axis
     for (int l = tid; l < 18 * NQ; l += T) {
       double xi[NQ], yo[N];
       cv_load<NQ>(vf + l * P1, 1, xi);
       eo_line<N, NQ, 1>(eo.St, xi, yo);
-      cv_store<N>(rb + l * N, 1, yo);
+      cv_store<N>(ra + l * N, 1, yo);
     }
     __syncthreads();
-    // lift, slow: ra[side a][sl][fa]
-    for (int l = tid; l < 18 * N; l += T) {
-      const int sa = l / N, fa = l % N;
-      double xi[NQ], yo[N];
-      cv_load<NQ>(rb + sa * NQ * N + fa, N, xi);
-      eo_line<N, NQ, 1>(eo.St, xi, yo);
-      cv_store<N>(ra + sa * FN + fa, N, yo);
-    }
-    __syncthreads();
-    // add the lifted sides onto their end nodes, one axis at a time (the two
-    // sides of an axis touch disjoint nodes; edges / corners get one side per
-    // phase)
+    // lift, slow, added straight onto the end nodes one axis at a time (the
+    // two sides of an axis touch disjoint nodes; edges / corners get one side
+    // per phase)
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      for (int i = tid; i < 6 * FN; i += T) {  // [s][a][sl][fa]
-        const int sa = i / FN, f = i % FN, s = sa / 3, a = sa % 3;
-        const int side = 2 * d + s;
-        so[a * NP + cv_end_node<N>(d, s, f / N, f % N)] += ra[(side * 3 + a) * FN + f];
+      for (int l = tid; l < 6 * N; l += T) {  // [s][a][fa]
+        const int sa = 6 * d + l / N, fa = l % N, s = (sa / 3) & 1, a = sa % 3;
+        double xi[NQ], yo[N];
+        cv_load<NQ>(ra + sa * NQ * N + fa, N, xi);
+        eo_line<N, NQ, 1>(eo.St, xi, yo);
+#pragma unroll
+        for (int sl = 0; sl < N; ++sl) so[a * NP + cv_end_node<N>(d, s, sl, fa)] += yo[sl];
       }
       __syncthreads();
     }
+
     if (lev == nh - 1) {
       if (prm.vol_data != nullptr) {
         // (v, f) with the body force at the quadrature points, z, y, x
@@ -398,6 +388,7 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
     // side info of item w + 2 into this item's slot (read by the LF phase
     // above and by the prefetch at the start of this item: both done)
     if (w + 2 < nitems) side_info(w + 2);
+    asm volatile("cp.async.wait_all;" ::: "memory");  // the next item's neighbour layers
     __syncthreads();  // so / skind are rewritten by the next items
     if (++lev == nh) {
       lev = 0;

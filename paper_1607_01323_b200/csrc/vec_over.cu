@@ -47,10 +47,10 @@ static int launch_vconv(dg_ctx *c, double *dst, const VecParams &prm, cudaStream
 }
 
 // persistent pipelined kernel (vconv2.cuh): as many CTAs as fit on the GPU
-template <int N, int NQ>
+template <int N, int NQ, int TV = 0, int MB = 0>
 static int launch_vconv2(dg_ctx *c, double *dst, const VecParams &prm, cudaStream_t st) {
-  using C = Cv2Cfg<N, NQ>;
-  auto kern = vconv2_kernel<N, NQ>;
+  using C = Cv2Cfg<N, NQ, TV, MB>;
+  auto kern = vconv2_kernel<N, NQ, TV, MB>;
   static int grid_max = 0;
   if (!grid_max) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -84,6 +84,10 @@ int vecop_over(dg_ctx *c, const double *src, double *dst, const VecParams &prm, 
     for (int j = 0; j < prm.n_hist; ++j)
       aligned = aligned && (reinterpret_cast<uintptr_t>(prm.hist[j]) & 15) == 0;
     if (!old && aligned) {
+      const int cfg = v ? atoi(v) : 0;  // thread / occupancy A/B at Q5
+      if (c->n == 6 && c->nq_over == 8 && cfg == 2) return launch_vconv2<6, 8, 256, 2>(c, dst, prm, st);
+      if (c->n == 6 && c->nq_over == 8 && cfg == 3) return launch_vconv2<6, 8, 192, 2>(c, dst, prm, st);
+      if (c->n == 6 && c->nq_over == 8 && cfg == 4) return launch_vconv2<6, 8, 128, 4>(c, dst, prm, st);
 #define DG_V2(NN, QQ) \
   if (c->n == NN && c->nq_over == QQ) return launch_vconv2<NN, QQ>(c, dst, prm, st);
       // even N only: the cell and its TMA copies are whole 16 B units
