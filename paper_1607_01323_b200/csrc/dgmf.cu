@@ -788,23 +788,47 @@ struct WInt {
   double w[kMaxN];
 };
 
-__device__ __forceinline__ double dual_weight(const Geo &g, int dim, int n, const WInt &wi,
+// w: the 1D integrals staged in shared memory by the calling kernel
+// (indexing the WInt kernel parameter per lane serialises the constant
+// cache); 32-bit index math below 2^32 DoFs
+__device__ __forceinline__ double dual_weight(const Geo &g, int dim, int n, const double *w,
                                               int64_t i) {
-  const int64_t np = (dim == 3) ? (int64_t)n * n * n : (int64_t)n * n;
-  const int64_t e = i / np;
-  int o = (int)(i % np);
-  const int x = o % n;
-  o /= n;
-  const int y = o % n;
-  const int z = (dim == 3) ? o / n : 0;
-  const int ix = (int)(e % g.nx);
-  const int64_t r = e / g.nx;
-  const int iy = (int)(r % g.ny);
-  const int iz = (int)(r / g.ny);
-  double v = 0.5 * g.hx[ix] * wi.w[x] * 0.5 * g.hy[iy] * wi.w[y];
-  if (dim == 3) v *= 0.5 * g.hz[iz] * wi.w[z];
+  int x, y, z, ix, iy, iz;
+  if ((uint64_t)i < (1ull << 32)) {
+    const unsigned np = (dim == 3) ? (unsigned)(n * n * n) : (unsigned)(n * n);
+    const unsigned ui = (unsigned)i, e = ui / np;
+    unsigned o = ui - e * np;
+    x = (int)(o % (unsigned)n);
+    o /= (unsigned)n;
+    y = (int)(o % (unsigned)n);
+    z = (dim == 3) ? (int)(o / (unsigned)n) : 0;
+    const unsigned r = e / (unsigned)g.nx;
+    ix = (int)(e - r * (unsigned)g.nx);
+    iy = (int)(r % (unsigned)g.ny);
+    iz = (int)(r / (unsigned)g.ny);
+  } else {
+    const int64_t np = (dim == 3) ? (int64_t)n * n * n : (int64_t)n * n;
+    const int64_t e = i / np;
+    int o = (int)(i % np);
+    x = o % n;
+    o /= n;
+    y = o % n;
+    z = (dim == 3) ? o / n : 0;
+    ix = (int)(e % g.nx);
+    const int64_t r = e / g.nx;
+    iy = (int)(r % g.ny);
+    iz = (int)(r / g.ny);
+  }
+  double v = 0.5 * g.hx[ix] * w[x] * 0.5 * g.hy[iy] * w[y];
+  if (dim == 3) v *= 0.5 * g.hz[iz] * w[z];
   return v;
 }
+
+// stage the WInt parameter in shared memory (all threads; ends with a barrier)
+#define DG_STAGE_WINT(sw, wi)                                     \
+  __shared__ double sw[kMaxN];                                    \
+  if (threadIdx.x < kMaxN) sw[threadIdx.x] = (wi).w[threadIdx.x]; \
+  __syncthreads()
 
 // face traces of the first (side 0: value, dL . line) or last (side 1:
 // value, dR . line) x-layer: one thread per (cell (iy, iz), y, z), the x-line
@@ -831,10 +855,11 @@ __global__ void halo_trace_kernel(const double *__restrict__ src, double *__rest
 __global__ void wdot_partial_kernel(const double *__restrict__ p, int64_t n, Geo g, int dim,
                                     int nn, WInt wi, double *__restrict__ partial) {
   __shared__ double sh[32];
+  DG_STAGE_WINT(sw, wi);
   double acc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    acc += p[i] * dual_weight(g, dim, nn, wi, i);
+    acc += p[i] * dual_weight(g, dim, nn, sw, i);
   acc = block_sum(acc, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = acc;
 }
@@ -843,10 +868,11 @@ __global__ void wdot_partial_kernel(const double *__restrict__ p, int64_t n, Geo
 __global__ void zero_mean_apply_kernel(double *__restrict__ b, int64_t n, Geo g, int dim, int nn,
                                        WInt wi, const double *__restrict__ s, double vol,
                                        int mode) {
+  DG_STAGE_WINT(sw, wi);
   const double coef = __ddiv_rn(*s, vol);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    if (mode == 0) b[i] = __dsub_rn(b[i], __dmul_rn(coef, dual_weight(g, dim, nn, wi, i)));
+    if (mode == 0) b[i] = __dsub_rn(b[i], __dmul_rn(coef, dual_weight(g, dim, nn, sw, i)));
     else b[i] = __dsub_rn(b[i], coef);
   }
 }
@@ -1224,6 +1250,7 @@ static int ensure_red3(dg_ctx *c) {
 __global__ void penalty_cell_kernel(const double *__restrict__ u, Geo g, int dim, int nn, WInt wi,
                                     int64_t ncells, double dt, double zd, double zc,
                                     double *__restrict__ tau_d, double *__restrict__ tau_ce) {
+  DG_STAGE_WINT(sw, wi);
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (e >= ncells) return;
@@ -1233,7 +1260,7 @@ __global__ void penalty_cell_kernel(const double *__restrict__ u, Geo g, int dim
     double acc = 0.0;
     for (int64_t o = lane; o < np; o += 32) {
       const int64_t i = e * np + o;
-      acc += u[(int64_t)c * ncells * np + i] * dual_weight(g, dim, nn, wi, i);
+      acc += u[(int64_t)c * ncells * np + i] * dual_weight(g, dim, nn, sw, i);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
