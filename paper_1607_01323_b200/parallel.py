@@ -168,11 +168,19 @@ class SlabLaplace:
         _lib.call("dg_halo_attach", self.ctx.handle, P(self.recv[0], self.has[0]),
                   P(self.recv[1], self.has[1]))
         self.comm = torch.cuda.Stream()
+        self.overlap = k != 4  # see vmult
         self.n_dofs = self.ctx.n_dofs
         self.volume = float(np.prod([v[-1] - v[0] for v in mesh.axis_vertices[:mesh.dim]]))
 
-    def vmult(self, src, dst, tau_scale=1.0):
-        """dst = L src on this slab (interior cells overlap the exchange)."""
+    def vmult(self, src, dst, tau_scale=1.0, overlap=None):
+        """dst = L src on this slab.  ``overlap`` False (default for the Q4
+        column kernel): exchange the face traces, then ONE launch over the
+        whole slab; True: the columns that touch no ghost side run while the
+        traces move, the rest after (dg_laplace_vmult_part 1 / 2).  Measured
+        on the C5 slabs (profiles/r02/slab_parts.py): splitting the launch
+        costs more than the exchange it hides -- 32x128x128 0.775 vs 0.633 ms,
+        16x128x128 0.337 vs 0.327 ms (no column of the 8x4 tiles is ghost-free
+        at 16 cells), against tens of microseconds for the exchange."""
         import torch
         P = lambda t: ctypes.c_void_p(t.data_ptr())
         main = torch.cuda.current_stream()
@@ -189,10 +197,13 @@ class SlabLaplace:
                       ctypes.c_void_p(self.comm.cuda_stream))
             self.comm_ops.exchange(self.send[0], self.send[1], self.recv[0], self.recv[1],
                                    self.lo, self.hi)
-        _lib.call("dg_laplace_vmult_part", h, P(src), P(dst), float(tau_scale), 1,
-                  ctypes.c_void_p(main.cuda_stream))
+        if overlap is None:
+            overlap = self.overlap
+        if overlap:
+            _lib.call("dg_laplace_vmult_part", h, P(src), P(dst), float(tau_scale), 1,
+                      ctypes.c_void_p(main.cuda_stream))
         main.wait_stream(self.comm)
-        _lib.call("dg_laplace_vmult_part", h, P(src), P(dst), float(tau_scale), 2,
+        _lib.call("dg_laplace_vmult_part", h, P(src), P(dst), float(tau_scale), 2 if overlap else 0,
                   ctypes.c_void_p(main.cuda_stream))
         return dst
 
