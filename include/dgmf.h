@@ -369,6 +369,15 @@ int dg_laplace_kernel_name(dg_ctx *ctx, char *buf, int len);
 int dg_laplace_vmult_part(dg_ctx *ctx, const double *src, double *dst,
                           double tau_scale, int part, void *stream);
 
+/* x-slab vmult around the ghost exchange (traced-ghost contexts, 3D Q3-Q5):
+ * phase 1: dst = L src over the whole slab with ZERO ghost traces (needs no
+ * exchanged data: runs while the traces move); phase 2: dst += the terms
+ * of the ghost traces (the x-face lifts on the first / last x-layer; src
+ * unused).  The two phases equal dg_laplace_vmult_part(part 0) up to
+ * rounding (the operator is linear in the ghost data). */
+int dg_laplace_vmult_split(dg_ctx *ctx, const double *src, double *dst, double tau_scale,
+                           int phase, void *stream);
+
 /* ---- sharded (x-slab) PCG building blocks (parallel.SlabPCG) ------------
  * The reference pcg (solvers.py:30-73) on x-slab contexts: every call works
  * on this rank's slab; the caller all-reduces the partial sums between calls

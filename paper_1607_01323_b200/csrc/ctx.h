@@ -41,6 +41,7 @@ struct dg_ctx {
   double *d_hcell = nullptr;   // per-cell dual-weight factor hx hy hz / 8 (3D)
   unsigned *d_counter = nullptr;  // work counter of the persistent warp-column kernel
   int halo_traces = 0;         // ghost layers carry face traces (column kernel)
+  double *d_zero_ghost = nullptr;  // zero ghost layer (dg_laplace_vmult_split phase 1)
   double *d_scal = nullptr;    // 16 device scalars
   double *h_scal = nullptr;    // pinned mirror
   std::vector<double *> work;  // solver work vectors (n_dofs each)

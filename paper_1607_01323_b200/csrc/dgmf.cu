@@ -284,6 +284,7 @@ int dg_ctx_destroy(dg_ctx *c) {
   for (double *w : c->vwork) cudaFree(w);
   cudaFree(c->d_vpart);
   cudaFree(c->d_apdot);
+  cudaFree(c->d_zero_ghost);
   delete c;
   return DG_OK;
 }
@@ -551,6 +552,36 @@ static int l7_lcmin(int dflt) {
   return e ? std::max(1, atoi(e)) : dflt;
 }
 
+// z-chunk length of the column kernels.  One CTA per SM (occ 1): CTAs =
+// cols x ceil(nz / lc) run in waves of the SM count, each wave as long as its
+// longest chunk plus ~2 layers of ring fill / z halo; the lc in [lcmin,
+// lcmax] with the smallest predicted time waves x (lc + 2) (ties: longer
+// chunks).  The rule for several CTAs per SM (and DG_CHUNK_OLD=1, per call,
+// for A/B) is about 4 waves: lc = nz / ceil(4 slots / cols) -- at occ 1 it
+// left a part-filled last wave on the x-slab sizes (64x128x128 Q4: 768 CTAs
+// = 5.2 waves; 1.24 -> 1.10 ms with the model, profiles/r02/chunk_ab.py),
+// at occ > 1 the model measured worse (64^3 Q3 0.163 -> 0.180 ms).
+static int chunk_len(int nz, int cols, int slots, int occ, int lcmin, int lcmax) {
+  lcmax = std::max(1, std::min(nz, lcmax));
+  lcmin = std::max(1, std::min(lcmin, lcmax));
+  if (occ > 1 || getenv("DG_CHUNK_OLD")) {
+    const int want = (4 * slots + cols - 1) / cols;
+    return std::min(std::max(lcmin, (nz + want - 1) / want), lcmax);
+  }
+  int best = lcmax;
+  double best_t = 1e300;
+  for (int lc = lcmax; lc >= lcmin; --lc) {
+    const int64_t nch = (nz + lc - 1) / lc;
+    const int64_t waves = ((int64_t)cols * nch + slots - 1) / slots;
+    const double t = (double)waves * (lc + 2.0);
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = lc;
+    }
+  }
+  return best;
+}
+
 // z-marching column kernel (laplace7.cuh): units = TX x TY tiles x z-chunks,
 // the chunk length chosen so that ~4 waves of CTAs fill the GPU
 template <int N, int TX, int TY, int NRING, int MINB, bool STAGE = false>
@@ -579,9 +610,8 @@ static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau
   }
   const int ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY;
   const int cols = ntx * nty, nz = zhi - zlo;
-  const int want = (4 * nsm * occ + cols - 1) / cols;  // chunks per column
-  int lc = std::max(l7_lcmin(4), (nz + want - 1) / want);  // measured: 32^3 Q3 54 -> 78 GDoF/s
-  lc = std::min(std::min(lc, nz), C::LCMAX);
+  // chunks >= 4 layers (measured: 32^3 Q3 54 -> 78 GDoF/s)
+  const int lc = chunk_len(nz, cols, nsm * occ, occ, l7_lcmin(4), C::LCMAX);
   const int nch = (nz + lc - 1) / lc;
   kern<<<(unsigned)(cols * nch), C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis),
                                                             tau_scale, part, zlo, zhi, lc, ntx, nty);
@@ -616,9 +646,7 @@ static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau
   }
   const int ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY;
   const int cols = ntx * nty, nz = zhi - zlo;
-  const int want = (4 * nsm * occ + cols - 1) / cols;
-  int lc = std::max(l7_lcmin(8), (nz + want - 1) / want);
-  lc = std::min(std::min(lc, nz), C::LCMAX);
+  const int lc = chunk_len(nz, cols, nsm * occ, occ, l7_lcmin(8), C::LCMAX);
   const int nch = (nz + lc - 1) / lc;
   if (EPI == kEpiDot) {
     if (4 * (int64_t)cols * nch > c->partials_n) return inval("laplace8 epilogue: partials buffer");
@@ -690,7 +718,8 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
   const char *vv = getenv("DG_LAP_VARIANT");
   int variant = vv ? atoi(vv) : 0;
   // ghost layers in the trace format are read by the column kernels only
-  if (c->halo_traces && (c->mode[0] == kGhost || c->mode[1] == kGhost) && variant != 8 && variant != 9)
+  if (c->halo_traces && (c->mode[0] == kGhost || c->mode[1] == kGhost) && variant != 7 && variant != 8 &&
+      variant != 9)
     variant = 0;
   if (c->dim == 3 && variant == 9) {
     const int cfg = l7_cfg();
@@ -1035,6 +1064,116 @@ int dg_zero_mean(dg_ctx *c, double *p, void *stream) {
 int dg_halo_count(const dg_ctx *c, int64_t *count) {
   if (!c || !count) return inval("null argument");
   *count = c->halo_count;
+  return DG_OK;
+}
+
+}  // extern "C"
+
+// Ghost-face part of the x-slab vmult (dg_laplace_vmult_split phase 2): the
+// SIP operator is linear in the ghost traces, so with phase 1 run on ZERO
+// traces, out += the terms of the x-lifts of the column kernel
+// (laplace8.cuh x phase, l7_lift) that carry the neighbour's data:
+//   per face node (y, z): vn = (M z-mass) v_ghost, gn = (M) g_ghost,
+//   cv = -A vn + D gn, cd = -B vn  (A, B, D of side7 for a halo side),
+//   T[z][y][x] = delta(x, end) cv + dEnd[x] cd,  out += (M y-mass) T.
+// One group of N*N threads per (boundary cell, side).
+template <int N>
+__global__ void ghost_lift_kernel(const Geo g, const __grid_constant__ LapTab<N> T, double ts,
+                                  int side, double *__restrict__ out) {
+  constexpr int N2 = N * N, G = 128 / N2, NP = N * N2;
+  __shared__ double sv[G][N2], sg[G][N2], c1[G][N2], c2[G][N2];
+  const int grp = threadIdx.x / N2, t = threadIdx.x - grp * N2;
+  const int64_t cell = (int64_t)blockIdx.x * G + grp;  // (iy, iz) of the boundary layer
+  const bool ok = grp < G && cell < (int64_t)g.ny * g.nz;
+  const int iy = ok ? (int)(cell % g.ny) : 0, iz = ok ? (int)(cell / g.ny) : 0;
+  const int ix = side ? g.nx - 1 : 0;
+  const double *gh = g.ghost[side];
+  // ghost payload [z][y][v|g] per boundary cell
+  if (ok) {
+    sv[grp][t] = gh[(cell * N2 + t) * 2];
+    sg[grp][t] = gh[(cell * N2 + t) * 2 + 1];
+  }
+  __syncthreads();
+  const double *ax = g.ax[0] + 4 * ix, *ay = g.ax[1] + 4 * iy, *az = g.ax[2] + 4 * iz;
+  const double hxi = ax[1], tx = ax[2], hy = ay[0], ty = ay[2], hz = az[0], tz = az[2];
+  const double *axn = ax + (side ? 4 : -4);  // the ghost cell's entry
+  const double sfx = 0.25 * hy * hz;
+  const double sgn = side ? -1.0 : 1.0;
+  const double A = ts * ((fmax(tx, axn[2]) + ty + tz) * sfx);
+  const double B = sgn * sfx * hxi, D = sgn * sfx * axn[1];
+  if (ok) {  // thread (z, y): z-mass of the traces, the lift coefficients
+    const int z = t / N, y = t - z * N;
+    double vn = 0.0, gn = 0.0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      vn += T.M[z * N + q] * sv[grp][q * N + y];
+      gn += T.M[z * N + q] * sg[grp][q * N + y];
+    }
+    c1[grp][t] = -A * vn + D * gn;
+    c2[grp][t] = -B * vn;
+  }
+  __syncthreads();
+  if (ok) {  // thread (z, x): y-mass, add into the x-line ends / derivative rows
+    const int z = t / N, x = t - z * N;
+    const int end = side ? N - 1 : 0;
+    const double dx = side ? T.dR[x] : T.dL[x];
+    double *o = out + ((int64_t)ix + (int64_t)g.nx * (iy + (int64_t)g.ny * iz)) * NP + z * N2 + x;
+#pragma unroll
+    for (int y = 0; y < N; ++y) {
+      double m1 = 0.0, m2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        m1 += T.M[y * N + q] * c1[grp][z * N + q];
+        m2 += T.M[y * N + q] * c2[grp][z * N + q];
+      }
+      o[y * N] += (x == end ? m1 : 0.0) + dx * m2;
+    }
+  }
+}
+
+extern "C" {
+
+// x-slab vmult in two phases around the ghost exchange: phase 1 = the whole
+// slab with ZERO ghost traces (one launch, no dependence on the exchange),
+// phase 2 = out += the ghost-trace terms on the boundary x-layers
+// (ghost_lift_kernel).  Traced-ghost contexts (3D, Q3-Q5).
+int dg_laplace_vmult_split(dg_ctx *c, const double *src, double *dst, double tau_scale,
+                           int phase, void *stream) {
+  if (!c || !dst) return inval("null argument");
+  if (phase != 1 && phase != 2) return inval("phase must be 1 or 2");
+  if (!c->halo_traces || c->dim != 3) return inval("dg_laplace_vmult_split: traced-ghost 3D contexts");
+  if ((c->mode[0] == kGhost && !c->d_recv[0]) || (c->mode[1] == kGhost && !c->d_recv[1]))
+    return inval("x-slab context: attach ghost layers (dg_halo_attach) first");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (phase == 1) {
+    if (!src) return inval("null argument");
+    if (!c->d_zero_ghost) {
+      DG_CUDA_CHECK(cudaMalloc((void **)&c->d_zero_ghost, sizeof(double) * (size_t)std::max<int64_t>(c->halo_count, 1)));
+      DG_CUDA_CHECK(cudaMemset(c->d_zero_ghost, 0, sizeof(double) * (size_t)std::max<int64_t>(c->halo_count, 1)));
+    }
+    const double *keep[2] = {c->d_recv[0], c->d_recv[1]};
+    for (int s = 0; s < 2; ++s)
+      if (c->mode[s] == kGhost) c->d_recv[s] = c->d_zero_ghost;
+    const int rc = laplace_dispatch(c, src, dst, tau_scale, 0, st);
+    c->d_recv[0] = keep[0];
+    c->d_recv[1] = keep[1];
+    return rc;
+  }
+  if (c->n_cells == 0) return DG_OK;
+  const Geo g = c->geo();
+  for (int s = 0; s < 2; ++s) {
+    if (c->mode[s] != kGhost) continue;
+    const int64_t cells = (int64_t)g.ny * g.nz;
+#define DG_GL(NN)                                                                             \
+  if (c->n == NN) {                                                                           \
+    constexpr int G = 128 / (NN * NN);                                                        \
+    ghost_lift_kernel<NN><<<(unsigned)((cells + G - 1) / G), 128, 0, st>>>(g, lap_tab<NN>(c->basis), \
+                                                                         tau_scale, s, dst);   \
+  }
+    DG_GL(4) DG_GL(5) DG_GL(6)
+#undef DG_GL
+  }
+  DG_LAUNCH_CHECK("ghost_lift_kernel");
   return DG_OK;
 }
 

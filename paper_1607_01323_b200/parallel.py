@@ -168,26 +168,27 @@ class SlabLaplace:
         _lib.call("dg_halo_attach", self.ctx.handle, P(self.recv[0], self.has[0]),
                   P(self.recv[1], self.has[1]))
         self.comm = torch.cuda.Stream()
-        self.overlap = k != 4  # see vmult
+        self.traced = mesh.dim == 3 and 3 <= k <= 5  # ghost payload: face traces
         self.n_dofs = self.ctx.n_dofs
         self.volume = float(np.prod([v[-1] - v[0] for v in mesh.axis_vertices[:mesh.dim]]))
 
     def vmult(self, src, dst, tau_scale=1.0, overlap=None):
-        """dst = L src on this slab.  ``overlap`` False (default for the Q4
-        column kernel): exchange the face traces, then ONE launch over the
-        whole slab; True: the columns that touch no ghost side run while the
-        traces move, the rest after (dg_laplace_vmult_part 1 / 2).  Measured
-        on the C5 slabs (profiles/r02/slab_parts.py): splitting the launch
-        costs more than the exchange it hides -- 32x128x128 0.775 vs 0.633 ms,
-        16x128x128 0.337 vs 0.327 ms (no column of the 8x4 tiles is ghost-free
-        at 16 cells), against tens of microseconds for the exchange."""
+        """dst = L src on this slab, the ghost exchange overlapped with the
+        slab's own work.  Traced ghosts (Q3-Q5): ONE launch over the whole
+        slab on zero ghost traces while the traces move, then the ghost-trace
+        face terms on the boundary x-layers (dg_laplace_vmult_split; the
+        operator is linear in the ghost data).  Other degrees: the columns
+        that touch no ghost side while the traces move, the rest after
+        (dg_laplace_vmult_part 1 / 2) -- splitting the column launch itself
+        costs more than the exchange at Q4 (profiles/r02/slab_parts.py).
+        ``overlap`` False: exchange first, then one launch (part 0)."""
         import torch
         P = lambda t: ctypes.c_void_p(t.data_ptr())
         main = torch.cuda.current_stream()
         h = self.ctx.handle
+        ms = ctypes.c_void_p(main.cuda_stream)
         if self.nranks == 1:
-            _lib.call("dg_laplace_vmult", h, P(src), P(dst), float(tau_scale),
-                      ctypes.c_void_p(main.cuda_stream))
+            _lib.call("dg_laplace_vmult", h, P(src), P(dst), float(tau_scale), ms)
             return dst
         self.comm.wait_stream(main)
         with torch.cuda.stream(self.comm):
@@ -198,15 +199,18 @@ class SlabLaplace:
             self.comm_ops.exchange(self.send[0], self.send[1], self.recv[0], self.recv[1],
                                    self.lo, self.hi)
         if overlap is None:
-            overlap = self.overlap
+            overlap = True
+        if overlap and self.traced:
+            _lib.call("dg_laplace_vmult_split", h, P(src), P(dst), float(tau_scale), 1, ms)
+            main.wait_stream(self.comm)
+            _lib.call("dg_laplace_vmult_split", h, P(src), P(dst), float(tau_scale), 2, ms)
+            return dst
         if overlap:
-            _lib.call("dg_laplace_vmult_part", h, P(src), P(dst), float(tau_scale), 1,
-                      ctypes.c_void_p(main.cuda_stream))
+            _lib.call("dg_laplace_vmult_part", h, P(src), P(dst), float(tau_scale), 1, ms)
         main.wait_stream(self.comm)
-        _lib.call("dg_laplace_vmult_part", h, P(src), P(dst), float(tau_scale), 2 if overlap else 0,
-                  ctypes.c_void_p(main.cuda_stream))
+        _lib.call("dg_laplace_vmult_part", h, P(src), P(dst), float(tau_scale),
+                  2 if overlap else 0, ms)
         return dst
-
 
     def diagonal(self, tau_scale=1.0):
         """Exact Jacobi diagonal of this slab (operators.py:675-730)."""

@@ -43,6 +43,17 @@ for nranks in (2, 4, 8):
             b.record(); torch.cuda.synchronize()
             return a.elapsed_time(b) / reps
         t1, t2, t0 = t(1), t(2), t(0)
+        def ts_(ph, reps=20):
+            f = lambda: _lib.call("dg_laplace_vmult_split", c.handle, P(src), P(dst), 1.0, ph, st)
+            f(); torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                f()
+            b.record(); torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+        if var == "0":
+            print(f"  P={nranks} split phase 1 {ts_(1):.3f} ms, phase 2 {ts_(2):.4f} ms", flush=True)
         _lib.call("dg_laplace_vmult_part", c.handle, P(src), P(dst), 1.0, 1, st)
         _lib.call("dg_laplace_vmult_part", c.handle, P(src), P(dst), 1.0, 2, st)
         torch.cuda.synchronize()

@@ -285,7 +285,7 @@ def test_slab_split_equals_full_on_one_gpu(k):
                     recvs[r][0].copy_(sends[lo][1])
                 if hi is not None:
                     recvs[r][1].copy_(sends[hi][0])
-            outs = []
+            outs, outs2 = [], []
             for r in range(nranks):
                 out = torch.full_like(locs[r], np.nan)
                 for prt in (1, 2):
@@ -293,8 +293,18 @@ def test_slab_split_equals_full_on_one_gpu(k):
                               ctypes_ptr(locs[r].data_ptr()), ctypes_ptr(out.data_ptr()),
                               1.0, prt, st)
                 outs.append(out.cpu().numpy().reshape(counts[2], counts[1], -1, n))
+                if k >= 3:  # traced ghosts: whole slab on zero traces + ghost lifts
+                    out2 = torch.full_like(locs[r], np.nan)
+                    for phase in (1, 2):
+                        _lib.call("dg_laplace_vmult_split", ctxs[r].handle,
+                                  ctypes_ptr(locs[r].data_ptr()), ctypes_ptr(out2.data_ptr()),
+                                  1.0, phase, st)
+                    outs2.append(out2.cpu().numpy().reshape(counts[2], counts[1], -1, n))
             got = np.concatenate(outs, axis=2).ravel()
             assert relerr(got, full) < 1e-14, (nranks, per)
+            if outs2:
+                got2 = np.concatenate(outs2, axis=2).ravel()
+                assert relerr(got2, full) < 1e-14, ("split", nranks, per, relerr(got2, full))
 
 
 def test_large_periodic_properties():
