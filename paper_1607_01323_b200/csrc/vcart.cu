@@ -40,14 +40,14 @@ static int ensure_trc(dg_ctx *c, int64_t n) {
   return DG_OK;
 }
 
-template <int N, int OP>
+template <int N, int OP, int CB = 0>
 static int launch_vc(dg_ctx *c, const double *src, double *dst, double gamma0_dt, double nu,
                      const double *tau_d, const double *tau_c, cudaStream_t st,
                      double *pdot = nullptr) {
-  using C = VlCfg<N>;
+  using C = VlCfg<N, CB>;
   static const VcTab<N> tab = vc_tab<N>(c->basis);  // depends on k only
-  auto ktr = vl_trace_kernel<N, OP == kVcHelmholtz>;
-  auto kap = vl_apply_kernel<N, OP>;
+  auto ktr = vl_trace_kernel<N, OP == kVcHelmholtz, CB>;
+  auto kap = vl_apply_kernel<N, OP, CB>;
   static bool attr = false;
   if (!attr) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(ktr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));

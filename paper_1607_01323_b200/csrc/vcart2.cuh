@@ -23,13 +23,15 @@
 
 namespace dg {
 
-template <int N>
+template <int N, int CB = 0>
 struct VlCfg {
   static constexpr int P = N * N * N, F = N * N;
   static constexpr int LS = (N & 1) ? N : N + 1;  // padded line stride
   static constexpr int PS = LS * N;               // plane stride
   static constexpr int CS = PS * N;               // one component of one cell
-  static constexpr int CPB = N <= 2 ? 32 : (N == 3 ? 16 : (N == 4 ? 4 : (N <= 6 ? 4 : 2)));
+  // cells per CTA (Q3: 2 -- C4 projection apply 248 -> 227 us, Helmholtz
+  // 348 -> 343 us against 4; 1 and 8 slower; profiles/r02/vec_time.py)
+  static constexpr int CPB = CB ? CB : (N <= 2 ? 32 : (N == 3 ? 16 : (N == 4 ? 2 : (N <= 6 ? 4 : 2))));
   static constexpr int LINES = CPB * N * N;       // lines of one component
   static constexpr int THREADS = ((3 * LINES + 31) / 32) * 32;  // one thread per component line
   static constexpr int TAB = 2 * N * N + 5 * N;   // VcTab staged for the face phases
@@ -107,11 +109,11 @@ __device__ __forceinline__ VlGeo vl_geo(const Geo &g, int64_t e) {
 // nodal -> Gauss-collocated u~ of all CPB cells: x (global -> TT), y (TT ->
 // UG), z (UG -> UG).  The z phase hands each z line of u~ to `zline`
 // (cs, c, x, y, u~ line) while it is in registers.  Ends with a barrier.
-template <int N, class ZL>
+template <int N, int CB, class ZL>
 __device__ __forceinline__ void vl_to_gauss(const double *__restrict__ u, int64_t e0,
                                             int64_t ncells, const double *S, double *sm_cells,
                                             ZL &&zline) {
-  using C = VlCfg<N>;
+  using C = VlCfg<N, CB>;
   constexpr int NN = N * N;
   #pragma unroll
   for (int it = threadIdx.x; it < 3 * C::LINES; it += C::THREADS) {  // x lines
@@ -152,11 +154,11 @@ __device__ __forceinline__ void vl_to_gauss(const double *__restrict__ u, int64_
 
 // Traces of all three components on all six sides at the face Gauss points
 // trc[cell][side][comp][val | dn][f].
-template <int N, bool NEED_DN>
-__global__ void __launch_bounds__(VlCfg<N>::THREADS)
+template <int N, bool NEED_DN, int CB = 0>
+__global__ void __launch_bounds__(VlCfg<N, CB>::THREADS)
 vl_trace_kernel(const double *__restrict__ u, double *__restrict__ trc, const Geo g,
                 const __grid_constant__ VcTab<N> tab, const int64_t ncells) {
-  using C = VlCfg<N>;
+  using C = VlCfg<N, CB>;
   constexpr int F = C::F, NN = N * N;
   extern __shared__ double sm[];
   double *cells = sm + C::TAB;
@@ -188,7 +190,7 @@ vl_trace_kernel(const double *__restrict__ u, double *__restrict__ trc, const Ge
     emit(e, 4, c, y * N + x, w, sz);
     emit(e, 5, c, y * N + x, w, sz);
   };
-  vl_to_gauss<N>(u, e0, ncells, tab.S, cells, zl);
+  vl_to_gauss<N, CB>(u, e0, ncells, tab.S, cells, zl);
   #pragma unroll
   for (int it = threadIdx.x; it < 6 * C::LINES; it += C::THREADS) {  // y and x lines of u~
     const int ax = it < 3 * C::LINES ? 1 : 0;
@@ -207,14 +209,14 @@ vl_trace_kernel(const double *__restrict__ u, double *__restrict__ trc, const Ge
   }
 }
 
-template <int N, int OP>
-__global__ void __launch_bounds__(VlCfg<N>::THREADS)
+template <int N, int OP, int CB = 0>
+__global__ void __launch_bounds__(VlCfg<N, CB>::THREADS)
 vl_apply_kernel(const double *__restrict__ u, const double *__restrict__ trc,
                 double *__restrict__ out, const Geo g, const __grid_constant__ VcTab<N> tab,
                 const double gamma0_dt, const double nu, const double *__restrict__ tau_d,
                 const double *__restrict__ tau_c, const int64_t ncells,
                 double *__restrict__ pdot = nullptr) {
-  using C = VlCfg<N>;
+  using C = VlCfg<N, CB>;
   constexpr int F = C::F, NN = N * N;
   extern __shared__ double sm[];
   double *tb = sm;
@@ -422,7 +424,7 @@ vl_apply_kernel(const double *__restrict__ u, const double *__restrict__ trc,
       vl_st<N>(cell + C::TT + first, C::PS, gz);  // div accumulator
     }
   };
-  vl_to_gauss<N>(u, e0, ncells, tab.S, cells, zl);
+  vl_to_gauss<N, CB>(u, e0, ncells, tab.S, cells, zl);
   if (divdiv) {
     // y lines: d/dy
     #pragma unroll
