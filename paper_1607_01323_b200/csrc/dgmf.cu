@@ -496,7 +496,8 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
                                 int epi, const EpiArgs &ea, cudaStream_t st) {
   c->epi_nparts = laplace_bricks(c);
   // DG_EPI_COL=1: the column kernel's cooperative epilogue at Q4 (measured
-  // slower: C2 PCG 0.91 vs 0.57 ms per iteration -- a barrier per layer and
+  // slower: C2 PCG 0.62 vs 0.57 ms per iteration (0.91 before its loads were
+  // batched per row and prefetched into L2) -- a barrier per layer and
   // the epilogue vectors streamed by one 320-thread CTA per SM); the v4
   // bricks' 416-thread CTAs stream them better
   static const bool col = getenv("DG_EPI_COL") != nullptr;

@@ -350,6 +350,15 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     const bool more = p + 1 < nlay;
     halo_load(more ? iz + 1 : -1);
     halo_stage2(par);
+    if (EPI == kEpiCheb && (N & 1)) {  // this layer's epilogue operands -> L2
+      const int R = ex * NP;
+      for (int i = tid * 16; i < 4 * ey * R; i += 16 * C::THREADS) {  // 128 B lines
+        const int v = i / (ey * R), rem = i - v * (ey * R), yy = rem / R, j = rem - yy * R;
+        const size_t gi = ((size_t)x0 + (size_t)g.nx * (y0 + yy) + nxy * iz) * NP + j;
+        const double *p = v == 0 ? ea.rc : (v == 1 ? ea.diag : (v == 2 ? ea.x : u));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p + gi));
+      }
+    }
     // ================= z phase: columns x in this half of plane y = s =================
     {
       const double *q = cc + c * C::CCS;
@@ -479,7 +488,44 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     }
     if (tma && EPI == kEpiStore) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();  // B_b: out complete in the slot
-    if (EPI != kEpiStore) {
+    if (EPI == kEpiCheb && (N & 1)) {
+      // Chebyshev epilogue, odd N (a tile row of cells is one contiguous run
+      // in global and shared memory): per row, each thread loads the operands
+      // of up to 4 points (prefetched into L2 during the z phase) before any
+      // arithmetic or store, so the row's loads are in flight together
+      constexpr int U = 4;
+      const int R = ex * NP;
+      for (int yy = 0; yy < ey; ++yy) {
+        const size_t rb = ((size_t)x0 + (size_t)g.nx * (y0 + yy) + nxy * iz) * NP;
+        const double *sl = slot + TX * yy * CSTR;
+        for (int j0 = tid; j0 < R; j0 += U * C::THREADS) {
+          double yv[U], rc[U], dg[U], xv[U], uv[U];
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            const int j = j0 + q * C::THREADS;
+            if (j < R) {
+              yv[q] = sl[j];
+              rc[q] = ea.rc[rb + j];
+              dg[q] = ea.diag[rb + j];
+              xv[q] = ea.x[rb + j];
+              uv[q] = u[rb + j];
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            const int j = j0 + q * C::THREADS;
+            if (j < R) {
+              const double r = __dsub_rn(rc[q], yv[q]);
+              const double dn = __dadd_rn(__dmul_rn(ea.a, uv[q]), __dmul_rn(ea.b, __ddiv_rn(r, dg[q])));
+              ea.rc[rb + j] = r;
+              ea.dnew[rb + j] = dn;
+              ea.x[rb + j] = __dadd_rn(xv[q], dn);
+            }
+          }
+        }
+      }
+      __syncthreads();  // the slot is refilled by a later z phase
+    } else if (EPI != kEpiStore) {
       // epilogue on this layer's cells: out / Chebyshev vectors / partial sums
       const double hzl = hz;
       for (int i = tid; i < ex * ey * NP; i += C::THREADS) {
