@@ -217,13 +217,15 @@ def cpu_baseline(k):
                                     f"{ca} BLAS threads)"}}
 
 
-def run_c4_step(nsteps=5):
+def run_c4_step(nsteps=5, mg_precision="fp64"):
     """BASELINE config 4: dual-splitting steps on the 64 x 32 x 32 Q3 channel
     (y graded 1.8, periodic x/z, walls), nu = 1/180, dt = 1e-3, BDF2, V4,
     u0 = (1 - y^2, 0, 0) + 0.1 U(-1,1) (seed 3), history [u0, u0].  The first
     two steps are warm-up (lazy loading of the kernel modules they touch
     first, graph capture of the V-cycle); the median of the rest is
-    reported, every step is listed."""
+    reported, every step is listed.  mg_precision "fp32": the paper's
+    single-precision V-cycle inside the fp64 pressure CG,
+    reported beside the fp64 headline, not instead of it."""
     import numpy as np
     import torch
     from paper_1607_01323_b200 import multigrid as MG, operators as ops, stepper as S
@@ -232,7 +234,8 @@ def run_c4_step(nsteps=5):
                                    grading=(0.0, 1.8, 0.0), periodic=(True, False, True))
     spaces = [DgSpace(m, 3) for m in meshes]
     spec = ops.BoundarySpec({"ymin": ops.DirichletBC(None), "ymax": ops.DirichletBC(None)})
-    cfg = S.StepConfig(dt=1e-3, nu=1 / 180, J=2, variant=ops.VariantConfig("V4"))
+    cfg = S.StepConfig(dt=1e-3, nu=1 / 180, J=2, variant=ops.VariantConfig("V4"),
+                       mg_precision=mg_precision)
     vc = S.VelocityCorrection(spaces, spec, cfg)
     x, y, z = spaces[-1].node_coords()
     rng = np.random.default_rng(3)
@@ -554,6 +557,10 @@ def main():
     step = None
     if rank == 0 and world == 1 and not args.no_step:
         step = run_c4_step()
+        s32 = run_c4_step(4, "fp32")
+        step["mg_fp32"] = {"ms_per_step_steady": s32["ms_per_step_steady"],
+                           "iterations": [x["iterations"] for x in s32["steps"]],
+                           "note": "the paper's single-precision V-cycle in the fp64 CG"}
     small = dsweep = None
     if rank == 0 and world == 1 and not args.no_step:
         small = run_small_configs()
