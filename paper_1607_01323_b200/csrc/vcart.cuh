@@ -116,7 +116,11 @@ vpcg_update_kernel(double *__restrict__ x, double *__restrict__ r, const double 
   constexpr int P = C::P;
   __shared__ double buf[2][C::CPB * 3 * P];
   __shared__ double red[32];
+  // M^-1 rows in shared memory: indexing the parameter by the lane's node
+  // coordinate serialised the constant cache
+  __shared__ double sA[N * N];
   if (!(scal[1] > 0.0)) return;  // breakdown: the host stops, x and r stay
+  if (threadIdx.x < N * N) sA[threadIdx.x] = mi.A[threadIdx.x];
   const double alpha = __ddiv_rn(scal[0], scal[1]);
   // blockDim = THREADS rounded up to whole warps (full-mask shuffles below);
   // the padding threads own no node
@@ -126,14 +130,24 @@ vpcg_update_kernel(double *__restrict__ x, double *__restrict__ r, const double 
   const int64_t e = (int64_t)blockIdx.x * C::CPB + cs;
   const bool valid = in && e < ncells;
   double *b0 = buf[0] + cs * 3 * P, *b1 = buf[1] + cs * 3 * P;
-  double rv[3];
+  double rv[3], xv[3], pv[3], av[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {  // all twelve loads first
+    const int64_t i = ((int64_t)c * ncells + e) * P + q;
+    if (valid) {
+      xv[c] = x[i];
+      pv[c] = p[i];
+      rv[c] = r[i];
+      av[c] = Ap[i];
+    }
+  }
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const int64_t i = ((int64_t)c * ncells + e) * P + q;
     double v = 0.0;
     if (valid) {
-      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
-      v = __dsub_rn(r[i], __dmul_rn(alpha, Ap[i]));
+      x[i] = __dadd_rn(xv[c], __dmul_rn(alpha, pv[c]));
+      v = __dsub_rn(rv[c], __dmul_rn(alpha, av[c]));
       r[i] = v;
     }
     rv[c] = v;
@@ -142,25 +156,27 @@ vpcg_update_kernel(double *__restrict__ x, double *__restrict__ r, const double 
   __syncthreads();
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    const double t = vc_dot<N, 0>(mi.A + x0 * N, 1, b0 + c * P, x0, y0, z0);
+    const double t = vc_dot<N, 0>(sA + x0 * N, 1, b0 + c * P, x0, y0, z0);
     if (in) b1[c * P + q] = t;
   }
   __syncthreads();
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    const double t = vc_dot<N, 1>(mi.A + y0 * N, 1, b1 + c * P, x0, y0, z0);
+    const double t = vc_dot<N, 1>(sA + y0 * N, 1, b1 + c * P, x0, y0, z0);
     if (in) b0[c * P + q] = t;
   }
   __syncthreads();
   double acc = 0.0;
   if (valid) {
-    const int ix = (int)(e % g.nx), iy = (int)((e / g.nx) % g.ny), iz = (int)(e / ((int64_t)g.nx * g.ny));
+    const unsigned eu = (unsigned)e, nx = (unsigned)g.nx, ny = (unsigned)g.ny;
+    const unsigned qq = eu / nx, iz = qq / ny;
+    const int ix = (int)(eu - qq * nx), iy = (int)(qq - iz * ny);
     double s = 0.5 * g.hx[ix] * 0.5 * g.hy[iy];
     s *= 0.5 * g.hz[iz];
     s = 1.0 / s;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double zv = s * vc_dot<N, 2>(mi.A + z0 * N, 1, b0 + c * P, x0, y0, z0);
+      const double zv = s * vc_dot<N, 2>(sA + z0 * N, 1, b0 + c * P, x0, y0, z0);
       z[((int64_t)c * ncells + e) * P + q] = zv;
       acc += rv[c] * zv;
     }
