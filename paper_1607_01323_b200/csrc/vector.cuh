@@ -37,12 +37,23 @@ static __global__ void dot_partial_kernel(const double *__restrict__ x,
   if (threadIdx.x == 0) partial[blockIdx.x] = acc;
 }
 
-// out[0] = sum(partial[0..m)) in fixed order (one block)
+// out[0] = sum(partial[0..m)) in fixed order (one block); long arrays (the
+// per-CTA partials of the vector kernels: 16-32k) with four independent
+// accumulators per thread (m <= blockDim: one element per thread, as before)
 static __global__ void sum_partials_kernel(const double *__restrict__ partial, int m,
                                     double *__restrict__ out) {
   __shared__ double sh[32];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) acc += partial[i];
+  const int bd = blockDim.x;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int i = threadIdx.x;
+  for (; i + 3 * bd < m; i += 4 * bd) {
+    a0 += partial[i];
+    a1 += partial[i + bd];
+    a2 += partial[i + 2 * bd];
+    a3 += partial[i + 3 * bd];
+  }
+  for (; i < m; i += bd) a0 += partial[i];
+  double acc = (a0 + a1) + (a2 + a3);
   acc = block_sum(acc, sh);
   if (threadIdx.x == 0) *out = acc;
 }
