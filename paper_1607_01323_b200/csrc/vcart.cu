@@ -40,10 +40,15 @@ static int ensure_trc(dg_ctx *c, int64_t n) {
   return DG_OK;
 }
 
+// pz != null (the velocity PCG): the trace kernel first updates the direction
+// in place, src = pz + beta src, and sets scal[0] = rz_new (vpcg_p_kernel's
+// work); *fused = whether it did (no trace kernel without face terms)
 template <int N, int OP, int CB = 0>
 static int launch_vc(dg_ctx *c, const double *src, double *dst, double gamma0_dt, double nu,
                      const double *tau_d, const double *tau_c, cudaStream_t st,
-                     double *pdot = nullptr) {
+                     double *pdot = nullptr, const double *pz = nullptr, double beta = 0.0,
+                     double *scal = nullptr, double rz_new = 0.0, bool *fused = nullptr) {
+  if (fused) *fused = false;
   using C = VlCfg<N, CB>;
   static const VcTab<N> tab = vc_tab<N>(c->basis);  // depends on k only
   auto ktr = vl_trace_kernel<N, OP == kVcHelmholtz, CB>;
@@ -64,8 +69,10 @@ static int launch_vc(dg_ctx *c, const double *src, double *dst, double gamma0_dt
   const unsigned grid = (unsigned)((c->n_cells + C::CPB - 1) / C::CPB);
   const Geo g = c->geo();
   if (faces) {
-    ktr<<<grid, C::THREADS, C::SMEM, st>>>(src, c->d_trc, g, tab, c->n_cells);
+    ktr<<<grid, C::THREADS, C::SMEM, st>>>(src, c->d_trc, g, tab, c->n_cells, pz, beta, scal,
+                                            rz_new);
     DG_LAUNCH_CHECK("vl_trace_kernel");
+    if (fused) *fused = pz != nullptr;
   }
   kap<<<grid, C::THREADS, C::SMEM, st>>>(src, c->d_trc, dst, g, tab, gamma0_dt, nu, tau_d, tau_c,
                                           c->n_cells, pdot);
@@ -98,7 +105,10 @@ int vcart_apply(dg_ctx *c, int op, const double *src, double *dst, double gamma0
 // *nparts = the number of CTAs.  DG_ENOTSUP where vcart_apply has no fast path.
 static int vcart_apply_dot(dg_ctx *c, int op, const double *src, double *dst, double gamma0_dt,
                            double nu, const double *tau_d, const double *tau_c, double *pdot,
-                           int64_t *nparts, cudaStream_t st) {
+                           int64_t *nparts, cudaStream_t st, const double *pz = nullptr,
+                           double beta = 0.0, double *scal = nullptr, double rz_new = 0.0,
+                           bool *fused = nullptr) {
+  if (fused) *fused = false;
   static const bool generic = [] {
     const char *v = getenv("DG_VEC_GENERIC");
     return v && atoi(v) != 0;
@@ -109,8 +119,10 @@ static int vcart_apply_dot(dg_ctx *c, int op, const double *src, double *dst, do
   case NN:                                                                                          \
     *nparts = (c->n_cells + VlCfg<NN>::CPB - 1) / VlCfg<NN>::CPB;                                  \
     return op == kVcHelmholtz                                                                       \
-               ? launch_vc<NN, kVcHelmholtz>(c, src, dst, gamma0_dt, nu, tau_d, tau_c, st, pdot)   \
-               : launch_vc<NN, kVcProjection>(c, src, dst, gamma0_dt, nu, tau_d, tau_c, st, pdot);
+               ? launch_vc<NN, kVcHelmholtz>(c, src, dst, gamma0_dt, nu, tau_d, tau_c, st, pdot,   \
+                                             pz, beta, scal, rz_new, fused)                        \
+               : launch_vc<NN, kVcProjection>(c, src, dst, gamma0_dt, nu, tau_d, tau_c, st, pdot,  \
+                                              pz, beta, scal, rz_new, fused);
   switch (c->n) { DG_VC(2) DG_VC(3) DG_VC(4) DG_VC(5) DG_VC(6) DG_VC(7) DG_VC(8) }
 #undef DG_VC
   return DG_ENOTSUP;
@@ -284,10 +296,30 @@ extern "C" int dg_vector_pcg(dg_ctx *c, int op, double gamma0_dt, double nu, con
   // one iteration up to the new r.z: Ap = A p with p.Ap from the apply kernel
   // (or a separate dot where the generic operator runs), the fused update;
   // the partial sums are reduced in a fixed order
+  // pending p update (p = z + beta p, scal[0] = rz_new) of the previous
+  // iteration: folded into the next trace kernel when the fast path has one
+  static const bool generic = [] {
+    const char *v = getenv("DG_VEC_GENERIC");
+    return v && atoi(v) != 0;
+  }();
+  const bool fold_p = !generic && c->basis.nq == c->n && (op == 0 ? nu != 0.0 : tau_c != nullptr);
+  bool pend = false;
+  double pbeta = 0.0, prz = 0.0;
+  const int gb2 = vgrid(n);
+  auto flush_p = [&](cudaStream_t s) {
+    if (!pend) return;
+    vpcg_p_kernel<<<gb2, 256, 0, s>>>(p, z, pbeta, prz, scal, n);
+    pend = false;
+  };
   auto body = [&](cudaStream_t s) -> int {
     int64_t np = 0;
-    int rc2 = vcart_apply_dot(c, op, p, Ap, gamma0_dt, nu, tau_d, tau_c, c->d_apdot, &np, s);
+    bool fused = false;
+    int rc2 = vcart_apply_dot(c, op, p, Ap, gamma0_dt, nu, tau_d, tau_c, c->d_apdot, &np, s,
+                              pend ? z : nullptr, pbeta, scal, prz, &fused);
+    if (pend && rc2 == DG_OK && !fused) return inval("vector PCG: direction update not applied");
+    if (rc2 == DG_OK) pend = false;
     if (rc2 == DG_ENOTSUP) {
+      flush_p(s);
       if ((rc2 = apply(p, Ap, s))) return rc2;
       dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(p, Ap, n, c->d_red);
       sum_partials_kernel<<<1, 1024, 0, s>>>(c->d_red, kRedBlocks, scal + 1);
@@ -330,8 +362,14 @@ extern "C" int dg_vector_pcg(dg_ctx *c, int op, double gamma0_dt, double nu, con
       stats->breakdown = 1;
       return DG_OK;
     }
-    vpcg_p_kernel<<<gb, 256, 0, st>>>(p, z, rz_new / rz, rz_new, scal, n);
-    DG_LAUNCH_CHECK("vpcg_p_kernel");
+    if (fold_p) {
+      pend = true;  // applied by the next iteration's trace kernel
+      pbeta = rz_new / rz;
+      prz = rz_new;
+    } else {
+      vpcg_p_kernel<<<gb, 256, 0, st>>>(p, z, rz_new / rz, rz_new, scal, n);
+      DG_LAUNCH_CHECK("vpcg_p_kernel");
+    }
     rz = rz_new;
   }
   return DG_OK;

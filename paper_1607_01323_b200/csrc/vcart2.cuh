@@ -109,10 +109,14 @@ __device__ __forceinline__ VlGeo vl_geo(const Geo &g, int64_t e) {
 // nodal -> Gauss-collocated u~ of all CPB cells: x (global -> TT), y (TT ->
 // UG), z (UG -> UG).  The z phase hands each z line of u~ to `zline`
 // (cs, c, x, y, u~ line) while it is in registers.  Ends with a barrier.
+// pz != null: the input is first updated in place, u = pz + beta u (the CG
+// direction update p = z + beta p of the velocity PCG, rounded like
+// vpcg_p_kernel), so u may not be __restrict__
 template <int N, int CB, class ZL>
-__device__ __forceinline__ void vl_to_gauss(const double *__restrict__ u, int64_t e0,
+__device__ __forceinline__ void vl_to_gauss(const double *u, int64_t e0,
                                             int64_t ncells, const double *S, double *sm_cells,
-                                            ZL &&zline) {
+                                            ZL &&zline, const double *pz = nullptr,
+                                            double beta = 0.0) {
   using C = VlCfg<N, CB>;
   constexpr int NN = N * N;
   #pragma unroll
@@ -120,8 +124,17 @@ __device__ __forceinline__ void vl_to_gauss(const double *__restrict__ u, int64_
     const int cs = it / (3 * NN), c = (it / NN) % 3, l = it % NN, y = l % N, z = l / N;
     const int64_t e = e0 + cs;
     double v[N], w[N];
-    if (e < ncells) vl_ld<N>(u + ((int64_t)c * ncells + e) * C::P + (z * N + y) * N, 1, v);
-    else {
+    if (e < ncells) {
+      const int64_t off = ((int64_t)c * ncells + e) * C::P + (z * N + y) * N;
+      vl_ld<N>(u + off, 1, v);
+      if (pz) {
+        double zz[N];
+        vl_ld<N>(pz + off, 1, zz);
+#pragma unroll
+        for (int m = 0; m < N; ++m) v[m] = __dadd_rn(zz[m], __dmul_rn(beta, v[m]));
+        vl_st<N>(const_cast<double *>(u) + off, 1, v);
+      }
+    } else {
 #pragma unroll
       for (int m = 0; m < N; ++m) v[m] = 0.0;
     }
@@ -154,10 +167,14 @@ __device__ __forceinline__ void vl_to_gauss(const double *__restrict__ u, int64_
 
 // Traces of all three components on all six sides at the face Gauss points
 // trc[cell][side][comp][val | dn][f].
+// pz != null: p = pz + beta p in place first (u = p), and scal[0] = rz_new
 template <int N, bool NEED_DN, int CB = 0>
 __global__ void __launch_bounds__(VlCfg<N, CB>::THREADS)
-vl_trace_kernel(const double *__restrict__ u, double *__restrict__ trc, const Geo g,
-                const __grid_constant__ VcTab<N> tab, const int64_t ncells) {
+vl_trace_kernel(const double *u, double *__restrict__ trc, const Geo g,
+                const __grid_constant__ VcTab<N> tab, const int64_t ncells,
+                const double *__restrict__ pz = nullptr, double beta = 0.0,
+                double *__restrict__ scal = nullptr, double rz_new = 0.0) {
+  if (pz && scal && blockIdx.x == 0 && threadIdx.x == 0) scal[0] = rz_new;
   using C = VlCfg<N, CB>;
   constexpr int F = C::F, NN = N * N;
   extern __shared__ double sm[];
@@ -190,7 +207,7 @@ vl_trace_kernel(const double *__restrict__ u, double *__restrict__ trc, const Ge
     emit(e, 4, c, y * N + x, w, sz);
     emit(e, 5, c, y * N + x, w, sz);
   };
-  vl_to_gauss<N, CB>(u, e0, ncells, tab.S, cells, zl);
+  vl_to_gauss<N, CB>(u, e0, ncells, tab.S, cells, zl, pz, beta);
   #pragma unroll
   for (int it = threadIdx.x; it < 6 * C::LINES; it += C::THREADS) {  // y and x lines of u~
     const int ax = it < 3 * C::LINES ? 1 : 0;
