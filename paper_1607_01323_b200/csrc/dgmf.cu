@@ -771,11 +771,8 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
     if (c->n == 4) return launch_laplace7<4, 4, 4, 4, 4>(c, src, dst, tau_scale, part, st);
     // Q4: the half-plane variant (laplace8.cuh, 8x4 tile, 10 warps) -- +3..7 %
     // over laplace7<5,4,4,4,2> from 48^3 to 160^3 (profiles/r02/NOTES.md)
-    if (c->n == 5) {
-      const char *sv = getenv("DG_L8SLAB");  // x-slab tile experiment (per call)
-      if (traced && sv && atoi(sv) == 1) return launch_laplace8<5, 4, 8, 4, 1>(c, src, dst, tau_scale, part, st);
-      return launch_laplace8<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
-    }
+    // (x-slabs too: 4x8 tiles measured slower at every P, profiles/r02/slab_parts.py)
+    if (c->n == 5) return launch_laplace8<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
     if (c->n == 6) return launch_laplace7<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
   }
   if (c->dim == 3 && variant == 6 && c->n == 4)  // register-plane kernel at k = 3 (experiment)

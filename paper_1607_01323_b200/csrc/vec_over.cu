@@ -84,10 +84,8 @@ int vecop_over(dg_ctx *c, const double *src, double *dst, const VecParams &prm, 
     for (int j = 0; j < prm.n_hist; ++j)
       aligned = aligned && (reinterpret_cast<uintptr_t>(prm.hist[j]) & 15) == 0;
     if (!old && aligned) {
-      const int cfg = v ? atoi(v) : 0;  // thread / occupancy A/B at Q5
-      if (c->n == 6 && c->nq_over == 8 && cfg == 2) return launch_vconv2<6, 8, 256, 2>(c, dst, prm, st);
-      if (c->n == 6 && c->nq_over == 8 && cfg == 3) return launch_vconv2<6, 8, 192, 2>(c, dst, prm, st);
-      if (c->n == 6 && c->nq_over == 8 && cfg == 4) return launch_vconv2<6, 8, 128, 4>(c, dst, prm, st);
+      // (measured at Q5: 128 threads x 3 CTAs/SM best; 256 x 2: 0.866 ms,
+      // 192 x 2: 0.848, 128 x 4 (spills): 0.830 vs 0.804 ms)
 #define DG_V2(NN, QQ) \
   if (c->n == NN && c->nq_over == QQ) return launch_vconv2<NN, QQ>(c, dst, prm, st);
       // even N only: the cell and its TMA copies are whole 16 B units

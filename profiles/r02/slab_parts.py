@@ -1,7 +1,8 @@
 """x-slab vmult parts on one GPU: the interior slab of P ranks of the C5 mesh
 (128^3 Q4 walls), ghost traces filled by device copies; times part 1
 (columns not touching a ghost side: overlaps the exchange), part 2 (the rest)
-and the whole-mesh vmult of the same slab size.  DG_L8SLAB=1 selects
+and the whole-mesh vmult of the same slab size.  DG_L8SLAB=1 selected (knob
+removed after this measurement: 4x8 slower at every P)
 4x8 tiles (x-narrow) for slab contexts."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
