@@ -252,9 +252,12 @@ def test_slab_split_equals_full_on_one_gpu(k):
     from paper_1607_01323_b200.spaces import DeviceContext
     from paper_1607_01323_b200.operators import ctypes_ptr, _stream
     ext, counts = ((0, 1),) * 3, (8, 4, 3)
+    # x grading: the ghost cell's h and tau differ from the owner's (the ghost
+    # side coefficients of the split vmult's phase 2)
     for nranks in (2, 3):
-        for per in ((False, False, True), (True, False, True)):
-            mesh = M.build_box_mesh(ext, counts, periodic=per, grading=(0.0, 0.9, 0.0))
+        for per, gx in (((False, False, True), 0.0), ((True, False, True), 0.0),
+                        ((False, False, True), 0.8)):
+            mesh = M.build_box_mesh(ext, counts, periodic=per, grading=(gx, 0.9, 0.0))
             space = DgSpace(mesh, k)
             kinds = {t: ops.NeumannBC(None, None) for t in mesh.boundary_tags()}
             bcs = ops.BoundarySpec(kinds).resolve(space)
