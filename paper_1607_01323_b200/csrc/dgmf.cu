@@ -463,6 +463,10 @@ static int laplace_dispatch_f(dg_ctx *c, const float *src, float *dst, double ta
 
 // number of CTAs (bricks) of the default Laplace configuration: the size of
 // the kEpiDot partial-sum array
+// below kSmallMesh cells (multigrid coarse levels) the v4 bricks replace the
+// column kernel
+constexpr int64_t kSmallMesh = 16384;
+
 // Q3 meshes of at most 2048 cells run the v4 kernel with one cell per CTA:
 // graph-replayed vmults at 4x2x2 / 8x4x4 / 16x8x8 cells take 4.6 / 4.7 / 5.1 us
 // against 5.6 / 6.9 / 6.9 us with 4x4x2 bricks (profiles/r02/small_ab.py)
@@ -492,6 +496,10 @@ template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore>
 static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea = EpiArgs{});
 
+template <int N, int TX, int TY, int NRING, int MINB, bool STAGE = false, int EPI = kEpiStore>
+static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
+                           cudaStream_t st, const EpiArgs &ea = EpiArgs{});
+
 static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, double tau_scale,
                                 int epi, const EpiArgs &ea, cudaStream_t st) {
   c->epi_nparts = laplace_bricks(c);
@@ -517,6 +525,12 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
     if (epi == kEpiCheb) return launch_laplace<3, 4, 1, 1, 1, kEpiCheb>(c, src, dst, tau_scale, 0, st, ea);
     if (epi == kEpiDot) return launch_laplace<3, 4, 1, 1, 1, kEpiDot>(c, src, dst, tau_scale, 0, st, ea);
   }
+  // DG_EPI_COL=1 at Q3: the column kernel's Chebyshev epilogue (laplace7, 4
+  // CTAs/SM): 92.4 vs 88.5 us per step of the v4 bricks on the C4 fine level
+  // -- the CTAs' sweep and epilogue phases stay aligned, little overlap
+  if (col && epi == kEpiCheb && c->dim == 3 && c->n == 4 && c->n_cells >= kSmallMesh &&
+      c->mode[0] != kGhost && c->mode[1] != kGhost)
+    return launch_laplace7<4, 4, 4, 4, 4, false, kEpiCheb>(c, src, dst, tau_scale, 0, st, ea);
   DG_E(3, 3, 4, 4, 4) DG_E(3, 4, 4, 4, 2) DG_E(3, 5, 4, 2, 2) DG_E(3, 6, 2, 2, 1)
   DG_E(2, 3, 16, 8, 1) DG_E(2, 4, 16, 8, 1) DG_E(2, 5, 8, 8, 1) DG_E(2, 6, 8, 8, 1)
 #undef DG_E
@@ -585,15 +599,15 @@ static int chunk_len(int nz, int cols, int slots, int occ, int lcmin, int lcmax)
 
 // z-marching column kernel (laplace7.cuh): units = TX x TY tiles x z-chunks,
 // the chunk length chosen so that ~4 waves of CTAs fill the GPU
-template <int N, int TX, int TY, int NRING, int MINB, bool STAGE = false>
+template <int N, int TX, int TY, int NRING, int MINB, bool STAGE, int EPI>
 static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
-                           cudaStream_t st) {
+                           cudaStream_t st, const EpiArgs &ea) {
   if (t_kname) {
-    *t_kname = kname("laplace7_kernel", {N, TX, TY, NRING, MINB, (int)STAGE});
+    *t_kname = kname("laplace7_kernel", {N, TX, TY, NRING, MINB, (int)STAGE, EPI});
     return DG_OK;
   }
   using C = Lap7Cfg<N, TX, TY, NRING>;
-  auto kern = laplace7_kernel<N, TX, TY, NRING, MINB, STAGE>;
+  auto kern = laplace7_kernel<N, TX, TY, NRING, MINB, STAGE, EPI>;
   static int nsm = 0, occ = 1;
   if (!nsm) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -615,7 +629,8 @@ static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau
   const int lc = chunk_len(nz, cols, nsm * occ, occ, l7_lcmin(4), C::LCMAX);
   const int nch = (nz + lc - 1) / lc;
   kern<<<(unsigned)(cols * nch), C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis),
-                                                            tau_scale, part, zlo, zhi, lc, ntx, nty);
+                                                            tau_scale, part, zlo, zhi, lc, ntx, nty,
+                                                            ea);
   DG_LAUNCH_CHECK("laplace7_kernel");
   return DG_OK;
 }
@@ -709,8 +724,6 @@ static int l7_cfg() {
   const char *e = getenv("DG_L7CFG");  // read per call: A/B within one process
   return e ? atoi(e) : 0;
 }
-
-constexpr int64_t kSmallMesh = 16384;
 
 static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                             cudaStream_t st) {

@@ -165,11 +165,18 @@ __device__ __forceinline__ double l7_pick(int kind, double shfl, double smem_val
   return kind == 0 ? shfl : smem_val;
 }
 
-template <int N, int TX, int TY, int NRING, int MINB, bool STAGE>
+// EPI = kEpiCheb: instead of storing out, each finished layer runs the fused
+// Chebyshev step on its points (laplace.cuh epi_store arithmetic): rc -= out,
+// dnew = a u + b rc / diag, x += dnew; the layer's operands are prefetched
+// into L2 during its z phase and loaded four points per thread at a time.
+// With several CTAs per SM one CTA's epilogue overlaps the others' sweeps.
+template <int N, int TX, int TY, int NRING, int MINB, bool STAGE, int EPI = kEpiStore>
 __global__ void __launch_bounds__(Lap7Cfg<N, TX, TY, NRING>::THREADS, MINB)
 laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g,
                 const __grid_constant__ LapTab<N> T, const double ts, const int part,
-                const int zlo, const int zhi, const int lc, const int ntx, const int nty) {
+                const int zlo, const int zhi, const int lc, const int ntx, const int nty,
+                const EpiArgs ea = EpiArgs{}) {
+  static_assert(EPI == kEpiStore || EPI == kEpiCheb, "laplace7: store or Chebyshev epilogue");
   using C = Lap7Cfg<N, TX, TY, NRING>;
   constexpr int NCT = C::NCT, NP = C::NP, CSTR = C::CSTR, H = N / 2, NE = (N + 1) / 2;
   constexpr int HO = H > 0 ? H : 1;
@@ -461,6 +468,15 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     const bool more = p + 1 < nlay;
     halo_load(more ? iz + 1 : -1);
     halo_stage2(par);
+    if (EPI == kEpiCheb) {  // this layer's epilogue operands -> L2 (128 B lines)
+      const int npts = ex * ey * NP;
+      for (int i = tid * 16; i < 4 * npts; i += 16 * C::THREADS) {
+        const int v = i / npts, j = i - v * npts, cl = j / NP, w = j - cl * NP;
+        const size_t gi = ((size_t)x0 + cl % ex + (size_t)g.nx * (y0 + cl / ex) + nxy * iz) * NP + w;
+        const double *pp = v == 0 ? ea.rc : (v == 1 ? ea.diag : (v == 2 ? ea.x : u));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pp + gi));
+      }
+    }
     {
       const double *q = cc + c * C::CCS;
       const double sfz = q[0], kz = q[1] * hzi, txy = q[2];
@@ -587,9 +603,45 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
         }
       }
     }
-    if (tma) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (tma && EPI == kEpiStore) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();  // B_b: out complete in the slot
-    if (tma) {
+    if (EPI == kEpiCheb) {
+      // cell-major points of the layer: a round of THREADS consecutive points
+      // per load batch, coalesced in global memory
+      constexpr int U = 4;
+      const int npts = ex * ey * NP;
+      for (int j0 = tid; j0 < npts; j0 += U * C::THREADS) {
+        double yv[U], rc[U], dg[U], xv[U], uv[U];
+        size_t gi[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int j = j0 + q * C::THREADS;
+          if (j < npts) {
+            const int cl = j / NP, w = j - cl * NP;
+            const int xx = cl % ex, yy = cl / ex;
+            gi[q] = ((size_t)x0 + xx + (size_t)g.nx * (y0 + yy) + nxy * iz) * NP + w;
+            yv[q] = slot[(xx + TX * yy) * CSTR + w];
+            rc[q] = ea.rc[gi[q]];
+            dg[q] = ea.diag[gi[q]];
+            xv[q] = ea.x[gi[q]];
+            uv[q] = u[gi[q]];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int j = j0 + q * C::THREADS;
+          if (j < npts) {
+            const double r = __dsub_rn(rc[q], yv[q]);
+            const double dn = __dadd_rn(__dmul_rn(ea.a, uv[q]), __dmul_rn(ea.b, __ddiv_rn(r, dg[q])));
+            ea.rc[gi[q]] = r;
+            ea.dnew[gi[q]] = dn;
+            ea.x[gi[q]] = __dadd_rn(xv[q], dn);
+          }
+        }
+      }
+      if (tma) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();  // the slot is reloaded in a later z phase
+    } else if (tma) {
       if (tid < 32) {  // one bulk store per lane of warp 0 (row / cell)
         const int nitem = (N & 1) ? ey : ex * ey;
         for (int i = tid; i < nitem; i += 32) {
@@ -609,7 +661,7 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       __syncthreads();  // the slot is reloaded in the next z phase
     }
   }
-  if (tid < 32 && tma) bulk_wait_read();
+  if (tid < 32 && tma && EPI == kEpiStore) bulk_wait_read();
 }
 
 }  // namespace dg

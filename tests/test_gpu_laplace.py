@@ -367,3 +367,27 @@ def test_fused_chebyshev_smooth_matches_generic(k):
         want = sol.chebyshev_smooth(L, diag, cfg, b, xin)
         got = sol.laplace_chebyshev_smooth(space, bcs, diag, cfg, b, xin)
         assert relerr(got.cpu().numpy(), want.cpu().numpy()) < 1e-13
+
+
+def test_column_chebyshev_epilogue_q3():
+    """The fused Chebyshev step on a Q3 mesh of >= 16384 cells (the v4
+    bricks; with DG_EPI_COL=1 in the environment the column kernel's epilogue,
+    laplace7 kEpiCheb) equals the reference-form chebyshev_smooth with the
+    Laplace callable, partial tiles and walls included (36 x 20 x 24 cells,
+    graded y)."""
+    from paper_1607_01323_b200 import operators as ops
+    mesh = M.build_box_mesh(((0, 1), (0, 2), (0, 1)), (36, 20, 24), periodic=(True, False, True),
+                            grading=(0.0, 1.2, 0.0))
+    space = DgSpace(mesh, 3)
+    bcs = ops.BoundarySpec({"ymin": ops.DirichletBC(None), "ymax": ops.NeumannBC(None, None)}
+                           ).resolve(space)
+    diag = ops.laplace_diagonal(space, bcs)
+    cfg = sol.ChebyshevConfig(5, 20.0, 2.7)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    b = torch.rand(space.n_dofs, dtype=torch.float64, device="cuda", generator=g)
+    x0 = torch.rand(space.n_dofs, dtype=torch.float64, device="cuda", generator=g)
+    L = lambda v: ops.apply_pressure_laplace(space, v, bcs)
+    for xin in (None, x0):
+        want = sol.chebyshev_smooth(L, diag, cfg, b, xin)
+        got = sol.laplace_chebyshev_smooth(space, bcs, diag, cfg, b, xin)
+        assert relerr(got.cpu().numpy(), want.cpu().numpy()) < 1e-13
