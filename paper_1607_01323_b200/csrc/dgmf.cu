@@ -492,7 +492,7 @@ static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau
                            cudaStream_t st, const EpiArgs &ea = EpiArgs{});
 
 // fused-epilogue vmults for the CG / Chebyshev loop (default bricks, k = 2..5)
-template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore>
+template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore, int HSM = 0, int HMAP = 0>
 static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea = EpiArgs{});
 
@@ -636,15 +636,16 @@ static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau
 }
 
 // half-plane column kernel (laplace8.cuh)
-template <int N, int TX, int TY, int NRING, int MINB, int EPI>
+template <int N, int TX, int TY, int NRING, int MINB, int EPI, int HSM, int HMAP>
 static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea) {
   if (t_kname) {
-    *t_kname = kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI});
+    *t_kname = (HSM || HMAP) ? kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI, HSM, HMAP})
+                             : kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI});
     return DG_OK;
   }
-  using C = Lap8Cfg<N, TX, TY, NRING>;
-  auto kern = laplace8_kernel<N, TX, TY, NRING, MINB, EPI>;
+  using C = Lap8Cfg<N, TX, TY, NRING, HSM>;
+  auto kern = laplace8_kernel<N, TX, TY, NRING, MINB, EPI, HSM, HMAP>;
   static int nsm = 0, occ = 1;
   if (!nsm) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -754,7 +755,10 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
       return launch_laplace8<4, 4, 4, 4, 4>(c, src, dst, tau_scale, part, st);
     }
     if (c->n == 5) {
-      return launch_laplace8<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
+      // round-2 session-3 A/B: 1 = halo in registers, round-robin halo items
+      if (cfg == 1) return launch_laplace8<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
+      if (cfg == 2) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 1, 0>(c, src, dst, tau_scale, part, st);
+      return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 1, 1>(c, src, dst, tau_scale, part, st);
     }
     if (c->n == 6) return launch_laplace8<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
   }
@@ -784,8 +788,10 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
     if (c->n == 4) return launch_laplace7<4, 4, 4, 4, 4>(c, src, dst, tau_scale, part, st);
     // Q4: the half-plane variant (laplace8.cuh, 8x4 tile, 10 warps) -- +3..7 %
     // over laplace7<5,4,4,4,2> from 48^3 to 160^3 (profiles/r02/NOTES.md)
-    // (x-slabs too: 4x8 tiles measured slower at every P, profiles/r02/slab_parts.py)
-    if (c->n == 5) return launch_laplace8<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
+    // (x-slabs too: 4x8 tiles measured slower at every P, profiles/r02/slab_parts.py);
+    // halo cells staged by cp.async in shared memory (HSM: 168 -> 144 registers,
+    // no spills) and halo work placed per SM sub-partition (HMAP): +4.8 % at 128^3
+    if (c->n == 5) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 1, 1>(c, src, dst, tau_scale, part, st);
     if (c->n == 6) return launch_laplace7<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
   }
   if (c->dim == 3 && variant == 6 && c->n == 4)  // register-plane kernel at k = 3 (experiment)

@@ -22,15 +22,34 @@
 
 namespace dg {
 
-template <int N, int TX, int TY, int NRING>
+template <int N, int TX, int TY, int NRING, int HSM = 0>
 struct Lap8Cfg : Lap7Cfg<N, TX, TY, NRING> {
+  using B = Lap7Cfg<N, TX, TY, NRING>;
   static constexpr int NCT = TX * TY;
   static constexpr int THREADS = (NCT == 16 ? 32 : 64) * N;
   static constexpr int LMAX = (N + 1) / 2;
-  static_assert(Lap7Cfg<N, TX, TY, NRING>::HITEMS <= THREADS, "one halo item per thread");
+  static_assert(B::HITEMS <= THREADS, "one halo item per thread");
+  // HSM: halo cells staged by cp.async in shared memory ([item][N*N], odd
+  // stride) instead of N*N registers per item thread
+  static constexpr int OFF_HST = ((B::NDBL + 1) / 2) * 2;
+  static constexpr int HSTR = N * N + ((N & 1) ? 0 : 1);
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(HSM ? OFF_HST + B::HITEMS * HSTR : B::NDBL);
   // lane halves run the same lines in lockstep (shuffles inside the line loops)
   static_assert(NCT == 32 || N % 2 == 0, "NCT = 16 halves need even N");
 };
+
+// 8-byte asynchronous global -> shared copy
+__device__ __forceinline__ void l8_cp_async8(double *dst, const double *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// HMAP (N = 5, NCT = 32): halo stage-1 items / stage-2 rows in 32-wide chunks
+// on chosen warps, so that each SM sub-partition (warp % 4) carries about
+// the same z-interval work (lines + halo); -1 = none
+__device__ __forceinline__ int l8_s1_chunk(int w) {
+  constexpr int tab[10] = {-1, 1, -1, -1, -1, -1, 2, 3, 0, -1};
+  return tab[w];
+}
 
 // NCT = 32: warp -> plane * 2 + half.  Odd N: h = 0 warps (N+1)/2 lines;
 // warps {0, 2, 3, 6, 7, ...} take them so that warp % 4 loads stay within one
@@ -47,13 +66,14 @@ __device__ __forceinline__ int l8_role(int w) {
 // EPI: kEpiStore (out by TMA bulk stores) or a CG / Chebyshev epilogue
 // (laplace.cuh epi_store) applied cooperatively to each finished layer of
 // the tile; kEpiDot leaves one partial-sum triple per CTA in ea.partials.
-template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore>
+template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore, int HSM = 0, int HMAP = 0>
 __global__ void __launch_bounds__(Lap8Cfg<N, TX, TY, NRING>::THREADS, MINB)
 laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g,
                 const __grid_constant__ LapTab<N> T, const double ts, const int part,
                 const int zlo, const int zhi, const int lc, const int ntx, const int nty,
                 const EpiArgs ea = EpiArgs{}) {
-  using C = Lap8Cfg<N, TX, TY, NRING>;
+  using C = Lap8Cfg<N, TX, TY, NRING, HSM>;
+  static_assert(HMAP == 0 || (N == 5 && TX * TY == 32), "HMAP tables are for N = 5, 32-cell tiles");
   constexpr int NCT = C::NCT, NP = C::NP, CSTR = C::CSTR, H = N / 2, NE = (N + 1) / 2;
   constexpr int HO = H > 0 ? H : 1;
   constexpr int N2 = N * N;
@@ -201,7 +221,12 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   };
 
   // ---- halo (as laplace7.cuh) ------------------------------------------------
-  const int hit = tid;
+  int hit = tid;
+  if (HMAP) {
+    const int ch = l8_s1_chunk(warp);
+    hit = ch < 0 ? C::THREADS : ch * 32 + lane;
+  }
+  double *const hst = smem + C::OFF_HST + (size_t)min(hit, C::HITEMS - 1) * C::HSTR;
   const bool hx_item = hit < 2 * TY * N;
   int hside = 0, hrow = 0, hpos = 0;
   if (hit < C::HITEMS) {
@@ -243,7 +268,8 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     if (nc >= y0 && nc < y0 + ey) return nullptr;
     return u + ((size_t)xx + (size_t)g.nx * nc + nxy * lay) * NP;
   };
-  double hreg[N][N];
+  constexpr int HR = HSM ? 1 : N;
+  double hreg[HR][N];
   const double *hsrc = nullptr;
   auto halo_load = [&](int lay) {
     hsrc = halo_src(lay);
@@ -251,27 +277,41 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     if (htrace) {  // [z][y][v|g] of the facing end, raw (M_z below)
 #pragma unroll
       for (int z = 0; z < N; ++z) {
-        hreg[z][0] = __ldg(hsrc + (z * N + hpos) * 2);
-        hreg[z][1] = __ldg(hsrc + (z * N + hpos) * 2 + 1);
+        if (HSM) {
+          l8_cp_async8(hst + 2 * z, hsrc + (z * N + hpos) * 2);
+          l8_cp_async8(hst + 2 * z + 1, hsrc + (z * N + hpos) * 2 + 1);
+        } else {
+          hreg[z % HR][0] = __ldg(hsrc + (z * N + hpos) * 2);
+          hreg[z % HR][1] = __ldg(hsrc + (z * N + hpos) * 2 + 1);
+        }
       }
       return;
     }
 #pragma unroll
     for (int z = 0; z < N; ++z)
 #pragma unroll
-      for (int q = 0; q < N; ++q)
-        hreg[z][q] = __ldg(hsrc + z * N2 + (hx_item ? hpos * N + q : q * N + hpos));
+      for (int q = 0; q < N; ++q) {
+        const double *src = hsrc + z * N2 + (hx_item ? hpos * N + q : q * N + hpos);
+        if (HSM) l8_cp_async8(hst + z * N + q, src);
+        else hreg[z % HR][q] = __ldg(src);
+      }
   };
   auto halo_stage1 = [&](int par) {
     if (!hsrc) return;
+    if (HSM) asm volatile("cp.async.wait_all;" ::: "memory");
     double v[N], gg[N], mv[N], mg[N];
 #pragma unroll
     for (int z = 0; z < N; ++z) {
-      double e[NE], o[HO], g0, g1;
-      eo_split<N>(hreg[z], e, o);
+      double e[NE], o[HO], g0, g1, hr[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        if (HSM) hr[q] = (htrace && q >= 2) ? 0.0 : hst[htrace ? 2 * z + q : z * N + q];
+        else hr[q] = hreg[z % HR][q];
+      }
+      eo_split<N>(hr, e, o);
       l7_ends<N>(T, e, o, g0, g1);
-      v[z] = htrace ? hreg[z][0] : (hside ? hreg[z][0] : hreg[z][N - 1]);
-      gg[z] = htrace ? hreg[z][1] : (hside ? g0 : g1);
+      v[z] = htrace ? hr[0] : (hside ? hr[0] : hr[N - 1]);
+      gg[z] = htrace ? hr[1] : (hside ? g0 : g1);
     }
     l7_mass<N>(T, v, mv);
     l7_mass<N>(T, gg, mg);
@@ -283,8 +323,16 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       hp[2 * z + 1] = mg[z];
     }
   };
+  // HMAP: stage-2 row chunks on warps 5, 9, 2, 3, 2 (see l8_s1_chunk)
   auto halo_stage2 = [&](int par) {
-    for (int i = tid; i < C::HROWS; i += C::THREADS) {
+    int i0 = tid, i1 = C::HROWS, di = C::THREADS;
+    if (HMAP) {
+      const int a = warp == 5 ? 0 : warp == 9 ? 1 : warp == 2 ? 2 : warp == 3 ? 3 : -1;
+      i0 = a < 0 ? C::HROWS : a * 32 + lane;
+      di = 64;  // warp 2 also takes chunk 4
+      if (warp != 2) i1 = min(i1, i0 + 1);
+    }
+    for (int i = i0; i < i1; i += di) {
       const int vg = i & 1, rz = i >> 1;
       const int z = rz % N, sj = rz / N;
       if ((sj % TX) >= ex) continue;
