@@ -496,7 +496,7 @@ template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore, int H
 static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea = EpiArgs{});
 
-template <int N, int TX, int TY, int NRING, int MINB, bool STAGE = false, int EPI = kEpiStore>
+template <int N, int TX, int TY, int NRING, int MINB, bool STAGE = false, int EPI = kEpiStore, int HSPL = 0>
 static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea = EpiArgs{});
 
@@ -599,15 +599,16 @@ static int chunk_len(int nz, int cols, int slots, int occ, int lcmin, int lcmax)
 
 // z-marching column kernel (laplace7.cuh): units = TX x TY tiles x z-chunks,
 // the chunk length chosen so that ~4 waves of CTAs fill the GPU
-template <int N, int TX, int TY, int NRING, int MINB, bool STAGE, int EPI>
+template <int N, int TX, int TY, int NRING, int MINB, bool STAGE, int EPI, int HSPL>
 static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea) {
   if (t_kname) {
-    *t_kname = kname("laplace7_kernel", {N, TX, TY, NRING, MINB, (int)STAGE, EPI});
+    *t_kname = HSPL ? kname("laplace7_kernel", {N, TX, TY, NRING, MINB, (int)STAGE, EPI, HSPL})
+                    : kname("laplace7_kernel", {N, TX, TY, NRING, MINB, (int)STAGE, EPI});
     return DG_OK;
   }
   using C = Lap7Cfg<N, TX, TY, NRING>;
-  auto kern = laplace7_kernel<N, TX, TY, NRING, MINB, STAGE, EPI>;
+  auto kern = laplace7_kernel<N, TX, TY, NRING, MINB, STAGE, EPI, HSPL>;
   static int nsm = 0, occ = 1;
   if (!nsm) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -775,6 +776,10 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
       if (cfg == 4) return launch_laplace7<5, 4, 4, 4, 2>(c, src, dst, tau_scale, part, st);
     }
     if (c->n == 6 && cfg == 1) return launch_laplace7<6, 4, 4, 3, 1>(c, src, dst, tau_scale, part, st);
+    // halo rows in one piece (round-2 sessions 1-2 defaults): Q3 96^3 107.1,
+    // Q5 64^3 76.7 GDoF/s vs 109.3 / 86.9 in two halves (3 or 6 parts: Q5 86.8 / 79.4)
+    if (c->n == 6 && cfg == 3) return launch_laplace7<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+    if (c->n == 4 && cfg == 3) return launch_laplace7<4, 4, 4, 4, 4>(c, src, dst, tau_scale, part, st);
     if (c->n == 3) return launch_laplace7<3, 8, 4, 3, 2>(c, src, dst, tau_scale, part, st);
   }
   // default 3D Q3-Q5: the z-marching column kernel (laplace7.cuh); tile, ring
@@ -785,14 +790,15 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
   const bool traced = c->halo_traces && (c->mode[0] == kGhost || c->mode[1] == kGhost);
   if (c->dim == 3 && variant == 0 && !traced && c->n_cells < kSmallMesh) variant = 4;
   if (c->dim == 3 && variant != 4 && variant != 6) {
-    if (c->n == 4) return launch_laplace7<4, 4, 4, 4, 4>(c, src, dst, tau_scale, part, st);
+    // Q3 / Q5: halo item rows loaded in two halves (HSPL; Q5 spills 288 -> 176 B)
+    if (c->n == 4) return launch_laplace7<4, 4, 4, 4, 4, false, kEpiStore, 1>(c, src, dst, tau_scale, part, st);
     // Q4: the half-plane variant (laplace8.cuh, 8x4 tile, 10 warps) -- +3..7 %
     // over laplace7<5,4,4,4,2> from 48^3 to 160^3 (profiles/r02/NOTES.md)
     // (x-slabs too: 4x8 tiles measured slower at every P, profiles/r02/slab_parts.py);
     // halo cells staged by cp.async in shared memory (HSM: 168 -> 144 registers,
     // no spills) and halo work placed per SM sub-partition (HMAP): +4.8 % at 128^3
     if (c->n == 5) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 1, 1>(c, src, dst, tau_scale, part, st);
-    if (c->n == 6) return launch_laplace7<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
+    if (c->n == 6) return launch_laplace7<6, 4, 4, 2, 2, false, kEpiStore, 1>(c, src, dst, tau_scale, part, st);
   }
   if (c->dim == 3 && variant == 6 && c->n == 4)  // register-plane kernel at k = 3 (experiment)
     return launch_laplace6<4, 4, 2, 2>(c, src, dst, tau_scale, part, st);

@@ -170,7 +170,7 @@ __device__ __forceinline__ double l7_pick(int kind, double shfl, double smem_val
 // dnew = a u + b rc / diag, x += dnew; the layer's operands are prefetched
 // into L2 during its z phase and loaded four points per thread at a time.
 // With several CTAs per SM one CTA's epilogue overlaps the others' sweeps.
-template <int N, int TX, int TY, int NRING, int MINB, bool STAGE, int EPI = kEpiStore>
+template <int N, int TX, int TY, int NRING, int MINB, bool STAGE, int EPI = kEpiStore, int HSPL = 0>
 __global__ void __launch_bounds__(Lap7Cfg<N, TX, TY, NRING>::THREADS, MINB)
 laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g,
                 const __grid_constant__ LapTab<N> T, const double ts, const int part,
@@ -357,38 +357,50 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     if (nc >= y0 && nc < y0 + ey) return nullptr;
     return u + ((size_t)xx + (size_t)g.nx * nc + nxy * lay) * NP;
   };
-  double hreg[N][N];
+  // HSPL: the halo item's N z-rows are loaded in HSPL + 1 parts of NH rows
+  // (part j + 1 issued part-way through the z lines, once part j is reduced
+  // to its facing-end value / derivative): NH rows of registers instead of N
+  constexpr int NPART = HSPL + 1;
+  constexpr int NH = (N + NPART - 1) / NPART;
+  double hreg[NH][N];
+  double v[N], gg[N];  // facing-end value / derivative per z row
   const double *hsrc = nullptr;
-  auto halo_load = [&](int lay) {
-    hsrc = halo_src(lay);
+  auto halo_load = [&](int lay, int hf) {
+    if (hf == 0) hsrc = halo_src(lay);
     if (!hsrc) return;
+    const int zb = hf * NH, ze = min(N, zb + NH);
     if (htrace) {  // [z][y][v|g] of the facing end, raw (M_z below)
 #pragma unroll
-      for (int z = 0; z < N; ++z) {
-        hreg[z][0] = __ldg(hsrc + (z * N + hpos) * 2);
-        hreg[z][1] = __ldg(hsrc + (z * N + hpos) * 2 + 1);
+      for (int z = zb; z < ze; ++z) {
+        hreg[z - zb][0] = __ldg(hsrc + (z * N + hpos) * 2);
+        hreg[z - zb][1] = __ldg(hsrc + (z * N + hpos) * 2 + 1);
       }
       return;
     }
 #pragma unroll
-    for (int z = 0; z < N; ++z)
+    for (int z = zb; z < ze; ++z)
 #pragma unroll
       for (int q = 0; q < N; ++q)
         // x halo: [z][x] of plane y = hpos ; y halo: [z][y] of plane x = hpos
-        hreg[z][q] = __ldg(hsrc + z * N2 + (hx_item ? hpos * N + q : q * N + hpos));
+        hreg[z - zb][q] = __ldg(hsrc + z * N2 + (hx_item ? hpos * N + q : q * N + hpos));
+  };
+  auto halo_reduce = [&](int hf) {  // rows of part hf (all rows without HSPL)
+    if (!hsrc) return;
+    const int zb = hf * NH, ze = min(N, zb + NH);
+#pragma unroll
+    for (int z = zb; z < ze; ++z) {
+      double e[NE], o[HO], g0, g1;
+      eo_split<N>(hreg[z - zb], e, o);
+      l7_ends<N>(T, e, o, g0, g1);
+      // lower side (hside 0): the neighbour's upper end faces the tile
+      v[z] = htrace ? hreg[z - zb][0] : (hside ? hreg[z - zb][0] : hreg[z - zb][N - 1]);
+      gg[z] = htrace ? hreg[z - zb][1] : (hside ? g0 : g1);
+    }
   };
   auto halo_stage1 = [&](int par) {
     if (!hsrc) return;
-    double v[N], gg[N], mv[N], mg[N];
-#pragma unroll
-    for (int z = 0; z < N; ++z) {
-      double e[NE], o[HO], g0, g1;
-      eo_split<N>(hreg[z], e, o);
-      l7_ends<N>(T, e, o, g0, g1);
-      // lower side (hside 0): the neighbour's upper end faces the tile
-      v[z] = htrace ? hreg[z][0] : (hside ? hreg[z][0] : hreg[z][N - 1]);
-      gg[z] = htrace ? hreg[z][1] : (hside ? g0 : g1);
-    }
+    halo_reduce(NPART - 1);
+    double mv[N], mg[N];
     l7_mass<N>(T, v, mv);
     l7_mass<N>(T, gg, mg);
     double *hp = hx_item ? hxb + par * C::HXN + ((hside * TY + hrow) * N + hpos) * N * 2
@@ -422,7 +434,12 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     ztv[x] = 0.0;
     ztg[x] = 0.0;
   }
-  halo_load(layer_of(1));
+  halo_load(layer_of(1), 0);
+#pragma unroll
+  for (int j = 1; j < NPART; ++j) {
+    halo_reduce(j - 1);
+    halo_load(layer_of(1), j);
+  }
   if (!tma) __syncthreads();
   if (layer_of(0) >= 0) {
     wait_slot(0);
@@ -466,7 +483,7 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     const int lay_up = layer_of(r + 1);
     wait_slot(r + 1);
     const bool more = p + 1 < nlay;
-    halo_load(more ? iz + 1 : -1);
+    halo_load(more ? iz + 1 : -1, 0);
     halo_stage2(par);
     if (EPI == kEpiCheb) {  // this layer's epilogue operands -> L2 (128 B lines)
       const int npts = ex * ey * NP;
@@ -516,6 +533,12 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
 #pragma unroll
         for (int z = 0; z < N; ++z) up[z * N2 + x] = y[z];
         if (NRING == 3 && x == N / 2) refill();
+#pragma unroll
+        for (int j = 1; j < NPART; ++j)
+          if (x == (j * N) / NPART - 1) {
+            halo_reduce(j - 1);
+            halo_load(more ? iz + 1 : -1, j);
+          }
       }
     }
     if (NRING == 4) refill();
