@@ -503,16 +503,15 @@ static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau
 static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, double tau_scale,
                                 int epi, const EpiArgs &ea, cudaStream_t st) {
   c->epi_nparts = laplace_bricks(c);
-  // DG_EPI_COL=1: the column kernel's cooperative epilogue at Q4 (measured
-  // slower: C2 PCG 0.62 vs 0.57 ms per iteration (0.91 before its loads were
-  // batched per row and prefetched into L2) -- a barrier per layer and
-  // the epilogue vectors streamed by one 320-thread CTA per SM); the v4
-  // bricks' 416-thread CTAs stream them better
-  static const bool col = getenv("DG_EPI_COL") != nullptr;
-  if (col && c->dim == 3 && c->n == 5 && c->n_cells >= 16384 && c->mode[0] != kGhost &&
+  // Column-kernel cooperative epilogues (DG_EPI_COL: unset = Q4 only, 1 = also
+  // Q3, 0 = never).  Q4: laplace8 with the halo in shared memory (HSM) beats
+  // the v4 bricks: C2 Chebyshev-Jacobi PCG 0.537 vs 0.571 ms per iteration
+  // (before HSM 0.62 vs 0.57, profiles/r02/cheb_time.py)
+  static const int col = getenv("DG_EPI_COL") ? atoi(getenv("DG_EPI_COL")) : -1;
+  if (col != 0 && c->dim == 3 && c->n == 5 && c->n_cells >= 16384 && c->mode[0] != kGhost &&
       c->mode[1] != kGhost) {
-    if (epi == kEpiCheb) return launch_laplace8<5, 8, 4, 4, 1, kEpiCheb>(c, src, dst, tau_scale, 0, st, ea);
-    if (epi == kEpiDot) return launch_laplace8<5, 8, 4, 4, 1, kEpiDot>(c, src, dst, tau_scale, 0, st, ea);
+    if (epi == kEpiCheb) return launch_laplace8<5, 8, 4, 4, 1, kEpiCheb, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
+    if (epi == kEpiDot) return launch_laplace8<5, 8, 4, 4, 1, kEpiDot, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
   }
 #define DG_E(D, NN, X, Y, Z)                                                                     \
   if (c->dim == D && c->n == NN) {                                                               \
@@ -527,10 +526,11 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
   }
   // DG_EPI_COL=1 at Q3: the column kernel's Chebyshev epilogue (laplace7, 4
   // CTAs/SM): 92.4 vs 88.5 us per step of the v4 bricks on the C4 fine level
-  // -- the CTAs' sweep and epilogue phases stay aligned, little overlap
-  if (col && epi == kEpiCheb && c->dim == 3 && c->n == 4 && c->n_cells >= kSmallMesh &&
+  // (112.5 vs 106.2 with the split halo) -- the CTAs' sweep and epilogue
+  // phases stay aligned, little overlap
+  if (col == 1 && epi == kEpiCheb && c->dim == 3 && c->n == 4 && c->n_cells >= kSmallMesh &&
       c->mode[0] != kGhost && c->mode[1] != kGhost)
-    return launch_laplace7<4, 4, 4, 4, 4, false, kEpiCheb>(c, src, dst, tau_scale, 0, st, ea);
+    return launch_laplace7<4, 4, 4, 4, 4, false, kEpiCheb, 1>(c, src, dst, tau_scale, 0, st, ea);
   DG_E(3, 3, 4, 4, 4) DG_E(3, 4, 4, 4, 2) DG_E(3, 5, 4, 2, 2) DG_E(3, 6, 2, 2, 1)
   DG_E(2, 3, 16, 8, 1) DG_E(2, 4, 16, 8, 1) DG_E(2, 5, 8, 8, 1) DG_E(2, 6, 8, 8, 1)
 #undef DG_E

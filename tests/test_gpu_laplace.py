@@ -369,16 +369,18 @@ def test_fused_chebyshev_smooth_matches_generic(k):
         assert relerr(got.cpu().numpy(), want.cpu().numpy()) < 1e-13
 
 
-def test_column_chebyshev_epilogue_q3():
-    """The fused Chebyshev step on a Q3 mesh of >= 16384 cells (the v4
-    bricks; with DG_EPI_COL=1 in the environment the column kernel's epilogue,
-    laplace7 kEpiCheb) equals the reference-form chebyshev_smooth with the
-    Laplace callable, partial tiles and walls included (36 x 20 x 24 cells,
-    graded y)."""
+@pytest.mark.parametrize("k", [3, 4])
+def test_column_chebyshev_epilogue(k):
+    """The fused Chebyshev step on a mesh of >= 16384 cells equals the
+    reference-form chebyshev_smooth with the Laplace callable, partial tiles
+    and walls included (36 x 20 x 24 cells, graded y).  Q4: the column
+    kernel's cooperative epilogue (laplace8 kEpiCheb, the default there);
+    Q3: the v4 bricks (laplace7 kEpiCheb with DG_EPI_COL=1 in the
+    environment)."""
     from paper_1607_01323_b200 import operators as ops
     mesh = M.build_box_mesh(((0, 1), (0, 2), (0, 1)), (36, 20, 24), periodic=(True, False, True),
                             grading=(0.0, 1.2, 0.0))
-    space = DgSpace(mesh, 3)
+    space = DgSpace(mesh, k)
     bcs = ops.BoundarySpec({"ymin": ops.DirichletBC(None), "ymax": ops.NeumannBC(None, None)}
                            ).resolve(space)
     diag = ops.laplace_diagonal(space, bcs)
@@ -391,3 +393,25 @@ def test_column_chebyshev_epilogue_q3():
         want = sol.chebyshev_smooth(L, diag, cfg, b, xin)
         got = sol.laplace_chebyshev_smooth(space, bcs, diag, cfg, b, xin)
         assert relerr(got.cpu().numpy(), want.cpu().numpy()) < 1e-13
+
+
+def test_column_epilogue_pcg_q4():
+    """Fused Chebyshev-Jacobi PCG on a Q4 mesh of >= 16384 cells (laplace8
+    kEpiDot / kEpiCheb epilogues) against the reference-signature pcg with
+    device callables: same iteration count, histories and solution."""
+    mesh = M.build_box_mesh(((0, 1), (0, 2), (0, 1)), (36, 20, 24), periodic=(True, False, True),
+                            grading=(0.0, 1.2, 0.0))
+    space = DgSpace(mesh, 4)
+    bcs = ops.BoundarySpec({"ymin": ops.DirichletBC(None),
+                            "ymax": ops.DirichletBC(None)}).resolve(space)
+    diag = ops.laplace_diagonal(space, bcs)
+    b = sol.zero_mean_project_dual(space, dev(np.random.default_rng(6).standard_normal(space.n_dofs)))
+    L = lambda v: ops.apply_pressure_laplace(space, v, bcs)
+    op = lambda v: sol.zero_mean_project_dual(space, L(v))
+    cfg = sol.ChebyshevConfig(5, 20.0, 2.8)
+    x1, s1 = sol.pcg(op, lambda r: sol.chebyshev_smooth(L, diag, cfg, r), b, rel_tol=1e-8)
+    x2, s2 = sol.laplace_pcg(space, bcs, b, project_dual=True, cheb=cfg, diag=diag, rel_tol=1e-8)
+    assert s1.converged and s2.converged
+    assert s1.iterations == s2.iterations
+    np.testing.assert_allclose(s1.history, s2.history, rtol=1e-7, atol=1e-10 * s1.history[0])
+    assert relerr(host(x1), host(x2)) < 1e-8
