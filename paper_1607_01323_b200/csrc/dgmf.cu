@@ -510,6 +510,7 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
   static const int col = getenv("DG_EPI_COL") ? atoi(getenv("DG_EPI_COL")) : -1;
   if (col != 0 && c->dim == 3 && c->n == 5 && c->n_cells >= 16384 && c->mode[0] != kGhost &&
       c->mode[1] != kGhost) {
+    // (HSM 1 here: C2 0.535 / 0.537 ms per iteration vs 0.549 with HSM 2)
     if (epi == kEpiCheb) return launch_laplace8<5, 8, 4, 4, 1, kEpiCheb, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
     if (epi == kEpiDot) return launch_laplace8<5, 8, 4, 4, 1, kEpiDot, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
   }
@@ -757,9 +758,11 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
     }
     if (c->n == 5) {
       // round-2 session-3 A/B: 1 = halo in registers, round-robin halo items
+      // (session 2), 2 = halo items staged per thread by cp.async, 3 = + HMAP
       if (cfg == 1) return launch_laplace8<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
       if (cfg == 2) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 1, 0>(c, src, dst, tau_scale, part, st);
-      return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 1, 1>(c, src, dst, tau_scale, part, st);
+      if (cfg == 3) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 1, 1>(c, src, dst, tau_scale, part, st);
+      return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
     }
     if (c->n == 6) return launch_laplace8<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
   }
@@ -795,9 +798,11 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
     // Q4: the half-plane variant (laplace8.cuh, 8x4 tile, 10 warps) -- +3..7 %
     // over laplace7<5,4,4,4,2> from 48^3 to 160^3 (profiles/r02/NOTES.md)
     // (x-slabs too: 4x8 tiles measured slower at every P, profiles/r02/slab_parts.py);
-    // halo cells staged by cp.async in shared memory (HSM: 168 -> 144 registers,
-    // no spills) and halo work placed per SM sub-partition (HMAP): +4.8 % at 128^3
-    if (c->n == 5) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 1, 1>(c, src, dst, tau_scale, part, st);
+    // halo cells staged in shared memory (HSM: no halo registers, no spills;
+    // HSM 2: whole cells copied by coalesced warp-wide cp.async from a per-CTA
+    // source table) and halo work placed per SM sub-partition (HMAP); per-layer
+    // set-up hoisted: 120.8 -> 133.7 GDoF/s at 128^3 (profiles/r02/NOTES.md)
+    if (c->n == 5) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
     if (c->n == 6) return launch_laplace7<6, 4, 4, 2, 2, false, kEpiStore, 1>(c, src, dst, tau_scale, part, st);
   }
   if (c->dim == 3 && variant == 6 && c->n == 4)  // register-plane kernel at k = 3 (experiment)

@@ -33,7 +33,15 @@ struct Lap8Cfg : Lap7Cfg<N, TX, TY, NRING> {
   // stride) instead of N*N registers per item thread
   static constexpr int OFF_HST = ((B::NDBL + 1) / 2) * 2;
   static constexpr int HSTR = N * N + ((N & 1) ? 0 : 1);
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(HSM ? OFF_HST + B::HITEMS * HSTR : B::NDBL);
+  // HSM = 2: the halo CELLS (2 (TX + TY) per layer) copied whole by the
+  // stage-1 warps, lanes on consecutive doubles (coalesced, one address per
+  // cell), into [cell][HCS]; per-cell source table [cell]{p0, layer stride, n}
+  static constexpr int HCELLS = 2 * (TX + TY);
+  static constexpr int HCS = N * N * N + ((N & 1) ? 2 : 1);
+  static constexpr int OFF_HTAB = OFF_HST + HCELLS * HCS;
+  static constexpr size_t SMEM =
+      sizeof(double) * (size_t)(HSM == 2 ? OFF_HTAB + 3 * HCELLS
+                                         : (HSM ? OFF_HST + B::HITEMS * HSTR : B::NDBL));
   // lane halves run the same lines in lockstep (shuffles inside the line loops)
   static_assert(NCT == 32 || N % 2 == 0, "NCT = 16 halves need even N");
 };
@@ -87,6 +95,7 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   double *const cc = smem + C::OFF_CC;
   uint64_t *const bar = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
   const double *const zero = smem + C::OFF_ZERO;
+  unsigned long long *const htab = reinterpret_cast<unsigned long long *>(smem + C::OFF_HTAB);
 
   // ---- unit: tile (tx, ty) x z-chunk -------------------------------------
   int unit = blockIdx.x;
@@ -186,8 +195,51 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
                    !(reinterpret_cast<uintptr_t>(out) & 15);
   if (tid == 0)
     for (int i = 0; i < NRING; ++i) mbar_init(&bar[i], 1);
+  if (HSM == 2 && tid < C::HCELLS) {  // halo cell sources of this tile (layer 0 + layer stride)
+    const double *p0 = nullptr;
+    size_t lst = 0;
+    int n = 0;
+    if (tid < 2 * TY) {  // x neighbours (side, row)
+      const int side = tid / TY, row = tid % TY, yy = y0 + row;
+      int nc = side ? x0 + ex : x0 - 1;
+      bool ok = row < ey;
+      if (ok && (nc < 0 || nc >= g.nx)) {
+        const int m = g.mode[side];
+        if (m == kWrap) nc = side ? 0 : g.nx - 1;
+        else if (m == kGhost) {
+          const int cs = g.ghost_traces ? 2 * N2 : NP;
+          p0 = g.ghost[side] + (size_t)yy * cs;
+          lst = (size_t)g.ny * cs;
+          n = cs;
+          ok = false;
+        } else ok = false;
+      }
+      if (ok && !(nc >= x0 && nc < x0 + ex)) {
+        p0 = u + ((size_t)nc + (size_t)g.nx * yy) * NP;
+        lst = nxy * NP;
+        n = NP;
+      }
+    } else {  // y neighbours (side, column)
+      const int c8 = tid - 2 * TY, side = c8 / TX, col = c8 % TX, xx = x0 + col;
+      int nc = side ? y0 + ey : y0 - 1;
+      bool ok = col < ex;
+      if (ok && (nc < 0 || nc >= g.ny)) {
+        if (g.mode[2 + side] == kWrap) nc = side ? 0 : g.ny - 1;
+        else ok = false;
+      }
+      if (ok && !(nc >= y0 && nc < y0 + ey)) {
+        p0 = u + ((size_t)xx + (size_t)g.nx * nc) * NP;
+        lst = nxy * NP;
+        n = NP;
+      }
+    }
+    htab[3 * tid] = reinterpret_cast<unsigned long long>(p0);
+    htab[3 * tid + 1] = lst;
+    htab[3 * tid + 2] = n;
+  }
   __syncthreads();
   auto issue = [&](int r) {
+    if (HSM == 2 && tma && tid >= 32) return;  // only warp 0 takes part with TMA
     if (r > nlay + 1) return;
     const int lay = layer_of(r);
     uint64_t *b = &bar[r % NRING];
@@ -221,11 +273,12 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   };
 
   // ---- halo (as laplace7.cuh) ------------------------------------------------
+  static_assert(HSM != 2 || (HMAP && N == 5 && TX * TY == 32), "HSM 2: 6 cells of 5 items per warp");
+  const int hch = HMAP ? l8_s1_chunk(warp) : -1;  // stage-1 chunk of this warp
   int hit = tid;
-  if (HMAP) {
-    const int ch = l8_s1_chunk(warp);
-    hit = ch < 0 ? C::THREADS : ch * 32 + lane;
-  }
+  if (HMAP) hit = hch < 0 ? C::THREADS : (HSM == 2 ? (lane < 30 ? hch * 30 + lane : C::THREADS)
+                                                    : hch * 32 + lane);
+  double *const hcell = smem + C::OFF_HST;  // HSM 2: staged halo cells
   double *const hst = smem + C::OFF_HST + (size_t)min(hit, C::HITEMS - 1) * C::HSTR;
   const bool hx_item = hit < 2 * TY * N;
   int hside = 0, hrow = 0, hpos = 0;
@@ -271,7 +324,29 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   constexpr int HR = HSM ? 1 : N;
   double hreg[HR][N];
   const double *hsrc = nullptr;
+  const int hmy = hit < C::HITEMS ? hit / N : 0;  // HSM 2: this item's cell
   auto halo_load = [&](int lay) {
+    if (HSM == 2) {
+      hsrc = nullptr;
+      if (hch < 0 || lay < 0) return;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        const int cid = hch * 6 + j;
+        if (cid >= C::HCELLS) break;
+        const int n = (int)htab[3 * cid + 2];
+        if (n == 0) continue;
+        const double *src = reinterpret_cast<const double *>(htab[3 * cid]) + (size_t)lay * htab[3 * cid + 1];
+        double *dst = hcell + cid * C::HCS;
+#pragma unroll
+        for (int m = 0; m < (NP + 31) / 32; ++m)
+          if (lane + 32 * m < n) l8_cp_async8(dst + lane + 32 * m, src + lane + 32 * m);
+      }
+      if (hit < C::HITEMS && htab[3 * hmy + 2] != 0) {
+        hsrc = hcell + hmy * C::HCS;  // flag + staged cell
+        htrace = htab[3 * hmy + 2] == (unsigned long long)(2 * N2);
+      }
+      return;
+    }
     hsrc = halo_src(lay);
     if (!hsrc) return;
     if (htrace) {  // [z][y][v|g] of the facing end, raw (M_z below)
@@ -297,15 +372,23 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       }
   };
   auto halo_stage1 = [&](int par) {
+    if (HSM == 2 && hch >= 0) {  // the warp's cells, copied by all its lanes
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+    }
     if (!hsrc) return;
-    if (HSM) asm volatile("cp.async.wait_all;" ::: "memory");
+    if (HSM == 1) asm volatile("cp.async.wait_all;" ::: "memory");
     double v[N], gg[N], mv[N], mg[N];
 #pragma unroll
     for (int z = 0; z < N; ++z) {
       double e[NE], o[HO], g0, g1, hr[N];
 #pragma unroll
       for (int q = 0; q < N; ++q) {
-        if (HSM) hr[q] = (htrace && q >= 2) ? 0.0 : hst[htrace ? 2 * z + q : z * N + q];
+        if (HSM == 2)
+          hr[q] = (htrace && q >= 2) ? 0.0
+                  : hcell[hmy * C::HCS +
+                          (htrace ? (z * N + hpos) * 2 + q : z * N2 + (hx_item ? hpos * N + q : q * N + hpos))];
+        else if (HSM) hr[q] = (htrace && q >= 2) ? 0.0 : hst[htrace ? 2 * z + q : z * N + q];
         else hr[q] = hreg[z % HR][q];
       }
       eo_split<N>(hr, e, o);
@@ -324,7 +407,35 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     }
   };
   // HMAP: stage-2 row chunks on warps 5, 9, 2, 3, 2 (see l8_s1_chunk)
+  // HSM 2: this thread's stage-2 rows (at most 2 with HMAP) resolved once
+  int s2off[2] = {-1, -1};
+  if (HSM == 2) {
+    const int a = warp == 5 ? 0 : warp == 9 ? 1 : warp == 2 ? 2 : warp == 3 ? 3 : -1;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int i = a < 0 ? C::HROWS : a * 32 + lane + 64 * rr;
+      if (i < C::HROWS && (rr == 0 || warp == 2)) {
+        const int vg = i & 1, rz = i >> 1;
+        const int z = rz % N, sj = rz / N;
+        if ((sj % TX) < ex) s2off[rr] = sj * N * N * 2 + z * 2 + vg;
+      }
+    }
+  }
   auto halo_stage2 = [&](int par) {
+    if (HSM == 2) {
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        if (s2off[rr] < 0) continue;
+        double *row = hyb + par * C::HYN + s2off[rr];
+        double v[N], y[N];
+#pragma unroll
+        for (int x = 0; x < N; ++x) v[x] = row[x * N * 2];
+        l7_mass<N>(T, v, y);
+#pragma unroll
+        for (int x = 0; x < N; ++x) row[x * N * 2] = y[x];
+      }
+      return;
+    }
     int i0 = tid, i1 = C::HROWS, di = C::THREADS;
     if (HMAP) {
       const int a = warp == 5 ? 0 : warp == 9 ? 1 : warp == 2 ? 2 : warp == 3 ? 3 : -1;
@@ -414,8 +525,11 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       const double taue = txy + tz;
       const int kz0 = iz == 0 ? (g.mode[4] == kWrap ? 0 : g.mode[4]) : 0;
       const int kz1 = iz == g.nz - 1 ? (g.mode[5] == kWrap ? 0 : g.mode[5]) : 0;
-      const Side7 s0 = side7(kz0, txy + fmax(tz, az[-4 + 2]), taue, sfz, hzi, az[-4 + 1], 1.0, ts);
-      const Side7 s1 = side7(kz1, txy + fmax(tz, az[4 + 2]), taue, sfz, hzi, az[4 + 1], -1.0, ts);
+      // tau of the z faces: max of the two cells' z parts (plain compare: no NaN
+      // fix-up sequence as in fmax)
+      const double tzl = az[-4 + 2], tzu = az[4 + 2];
+      const Side7 s0 = side7(kz0, txy + (tz > tzl ? tz : tzl), taue, sfz, hzi, az[-4 + 1], 1.0, ts);
+      const Side7 s1 = side7(kz1, txy + (tz > tzu ? tz : tzu), taue, sfz, hzi, az[4 + 1], -1.0, ts);
       double *up = slot + c * CSTR + s * N + l0;
       double *rp = rbuf + c * CSTR + s * N + l0;
       const double *lp = ring + ((r + 1) % NRING) * C::LAYER + c * CSTR + s * N + l0;
