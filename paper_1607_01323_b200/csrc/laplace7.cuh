@@ -276,6 +276,7 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   __syncthreads();
   // all threads call issue(); thread 0 issues TMA, or all threads copy
   auto issue = [&](int r) {
+    if (tma && tid >= 32) return;  // TMA: warp 0 alone (no per-warp layer arithmetic)
     if (r > nlay + 1) return;
     const int lay = layer_of(r);
     uint64_t *b = &bar[r % NRING];
@@ -411,7 +412,24 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       hp[2 * z + 1] = mg[z];
     }
   };
+  // one stage-2 row per thread (the Q3 / Q5 tiles): its offset resolved once
+  int s2off = -1;
+  if (C::HROWS <= C::THREADS && tid < C::HROWS) {
+    const int vg = tid & 1, rz = tid >> 1, z = rz % N, sj = rz / N;
+    if ((sj % TX) < ex) s2off = sj * N * N * 2 + z * 2 + vg;
+  }
   auto halo_stage2 = [&](int par) {  // y halo: M_x along x, rows (side, jx, z, v|g)
+    if (C::HROWS <= C::THREADS) {
+      if (s2off < 0) return;
+      double *row = hyb + par * C::HYN + s2off;
+      double v[N], y[N];
+#pragma unroll
+      for (int x = 0; x < N; ++x) v[x] = row[x * N * 2];
+      l7_mass<N>(T, v, y);
+#pragma unroll
+      for (int x = 0; x < N; ++x) row[x * N * 2] = y[x];
+      return;
+    }
     for (int i = tid; i < C::HROWS; i += C::THREADS) {
       const int vg = i & 1, rz = i >> 1;
       const int z = rz % N, sj = rz / N;  // sj = side * TX + jx
@@ -500,8 +518,10 @@ laplace7_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       const double taue = txy + tz;
       const int kz0 = iz == 0 ? (g.mode[4] == kWrap ? 0 : g.mode[4]) : 0;
       const int kz1 = iz == g.nz - 1 ? (g.mode[5] == kWrap ? 0 : g.mode[5]) : 0;
-      const Side7 s0 = side7(kz0, txy + fmax(tz, az[-4 + 2]), taue, sfz, hzi, az[-4 + 1], 1.0, ts);
-      const Side7 s1 = side7(kz1, txy + fmax(tz, az[4 + 2]), taue, sfz, hzi, az[4 + 1], -1.0, ts);
+      // z-face tau = max of the two cells' z parts (plain compare, no fmax NaN fix-up)
+      const double tzl = az[-4 + 2], tzu = az[4 + 2];
+      const Side7 s0 = side7(kz0, txy + (tz > tzl ? tz : tzl), taue, sfz, hzi, az[-4 + 1], 1.0, ts);
+      const Side7 s1 = side7(kz1, txy + (tz > tzu ? tz : tzu), taue, sfz, hzi, az[4 + 1], -1.0, ts);
       double *up = slot + cs * CSTR + s * N;
       double *rp = rbuf + cs * CSTR + s * N;
       const double *lp = ring + ((r + 1) % NRING) * C::LAYER + cs * CSTR + s * N;
