@@ -67,6 +67,17 @@ __device__ __forceinline__ void cp_async8(double *dst, const double *src, bool v
                : "memory");
 }
 
+// TMA bulk store of a shared-memory block (16-byte aligned, size a multiple
+// of 16) and the wait until the engine has read it
+__device__ __forceinline__ void cv2_s2g(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cv2_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void cv2_xyz(const Geo &g, int64_t e, int &ix, int &iy, int &iz) {
   const unsigned ei = (unsigned)e, nx = (unsigned)g.nx, ny = (unsigned)g.ny;
   const unsigned q = ei / nx;
@@ -113,7 +124,11 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
   __syncthreads();
 
   // item w = k nh + lev: cell blockIdx.x + k gridDim.x, history level lev
-  auto item_cell = [&](int64_t w) { return (int64_t)blockIdx.x + (w / nh) * gridDim.x; };
+  // items per CTA fit 32 bits: 32-bit division by nh (a 64-bit one cost ~100
+  // instructions of warp 0 per item)
+  auto item_cell = [&](int64_t w) {
+    return (int64_t)blockIdx.x + (int64_t)((unsigned)w / (unsigned)nh) * gridDim.x;
+  };
   auto side_info = [&](int64_t w) {  // threads 0-5
     if (tid < 6) {
       int ix, iy, iz;
@@ -126,7 +141,7 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
   // TMA of item w's own cell into buffer w & 1 (one thread)
   auto issue_own = [&](int64_t w) {
     const int64_t e = item_cell(w);
-    const double *src = p_hist[(int)(w % nh)];  // one thread, once per item
+    const double *src = p_hist[(int)((unsigned)w % (unsigned)nh)];  // one thread, once per item
     double *dst = sm + ((w & 1) ? C::SU1 : C::SU0);
     uint64_t *bar = &bars[w & 1];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -141,6 +156,21 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
     const double *src = p_hist[lv];
     const int sl = (int)(w & 1);
     double *snb = sm + C::NB + sl * 18 * FN;
+    if (3 * FN <= T) {  // thread -> (component, face node); one side per pass
+      const int nc_f = tid % FN, nc_c = tid / FN, nc_fs = nc_f / N, nc_fa = nc_f % N;
+      if (nc_c < 3) {
+#pragma unroll
+        for (int side = 0; side < 6; ++side) {
+          const bool in = skind[sl][side] == 0;
+          const double *p = in ? src + ((int64_t)nc_c * ncells + snbr[sl][side]) * NP +
+                                     cv_end_node<N>(side >> 1, (side & 1) ^ 1, nc_fs, nc_fa)
+                               : src;
+          cp_async8(snb + (side * 3 + nc_c) * FN + nc_f, p, in);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      return;
+    }
     for (int i = tid; i < 18 * FN; i += T) {
       const int side = i / (3 * FN), c = (i / FN) % 3, f = i % FN;
       const bool in = skind[sl][side] == 0;
@@ -245,6 +275,7 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
       cv_store<N>(ra + (((a * 2 + 0) * N + z) * N) * P1 + qx, P1, ya);
       cv_store<N>(ra + (((a * 2 + 1) * N + z) * N) * P1 + qx, P1, yb);
     }
+    if (tid == 0) cv2_wait_read();  // the previous cell's bulk store has read so
     __syncthreads();
     // x lines: out_a (=, first level; += later) S^T A_a + D^T B_a, and (same
     // phase, independent) the fast tangential sweep of the own / neighbour end
@@ -345,6 +376,7 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
 #pragma unroll
         for (int sl = 0; sl < N; ++sl) so[a * NP + cv_end_node<N>(d, s, sl, fa)] += yo[sl];
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // so -> bulk store
       __syncthreads();
     }
 
@@ -378,11 +410,22 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
 #pragma unroll
           for (int x = 0; x < N; ++x) o[x] += yo[x];
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
       }
-      for (int i = tid; i < 3 * NP; i += T) {
-        const int c = i / NP, o = i % NP;
-        out[((int64_t)c * ncells + e) * NP + o] = so[i];
+      if ((NP * sizeof(double)) % 16 == 0 && (smem_u32(so) & 15) == 0 &&
+          (reinterpret_cast<uintptr_t>(out) & 15) == 0) {  // 3 TMA bulk stores
+        if (tid == 0) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            cv2_s2g(out + ((int64_t)c * ncells + e) * NP, so + c * NP, (uint32_t)(NP * sizeof(double)));
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      } else {
+        for (int i = tid; i < 3 * NP; i += T) {
+          const int c = i / NP, o = i % NP;
+          out[((int64_t)c * ncells + e) * NP + o] = so[i];
+        }
       }
     }
     // side info of item w + 2 into this item's slot (read by the LF phase
@@ -395,6 +438,7 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
       e += gridDim.x;
     }
   }
+  if (tid == 0) cv2_wait_read();  // the last bulk store has read so
 }
 
 }  // namespace dg

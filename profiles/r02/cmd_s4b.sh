@@ -1,0 +1,4 @@
+for i in 1 2; do
+echo base; DG_LIB=$PWD/profiles/r02/libdgmf_base.so timeout 100 python profiles/r02/c3_ab.py 0 2>&1 | tail -1
+echo new; timeout 100 python profiles/r02/c3_ab.py 0 2>&1 | tail -1
+done
