@@ -135,7 +135,7 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
       cv2_xyz(g, item_cell(w), ix, iy, iz);
       int64_t nb;
       skind[w & 1][tid] = cv2_side(g, ix, iy, iz, tid, nb);
-      snbr[w & 1][tid] = nb;
+      snbr[w & 1][tid] = nb * NP;  // element offset of the neighbour cell
     }
   };
   // TMA of item w's own cell into buffer w & 1 (one thread)
@@ -159,11 +159,11 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
     if (3 * FN <= T) {  // thread -> (component, face node); one side per pass
       const int nc_f = tid % FN, nc_c = tid / FN, nc_fs = nc_f / N, nc_fa = nc_f % N;
       if (nc_c < 3) {
+        const double *srcc = src + (int64_t)nc_c * ncells * NP;  // this thread's component
 #pragma unroll
         for (int side = 0; side < 6; ++side) {
           const bool in = skind[sl][side] == 0;
-          const double *p = in ? src + ((int64_t)nc_c * ncells + snbr[sl][side]) * NP +
-                                     cv_end_node<N>(side >> 1, (side & 1) ^ 1, nc_fs, nc_fa)
+          const double *p = in ? srcc + snbr[sl][side] + cv_end_node<N>(side >> 1, (side & 1) ^ 1, nc_fs, nc_fa)
                                : src;
           cp_async8(snb + (side * 3 + nc_c) * FN + nc_f, p, in);
         }
@@ -174,7 +174,7 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
     for (int i = tid; i < 18 * FN; i += T) {
       const int side = i / (3 * FN), c = (i / FN) % 3, f = i % FN;
       const bool in = skind[sl][side] == 0;
-      const double *p = in ? src + ((int64_t)c * ncells + snbr[sl][side]) * NP +
+      const double *p = in ? src + (int64_t)c * ncells * NP + snbr[sl][side] +
                                  cv_end_node<N>(side >> 1, (side & 1) ^ 1, f / N, f % N)
                            : src;
       cp_async8(snb + i, p, in);
