@@ -762,7 +762,11 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
       if (cfg == 1) return launch_laplace8<5, 8, 4, 4, 1>(c, src, dst, tau_scale, part, st);
       if (cfg == 2) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 1, 0>(c, src, dst, tau_scale, part, st);
       if (cfg == 3) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 1, 1>(c, src, dst, tau_scale, part, st);
-      return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
+      // 4 / 5 / 6: 8x4 ring 3, 4x8 ring 4, 8x4 ring 4 (session-3 HSM 2 configurations)
+      if (cfg == 4) return launch_laplace8<5, 8, 4, 3, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
+      if (cfg == 5) return launch_laplace8<5, 4, 8, 4, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
+      if (cfg == 6) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
+      return launch_laplace8<5, 4, 8, 3, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
     }
     if (c->n == 6) return launch_laplace8<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
   }
@@ -801,8 +805,9 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
     // halo cells staged in shared memory (HSM: no halo registers, no spills;
     // HSM 2: whole cells copied by coalesced warp-wide cp.async from a per-CTA
     // source table) and halo work placed per SM sub-partition (HMAP); per-layer
-    // set-up hoisted: 120.8 -> 133.7 GDoF/s at 128^3 (profiles/r02/NOTES.md)
-    if (c->n == 5) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
+    // set-up hoisted: 120.8 -> 133.7 GDoF/s at 128^3; 4x8 tile, ring 3: 136.3
+    // (+1.6-1.9 % at 64^3-160^3 and on the x-slabs of P = 1-8; profiles/r02/NOTES.md)
+    if (c->n == 5) return launch_laplace8<5, 4, 8, 3, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
     if (c->n == 6) return launch_laplace7<6, 4, 4, 2, 2, false, kEpiStore, 1>(c, src, dst, tau_scale, part, st);
   }
   if (c->dim == 3 && variant == 6 && c->n == 4)  // register-plane kernel at k = 3 (experiment)
