@@ -511,6 +511,16 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
   if (col != 0 && c->dim == 3 && c->n == 5 && c->n_cells >= 16384 && c->mode[0] != kGhost &&
       c->mode[1] != kGhost) {
     // (HSM 1 here: C2 0.535 / 0.537 ms per iteration vs 0.549 with HSM 2)
+    const char *ec = getenv("DG_EPI_CFG");  // read per call: A/B
+    const int ecfg = ec ? atoi(ec) : 0;
+    if (ecfg == 1) {
+      if (epi == kEpiCheb) return launch_laplace8<5, 4, 8, 3, 1, kEpiCheb, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
+      if (epi == kEpiDot) return launch_laplace8<5, 4, 8, 3, 1, kEpiDot, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
+    }
+    if (ecfg == 2) {
+      if (epi == kEpiCheb) return launch_laplace8<5, 4, 8, 3, 1, kEpiCheb, 2, 1>(c, src, dst, tau_scale, 0, st, ea);
+      if (epi == kEpiDot) return launch_laplace8<5, 4, 8, 3, 1, kEpiDot, 2, 1>(c, src, dst, tau_scale, 0, st, ea);
+    }
     if (epi == kEpiCheb) return launch_laplace8<5, 8, 4, 4, 1, kEpiCheb, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
     if (epi == kEpiDot) return launch_laplace8<5, 8, 4, 4, 1, kEpiDot, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
   }
