@@ -233,12 +233,10 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
     }
     __syncthreads();
     // G_ab = beta u_a u_b JxW and its z test contraction (vconv.cuh jobs)
-    for (int l = tid; l < 8 * NQ2; l += T) {
-      const int job = l / NQ2, qxy = l % NQ2;
+    auto gjob = [&](const int job, const int qxy, const double wxy) {
       const int a = job == 1 ? 1 : (job == 2 ? 2 : (job >= 6 ? 1 : 0));
       const int b = job == 0 ? 0 : (job == 1 || job == 3 ? 1 : 2);
       const bool dz = job == 2 || job == 4 || job == 6;
-      const double wxy = beta * det * W[qxy % NQ] * W[qxy / NQ];
       double ua[NQ], ub[NQ], gz[NQ], zo[N];
       cv_load<NQ>(uq + a * QP + qxy, NQ2, ua);
       cv_load<NQ>(uq + b * QP + qxy, NQ2, ub);
@@ -256,6 +254,20 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
         double *z2 = rb + (1 * 3 + 0) * N * NQ2 + qxy;
 #pragma unroll
         for (int z = 0; z < N; ++z) z2[z * NQ2] = sc[0] * zo[z];
+      }
+        };
+    if (T % NQ2 == 0 && (8 * NQ2) % T == 0) {
+      // T / NQ2 jobs per pass: this thread's point and its job residue are
+      // fixed, the job index is a compile-time offset (no select chains)
+      constexpr int JP = T % NQ2 == 0 ? T / NQ2 : 1;
+      const int jh = tid / NQ2, qxy = tid - jh * NQ2;
+      const double wxy = beta * det * W[qxy % NQ] * W[qxy / NQ];
+#pragma unroll
+      for (int jp = 0; jp < 8 / JP; ++jp) gjob(jp * JP + jh, qxy, wxy);
+    } else {
+      for (int l = tid; l < 8 * NQ2; l += T) {
+        const int job = l / NQ2, qxy = l % NQ2;
+        gjob(job, qxy, beta * det * W[qxy % NQ] * W[qxy / NQ]);
       }
     }
     __syncthreads();
