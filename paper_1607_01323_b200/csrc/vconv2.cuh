@@ -78,6 +78,11 @@ __device__ __forceinline__ void cv2_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+template <int V>
+struct Cv2Job {  // compile-time job index of the G_ab phase
+  static constexpr int value = V;
+};
+
 __device__ __forceinline__ void cv2_xyz(const Geo &g, int64_t e, int &ix, int &iy, int &iz) {
   const unsigned ei = (unsigned)e, nx = (unsigned)g.nx, ny = (unsigned)g.ny;
   const unsigned q = ei / nx;
@@ -256,7 +261,49 @@ vconv2_kernel(double *__restrict__ out, const Geo g, const __grid_constant__ Qua
         for (int z = 0; z < N; ++z) z2[z * NQ2] = sc[0] * zo[z];
       }
         };
-    if (T % NQ2 == 0 && (8 * NQ2) % T == 0) {
+    // two jobs per pass (T = 2 NQ2): the warp-uniform job residue picks one of
+    // two fully compile-time job sequences; the three component lines at this
+    // point are loaded once for its four jobs
+    auto gjob_c = [&](auto JC, const double (&uc)[3][NQ], const int qxy, const double wxy) {
+      constexpr int job = decltype(JC)::value;
+      constexpr int a = job == 1 ? 1 : (job == 2 ? 2 : (job >= 6 ? 1 : 0));
+      constexpr int b = job == 0 ? 0 : (job == 1 || job == 3 ? 1 : 2);
+      constexpr bool dz = job == 2 || job == 4 || job == 6;
+      constexpr int r = dz ? a : (job == 5 || job == 7 ? 2 : a);
+      constexpr int t = dz ? 2 : (job == 5 ? 0 : (job == 7 ? 1 : b));
+      double gz[NQ], zo[N];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) gz[q] = uc[a][q] * uc[b][q] * (wxy * tab.w[q]);
+      if (dz) eo_line<N, NQ, -1>(eo.Dt, gz, zo);
+      else eo_line<N, NQ, 1>(eo.St, gz, zo);
+      const double st = sc[t];
+      double *zd = rb + (r * 3 + t) * N * NQ2 + qxy;
+#pragma unroll
+      for (int z = 0; z < N; ++z) zd[z * NQ2] = st * zo[z];
+      if (job == 3) {
+        double *z2 = rb + (1 * 3 + 0) * N * NQ2 + qxy;
+#pragma unroll
+        for (int z = 0; z < N; ++z) z2[z * NQ2] = sc[0] * zo[z];
+      }
+    };
+    if (T == 2 * NQ2) {
+      const int jh = tid / NQ2, qxy = tid - jh * NQ2;
+      const double wxy = beta * det * W[qxy % NQ] * W[qxy / NQ];
+      double uc[3][NQ];
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) cv_load<NQ>(uq + cc * QP + qxy, NQ2, uc[cc]);
+      if (jh == 0) {
+        gjob_c(Cv2Job<0>{}, uc, qxy, wxy);
+        gjob_c(Cv2Job<2>{}, uc, qxy, wxy);
+        gjob_c(Cv2Job<4>{}, uc, qxy, wxy);
+        gjob_c(Cv2Job<6>{}, uc, qxy, wxy);
+      } else {
+        gjob_c(Cv2Job<1>{}, uc, qxy, wxy);
+        gjob_c(Cv2Job<3>{}, uc, qxy, wxy);
+        gjob_c(Cv2Job<5>{}, uc, qxy, wxy);
+        gjob_c(Cv2Job<7>{}, uc, qxy, wxy);
+      }
+    } else if (T % NQ2 == 0 && (8 * NQ2) % T == 0) {
       // T / NQ2 jobs per pass: this thread's point and its job residue are
       // fixed, the job index is a compile-time offset (no select chains)
       constexpr int JP = T % NQ2 == 0 ? T / NQ2 : 1;
