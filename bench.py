@@ -336,6 +336,64 @@ def run_small_configs():
     return out
 
 
+def run_slab_emulation(n, k, t1_ms):
+    """Per-rank compute of the C5 x-slab vmult at P = 2, 4, 8 on ONE GPU: an
+    interior slab of the 128^3 mesh with its ghost face traces in device
+    buffers (what the NCCL exchange delivers), timed as the production
+    split vmult -- whole slab on zero ghost traces (the part that overlaps
+    the exchange) + the ghost-trace lifts.  Communication is not included
+    (payload and the NVLink time it needs at 900 GB/s are reported beside);
+    the compute-only efficiency is T1 / (P T_P)."""
+    import ctypes
+    import torch
+    from paper_1607_01323_b200 import mesh as M, _lib
+    from paper_1607_01323_b200.parallel import SlabPartition
+    from paper_1607_01323_b200.spaces import DeviceContext
+    from paper_1607_01323_b200.operators import ctypes_ptr
+    P = lambda t: ctypes_ptr(t.data_ptr())
+    out = {}
+    mesh = M.build_box_mesh(((0, 1),) * 3, (n, n, n))
+    kinds = (_lib.BC_VELOCITY_DIRICHLET,) * 6
+    st = ctypes_ptr(torch.cuda.current_stream().cuda_stream)
+    for nranks in (2, 4, 8):
+        part = SlabPartition(n, nranks, False)
+        x0, x1 = part.range(1)
+        c = DeviceContext(mesh, k, kinds, 0, (x0, x1))
+        cnt = ctypes.c_int64()
+        _lib.call("dg_halo_count", c.handle, ctypes.byref(cnt))
+        nloc = (x1 - x0) * n * n * (k + 1) ** 3
+        src = torch.rand(nloc, dtype=torch.float64, device="cuda")
+        dst = torch.empty_like(src)
+        rcv = [torch.rand(cnt.value, dtype=torch.float64, device="cuda") for _ in range(2)]
+        _lib.call("dg_halo_attach", c.handle, P(rcv[0]), P(rcv[1]))
+        ts = []
+        for ph in (1, 2):
+            f = lambda: _lib.call("dg_laplace_vmult_split", c.handle, P(src), P(dst), 1.0, ph, st)
+            f()
+            torch.cuda.synchronize()
+            best = 1e9
+            for _ in range(3):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(20):
+                    f()
+                b.record()
+                torch.cuda.synchronize()
+                best = min(best, a.elapsed_time(b) / 20)
+            ts.append(best)
+        tp = ts[0] + ts[1]
+        halo_bytes = 2 * cnt.value * 8  # both neighbours, one direction
+        out[f"P{nranks}"] = {"slab_cells": [x1 - x0, n, n], "whole_slab_ms": ts[0],
+                             "ghost_lift_ms": ts[1], "rank_vmult_ms": tp,
+                             "compute_efficiency": t1_ms / (nranks * tp),
+                             "halo_bytes_per_rank": halo_bytes,
+                             "nvlink_ms_at_900GBs": halo_bytes / 2 / 900e9 * 1e3}
+        del c, src, dst, rcv
+    out["note"] = ("one GPU, interior slab, ghost traces from device buffers; communication "
+                   "excluded (overlapped with the whole-slab phase in the product)")
+    return out
+
+
 def run_cg(dist_on):
     """BASELINE config 2: 32^3, Q4, periodic x,z, walls y, pure Neumann,
     rhs = zero_mean_project_dual(M (sin 2pi x cos pi y sin 2pi z + 1e-3 N(0,1),
@@ -565,6 +623,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_step:
         small = run_small_configs()
         dsweep = run_degree_sweep(hbm_peak()[0])
+    slab_emu = None
+    if rank == 0 and world == 1 and not args.no_step:
+        try:
+            slab_emu = run_slab_emulation(n, k, ms_step)
+        except Exception as exc:  # reported, never fatal for the headline line
+            slab_emu = {"error": repr(exc)[:200]}
     sweep = []
     if rank == 0 and world == 1 and args.sweep:
         sweep = run_sweep()
@@ -634,6 +698,8 @@ def main():
             line["configs"] = small
         if dsweep:
             line["degree_sweep_64cubed"] = dsweep
+        if slab_emu:
+            line["slab_emulation_1gpu"] = slab_emu
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

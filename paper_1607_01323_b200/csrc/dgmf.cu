@@ -1119,10 +1119,13 @@ int dg_halo_count(const dg_ctx *c, int64_t *count) {
 //   per face node (y, z): vn = (M z-mass) v_ghost, gn = (M) g_ghost,
 //   cv = -A vn + D gn, cd = -B vn  (A, B, D of side7 for a halo side),
 //   T[z][y][x] = delta(x, end) cv + dEnd[x] cd,  out += (M y-mass) T.
-// One group of N*N threads per (boundary cell, side).
+// One group of N*N threads per (boundary cell, side); both ghost sides in one
+// launch (blockIdx.y, side0 + blockIdx.y; one launch instead of two: the
+// x-slab rank of P = 8 spends 21 -> 1x us here).
 template <int N>
 __global__ void ghost_lift_kernel(const Geo g, const __grid_constant__ LapTab<N> T, double ts,
-                                  int side, double *__restrict__ out) {
+                                  int side0, double *__restrict__ out) {
+  const int side = side0 + (int)blockIdx.y;
   constexpr int N2 = N * N, G = 128 / N2, NP = N * N2;
   __shared__ double sv[G][N2], sg[G][N2], c1[G][N2], c2[G][N2];
   const int grp = threadIdx.x / N2, t = threadIdx.x - grp * N2;
@@ -1204,14 +1207,15 @@ int dg_laplace_vmult_split(dg_ctx *c, const double *src, double *dst, double tau
   }
   if (c->n_cells == 0) return DG_OK;
   const Geo g = c->geo();
-  for (int s = 0; s < 2; ++s) {
-    if (c->mode[s] != kGhost) continue;
+  const bool lo = c->mode[0] == kGhost, hi = c->mode[1] == kGhost;
+  if (lo || hi) {
+    const int side0 = lo ? 0 : 1, nsides = (lo ? 1 : 0) + (hi ? 1 : 0);
     const int64_t cells = (int64_t)g.ny * g.nz;
 #define DG_GL(NN)                                                                             \
   if (c->n == NN) {                                                                           \
     constexpr int G = 128 / (NN * NN);                                                        \
-    ghost_lift_kernel<NN><<<(unsigned)((cells + G - 1) / G), 128, 0, st>>>(g, lap_tab<NN>(c->basis), \
-                                                                         tau_scale, s, dst);   \
+    ghost_lift_kernel<NN><<<dim3((unsigned)((cells + G - 1) / G), (unsigned)nsides), 128, 0, st>>>( \
+        g, lap_tab<NN>(c->basis), tau_scale, side0, dst);                                     \
   }
     DG_GL(4) DG_GL(5) DG_GL(6)
 #undef DG_GL
