@@ -13,7 +13,7 @@ from paper_1607_01323_b200.operators import ctypes_ptr
 cfgs = (sys.argv[1] if len(sys.argv) > 1 else "0 6").split()
 n, k = 128, 4
 P = lambda t: ctypes_ptr(t.data_ptr())
-os.environ["DG_LAP_VARIANT"] = "8"
+os.environ["DG_LAP_VARIANT"] = os.environ.get("SLAB_VARIANT", "8")
 for nranks in (1, 2, 4, 8):
     mesh = M.build_box_mesh(((0, 1),) * 3, (n, n, n))
     part = SlabPartition(n, nranks, False)
