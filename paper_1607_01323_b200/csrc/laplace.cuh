@@ -734,10 +734,65 @@ laplace_vmult_kernel(const R *__restrict__ u, R *__restrict__ out, const Geo g,
     const double wxy = EPI == kEpiDot ? 0.125 * g.hx[x0 + jx] * g.hy[y0 + jy] * g.hz[z0 + jz] *
                                             ea.wint[tb] * ea.wint[ta]
                                       : 0.0;
+    if constexpr (EPI == kEpiCheb && !std::is_same<R, double>::value) {  // fp32 levels: same batching
+      R rc[N], dg[N], xv[N], uv[N];
 #pragma unroll
-    for (int i = 0; i < N; ++i)
-      epi_store<EPI, DIM, N>(u, out, ea, e * NP + (i * N + ta) * N + tb, y[i], wxy * ea.wint[i],
-                             eacc);
+      for (int i = 0; i < N; ++i) {
+        const size_t gi = e * NP + (i * N + ta) * N + tb;
+        rc[i] = ea.rc[gi];
+        dg[i] = ea.diag[gi];
+        xv[i] = ea.x[gi];
+        uv[i] = u[gi];
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const size_t gi = e * NP + (i * N + ta) * N + tb;
+        const R r = rc[i] - y[i];
+        const R dn = (R)ea.a * uv[i] + (R)ea.b * (r / dg[i]);
+        ea.rc[gi] = r;
+        ea.dnew[gi] = dn;
+        ea.x[gi] = xv[i] + dn;
+      }
+    } else if constexpr (EPI == kEpiDot) {  // u of the line's points loaded before the out stores
+      double pv[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) pv[i] = u[e * NP + (i * N + ta) * N + tb];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        out[e * NP + (i * N + ta) * N + tb] = y[i];
+        eacc[0] += pv[i] * y[i];
+        eacc[1] += y[i];
+        eacc[2] += pv[i] * (wxy * ea.wint[i]);
+      }
+    } else if constexpr (EPI == kEpiCheb && std::is_same<R, double>::value) {
+      // all operands of the line's N points loaded before any store (the
+      // epilogue pointers may alias as far as the compiler knows, so per-point
+      // load / store pairs serialised the L2 latency); same arithmetic as
+      // epi_store
+      double rc[N], dg[N], xv[N], uv[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const size_t gi = e * NP + (i * N + ta) * N + tb;
+        rc[i] = ea.rc[gi];
+        dg[i] = ea.diag[gi];
+        xv[i] = ea.x[gi];
+        uv[i] = u[gi];
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const size_t gi = e * NP + (i * N + ta) * N + tb;
+        const double r = __dsub_rn(rc[i], y[i]);
+        const double dn = __dadd_rn(__dmul_rn(ea.a, uv[i]), __dmul_rn(ea.b, __ddiv_rn(r, dg[i])));
+        ea.rc[gi] = r;
+        ea.dnew[gi] = dn;
+        ea.x[gi] = __dadd_rn(xv[i], dn);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        epi_store<EPI, DIM, N>(u, out, ea, e * NP + (i * N + ta) * N + tb, y[i], wxy * ea.wint[i],
+                               eacc);
+    }
   }
   if (EPI == kEpiDot) epi_reduce(eacc, reinterpret_cast<double *>(fbuf), ea, bx + gridDim.x * (by + gridDim.y * bz));
 }
