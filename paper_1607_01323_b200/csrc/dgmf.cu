@@ -492,7 +492,7 @@ static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau
                            cudaStream_t st, const EpiArgs &ea = EpiArgs{});
 
 // fused-epilogue vmults for the CG / Chebyshev loop (default bricks, k = 2..5)
-template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore, int HSM = 0, int HMAP = 0>
+template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore, int HSM = 0, int HMAP = 0, int FSD = 0>
 static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea = EpiArgs{});
 
@@ -648,16 +648,17 @@ static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau
 }
 
 // half-plane column kernel (laplace8.cuh)
-template <int N, int TX, int TY, int NRING, int MINB, int EPI, int HSM, int HMAP>
+template <int N, int TX, int TY, int NRING, int MINB, int EPI, int HSM, int HMAP, int FSD>
 static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea) {
   if (t_kname) {
-    *t_kname = (HSM || HMAP) ? kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI, HSM, HMAP})
+    *t_kname = FSD ? kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI, HSM, HMAP, FSD})
+               : (HSM || HMAP) ? kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI, HSM, HMAP})
                              : kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI});
     return DG_OK;
   }
   using C = Lap8Cfg<N, TX, TY, NRING, HSM>;
-  auto kern = laplace8_kernel<N, TX, TY, NRING, MINB, EPI, HSM, HMAP>;
+  auto kern = laplace8_kernel<N, TX, TY, NRING, MINB, EPI, HSM, HMAP, FSD>;
   static int nsm = 0, occ = 1;
   if (!nsm) {
     DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -776,7 +777,9 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
       if (cfg == 4) return launch_laplace8<5, 8, 4, 3, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
       if (cfg == 5) return launch_laplace8<5, 4, 8, 4, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
       if (cfg == 6) return launch_laplace8<5, 8, 4, 4, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
-      return launch_laplace8<5, 4, 8, 3, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
+      if (cfg == 7) return launch_laplace8<5, 4, 8, 3, 1, kEpiStore, 2, 1, 1>(c, src, dst, tau_scale, part, st);
+      if (cfg == 8) return launch_laplace8<5, 4, 8, 3, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
+      return launch_laplace8<5, 4, 8, 3, 1, kEpiStore, 2, 1, 1>(c, src, dst, tau_scale, part, st);
     }
     if (c->n == 6) return launch_laplace8<6, 4, 4, 2, 2>(c, src, dst, tau_scale, part, st);
   }
@@ -817,7 +820,8 @@ static int laplace_dispatch(dg_ctx *c, const double *src, double *dst, double ta
     // source table) and halo work placed per SM sub-partition (HMAP); per-layer
     // set-up hoisted: 120.8 -> 133.7 GDoF/s at 128^3; 4x8 tile, ring 3: 136.3
     // (+1.6-1.9 % at 64^3-160^3 and on the x-slabs of P = 1-8; profiles/r02/NOTES.md)
-    if (c->n == 5) return launch_laplace8<5, 4, 8, 3, 1, kEpiStore, 2, 1>(c, src, dst, tau_scale, part, st);
+    // x / y side coefficients per cell precomputed with the kinds folded in (FSD): +1 %
+    if (c->n == 5) return launch_laplace8<5, 4, 8, 3, 1, kEpiStore, 2, 1, 1>(c, src, dst, tau_scale, part, st);
     if (c->n == 6) return launch_laplace7<6, 4, 4, 2, 2, false, kEpiStore, 1>(c, src, dst, tau_scale, part, st);
   }
   if (c->dim == 3 && variant == 6 && c->n == 4)  // register-plane kernel at k = 3 (experiment)

@@ -39,9 +39,12 @@ struct Lap8Cfg : Lap7Cfg<N, TX, TY, NRING> {
   static constexpr int HCELLS = 2 * (TX + TY);
   static constexpr int HCS = N * N * N + ((N & 1) ? 2 : 1);
   static constexpr int OFF_HTAB = OFF_HST + HCELLS * HCS;
-  static constexpr size_t SMEM =
-      sizeof(double) * (size_t)(HSM == 2 ? OFF_HTAB + 3 * HCELLS
-                                         : (HSM ? OFF_HST + B::HITEMS * HSTR : B::NDBL));
+  // per-cell x / y side coefficients for FSD (A = PA hz (tA + tz), B = PB hz,
+  // D = PD hz per side, kind folded in; plus the stiffness scales / hz)
+  static constexpr int CC2 = 21;
+  static constexpr int OFF_CC2 = HSM == 2 ? OFF_HTAB + 3 * HCELLS
+                                          : (HSM ? OFF_HST + B::HITEMS * HSTR : B::NDBL);
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(OFF_CC2 + NCT * CC2);
   // lane halves run the same lines in lockstep (shuffles inside the line loops)
   static_assert(NCT == 32 || N % 2 == 0, "NCT = 16 halves need even N");
 };
@@ -74,7 +77,8 @@ __device__ __forceinline__ int l8_role(int w) {
 // EPI: kEpiStore (out by TMA bulk stores) or a CG / Chebyshev epilogue
 // (laplace.cuh epi_store) applied cooperatively to each finished layer of
 // the tile; kEpiDot leaves one partial-sum triple per CTA in ea.partials.
-template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore, int HSM = 0, int HMAP = 0>
+template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore, int HSM = 0, int HMAP = 0,
+          int FSD = 0>
 __global__ void __launch_bounds__(Lap8Cfg<N, TX, TY, NRING>::THREADS, MINB)
 laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g,
                 const __grid_constant__ LapTab<N> T, const double ts, const int part,
@@ -178,6 +182,28 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     q[12] = tx + fmax(ty, ay[4 + 2]);
     q[13] = ay[-4 + 1];
     q[14] = ay[4 + 1];
+    if (FSD) {  // side coefficients of this cell with its kinds folded in
+      double *f = smem + C::OFF_CC2 + c * C::CC2;
+      f[0] = 0.5 * hy * hxi;  // kx / hz
+      f[1] = 0.5 * hx * hyi;  // ky / hz
+      auto put = [&](double *o, int kind, double tmx, double sf, double hid, double hin, double sg) {
+        o[0] = o[1] = o[2] = o[3] = 0.0;
+        if (kind <= 1) {
+          o[0] = ts * sf;
+          o[1] = tmx;
+          o[2] = sg * sf * hid;
+          o[3] = sg * sf * hin;
+        } else if (kind == kBndNeumann) {
+          o[0] = ts * 2.0 * sf;
+          o[1] = tx + ty;
+          o[2] = 2.0 * sg * sf * hid;
+        }
+      };
+      put(f + 2, kx0, q[5], 0.25 * hy, hxi, q[7], 1.0);
+      put(f + 6, kx1, q[6], 0.25 * hy, hxi, q[8], -1.0);
+      put(f + 10, ky0, q[11], 0.25 * hx, hyi, q[13], 1.0);
+      put(f + 14, ky1, q[12], 0.25 * hx, hyi, q[14], -1.0);
+    }
   }
   for (int i = tid; i < 2 * N * N; i += C::THREADS) smem[C::OFF_ZERO + i] = 0.0;
   double *const zd = smem + C::OFF_ZD;
@@ -573,9 +599,13 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     double *const wp = slot + c * CSTR + s * N2;  // W rows -> T rows -> out
     double *const rp = rbuf + c * CSTR + s * N2;  // R rows -> V rows
     {
-      const double sfx = 0.25 * hy * hz, kx = 0.5 * hy * hz * hxi;
-      const Side7 s0 = side7(kx0, q[5] + tz, taue, sfx, hxi, q[7], 1.0, ts);
-      const Side7 s1 = side7(kx1, q[6] + tz, taue, sfx, hxi, q[8], -1.0, ts);
+      const double *f = smem + C::OFF_CC2 + c * C::CC2;
+      const double sfx = 0.25 * hy * hz;
+      const double kx = FSD ? f[0] * hz : 0.5 * hy * hz * hxi;
+      const Side7 s0 = FSD ? Side7{f[2] * hz * (f[3] + tz), f[4] * hz, f[5] * hz}
+                           : side7(kx0, q[5] + tz, taue, sfx, hxi, q[7], 1.0, ts);
+      const Side7 s1 = FSD ? Side7{f[6] * hz * (f[7] + tz), f[8] * hz, f[9] * hz}
+                           : side7(kx1, q[6] + tz, taue, sfx, hxi, q[8], -1.0, ts);
       const double *h0 = kx0 == 1 ? hxb + par * C::HXN + (jy * N) * N * 2 + 2 * s : zero;
       const double *h1 = kx1 == 1 ? hxb + par * C::HXN + ((TY + jy) * N) * N * 2 + 2 * s : zero;
 #pragma unroll
@@ -615,9 +645,13 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     pair_sync();
     // ================= y phase: columns x in this half of plane z = s =================
     {
-      const double sfy = 0.25 * hx * hz, ky = 0.5 * hx * hz * hyi;
-      const Side7 s0 = side7(ky0, q[11] + tz, taue, sfy, hyi, q[13], 1.0, ts);
-      const Side7 s1 = side7(ky1, q[12] + tz, taue, sfy, hyi, q[14], -1.0, ts);
+      const double *f = smem + C::OFF_CC2 + c * C::CC2;
+      const double sfy = 0.25 * hx * hz;
+      const double ky = FSD ? f[1] * hz : 0.5 * hx * hz * hyi;
+      const Side7 s0 = FSD ? Side7{f[10] * hz * (f[11] + tz), f[12] * hz, f[13] * hz}
+                           : side7(ky0, q[11] + tz, taue, sfy, hyi, q[13], 1.0, ts);
+      const Side7 s1 = FSD ? Side7{f[14] * hz * (f[15] + tz), f[16] * hz, f[17] * hz}
+                           : side7(ky1, q[12] + tz, taue, sfy, hyi, q[14], -1.0, ts);
       const double *h0 = ky0 == 1 ? hyb + par * C::HYN + (jx * N) * N * 2 + 2 * s : zero;
       const double *h1 = ky1 == 1 ? hyb + par * C::HYN + ((TX + jx) * N) * N * 2 + 2 * s : zero;
 #pragma unroll
