@@ -44,7 +44,10 @@ struct Lap8Cfg : Lap7Cfg<N, TX, TY, NRING> {
   static constexpr int CC2 = 21;
   static constexpr int OFF_CC2 = HSM == 2 ? OFF_HTAB + 3 * HCELLS
                                           : (HSM ? OFF_HST + B::HITEMS * HSTR : B::NDBL);
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(OFF_CC2 + NCT * CC2);
+  // FSD: per-layer z-side data [layer][a0, t0, b0, d0, a1, t1, b1, d1]:
+  // A = (ts sf_z) a (txy + t), B = sf_z b, D = sf_z d (kinds folded in)
+  static constexpr int OFF_ZS = OFF_CC2 + NCT * CC2;
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(OFF_ZS + 8 * B::LCMAX);
   // lane halves run the same lines in lockstep (shuffles inside the line loops)
   static_assert(NCT == 32 || N % 2 == 0, "NCT = 16 halves need even N");
 };
@@ -208,6 +211,33 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
   for (int i = tid; i < 2 * N * N; i += C::THREADS) smem[C::OFF_ZERO + i] = 0.0;
   double *const zd = smem + C::OFF_ZD;
   for (int i = tid; i < 4 * (nlay + 2); i += C::THREADS) zd[i] = g.ax[2][4 * (z0 - 1) + i];
+  double *const zs = smem + C::OFF_ZS;
+  if (FSD)
+    for (int L = tid; L < nlay; L += C::THREADS) {  // z sides of layer z0 + L
+      const int iz = z0 + L;
+      const double *a = g.ax[2] + 4 * iz;
+      const double tz = a[2], hzi = a[1];
+#pragma unroll
+      for (int sd = 0; sd < 2; ++sd) {
+        const double *an = a + (sd ? 4 : -4);
+        const bool edge = sd ? iz == g.nz - 1 : iz == 0;
+        const int m = g.mode[4 + sd];
+        const int kind = edge ? (m == kWrap ? 0 : m) : 0;
+        const double sg = sd ? -1.0 : 1.0;
+        double *o = zs + 8 * L + 4 * sd;
+        o[0] = o[1] = o[2] = o[3] = 0.0;
+        if (kind <= 1) {
+          o[0] = 1.0;
+          o[1] = tz > an[2] ? tz : an[2];
+          o[2] = sg * hzi;
+          o[3] = sg * an[1];
+        } else if (kind == kBndNeumann) {
+          o[0] = 2.0;
+          o[1] = tz;
+          o[2] = 2.0 * sg * hzi;
+        }
+      }
+    }
 
   // ---- ring ----------------------------------------------------------------
   auto layer_of = [&](int r) -> int {
@@ -554,8 +584,12 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       // tau of the z faces: max of the two cells' z parts (plain compare: no NaN
       // fix-up sequence as in fmax)
       const double tzl = az[-4 + 2], tzu = az[4 + 2];
-      const Side7 s0 = side7(kz0, txy + (tz > tzl ? tz : tzl), taue, sfz, hzi, az[-4 + 1], 1.0, ts);
-      const Side7 s1 = side7(kz1, txy + (tz > tzu ? tz : tzu), taue, sfz, hzi, az[4 + 1], -1.0, ts);
+      const double *zq = zs + 8 * p;
+      const double tsf = ts * sfz;
+      const Side7 s0 = FSD ? Side7{tsf * zq[0] * (txy + zq[1]), sfz * zq[2], sfz * zq[3]}
+                           : side7(kz0, txy + (tz > tzl ? tz : tzl), taue, sfz, hzi, az[-4 + 1], 1.0, ts);
+      const Side7 s1 = FSD ? Side7{tsf * zq[4] * (txy + zq[5]), sfz * zq[6], sfz * zq[7]}
+                           : side7(kz1, txy + (tz > tzu ? tz : tzu), taue, sfz, hzi, az[4 + 1], -1.0, ts);
       double *up = slot + c * CSTR + s * N + l0;
       double *rp = rbuf + c * CSTR + s * N + l0;
       const double *lp = ring + ((r + 1) % NRING) * C::LAYER + c * CSTR + s * N + l0;
