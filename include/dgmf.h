@@ -386,6 +386,15 @@ int dg_laplace_vmult_split(dg_ctx *ctx, const double *src, double *dst, double t
  * out3 = partial [p.Lp, sum(Lp), p.w] (w = dual weights; deterministic). */
 int dg_cg_dots(dg_ctx *ctx, const double *p, const double *Lp, double *out3,
                void *stream);
+/* The CG step's operator application with its dot products in one pass
+ * (solvers.py:56-60: Ap = op(p), pAp = p.Ap): Lp = L p and out3 as
+ * dg_cg_dots.  3D Q4 meshes of >= 16k cells: one launch of the column
+ * kernel, the sums formed in its y phase from a shared-memory copy of the
+ * layer's p (p and Lp cross HBM once); otherwise dg_laplace_vmult followed
+ * by dg_cg_dots.  Contexts without remote sides only (x-slab ranks use
+ * dg_laplace_vmult_split + dg_cg_dots): DG_EINVAL otherwise. */
+int dg_laplace_vmult_dots(dg_ctx *ctx, const double *p, double *Lp, double tau_scale,
+                          double *out3, void *stream);
 /* alpha = scal[0] / pAp, pAp = p.Lp - (sum(Lp)/|Omega|) p.w (project_dual:
  * op = zero_mean_project_dual o L, solvers.py:187-198) or p.Lp; no update
  * when pAp <= 0 (breakdown, the caller stops).  x += alpha p ;

@@ -659,13 +659,15 @@ static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau
   }
   using C = Lap8Cfg<N, TX, TY, NRING, HSM>;
   auto kern = laplace8_kernel<N, TX, TY, NRING, MINB, EPI, HSM, HMAP, FSD>;
+  constexpr size_t kSmem = EPI == kEpiDotS ? C::SMEM_DOTS : C::SMEM;
+  static_assert(kSmem <= 232448, "laplace8: more than 227 KB of shared memory");
   static int nsm = 0, occ = 1;
   if (!nsm) {
-    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    DG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     int dev = 0;
     DG_CUDA_CHECK(cudaGetDevice(&dev));
     DG_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    DG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM));
+    DG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, kSmem));
     if (occ < 1) occ = 1;
   }
   const Geo g = c->geo();
@@ -678,11 +680,11 @@ static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau
   const int cols = ntx * nty, nz = zhi - zlo;
   const int lc = chunk_len(nz, cols, nsm * occ, occ, l7_lcmin(8), C::LCMAX);
   const int nch = (nz + lc - 1) / lc;
-  if (EPI == kEpiDot) {
+  if (EPI == kEpiDot || EPI == kEpiDotS) {
     if (4 * (int64_t)cols * nch > c->partials_n) return inval("laplace8 epilogue: partials buffer");
     c->epi_nparts = (int64_t)cols * nch;
   }
-  kern<<<(unsigned)(cols * nch), C::THREADS, C::SMEM, st>>>(src, dst, g, lap_tab<N>(c->basis),
+  kern<<<(unsigned)(cols * nch), C::THREADS, kSmem, st>>>(src, dst, g, lap_tab<N>(c->basis),
                                                             tau_scale, part, zlo, zhi, lc, ntx, nty,
                                                             ea);
   DG_LAUNCH_CHECK("laplace8_kernel");

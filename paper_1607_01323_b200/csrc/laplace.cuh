@@ -228,7 +228,11 @@ __device__ __forceinline__ void eo_merge(const R *E, const R *O, R *y) {
 //   kEpiDot    out = L u and per-CTA partial sums of u.Lu, sum(Lu), u.w
 //              (w = integrals of the basis functions, the dual zero-mean
 //              weights) for pAp of the projected operator
-enum LapEpi : int { kEpiStore = 0, kEpiCheb = 1, kEpiDot = 2 };
+//   kEpiDotS   (laplace8 only) as kEpiDot, but out leaves by the TMA bulk
+//              stores of kEpiStore and the sums are formed in the y phase
+//              from a shared-memory copy of the layer's u (no global
+//              re-read of u, no extra barrier)
+enum LapEpi : int { kEpiStore = 0, kEpiCheb = 1, kEpiDot = 2, kEpiDotS = 3 };
 template <class R>
 struct EpiArgsT {
   R *rc;

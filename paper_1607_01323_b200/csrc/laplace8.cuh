@@ -48,6 +48,11 @@ struct Lap8Cfg : Lap7Cfg<N, TX, TY, NRING> {
   // A = (ts sf_z) a (txy + t), B = sf_z b, D = sf_z d (kinds folded in)
   static constexpr int OFF_ZS = OFF_CC2 + NCT * CC2;
   static constexpr size_t SMEM = sizeof(double) * (size_t)(OFF_ZS + 8 * B::LCMAX);
+  // kEpiDotS: copy of the layer's u ([cell][CSTR] as a ring slot) and the
+  // products wint[z] wint[x] of the dual weights
+  static constexpr int OFF_UB = ((OFF_ZS + 8 * B::LCMAX + 1) / 2) * 2;
+  static constexpr int OFF_WT = OFF_UB + B::LAYER;
+  static constexpr size_t SMEM_DOTS = sizeof(double) * (size_t)(OFF_WT + N * N);
   // lane halves run the same lines in lockstep (shuffles inside the line loops)
   static_assert(NCT == 32 || N % 2 == 0, "NCT = 16 halves need even N");
 };
@@ -119,7 +124,7 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     if ((part == 1 && touches) || (part == 2 && !touches)) skip = true;
   }
   if (skip) {
-    if (EPI == kEpiDot && threadIdx.x < 3) ea.partials[(size_t)blockIdx.x * 4 + threadIdx.x] = 0.0;
+    if ((EPI == kEpiDot || EPI == kEpiDotS) && threadIdx.x < 3) ea.partials[(size_t)blockIdx.x * 4 + threadIdx.x] = 0.0;
     return;
   }
   double eacc[3] = {0.0, 0.0, 0.0};  // kEpiDot partial sums of this CTA
@@ -209,6 +214,14 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     }
   }
   for (int i = tid; i < 2 * N * N; i += C::THREADS) smem[C::OFF_ZERO + i] = 0.0;
+  double *const ubuf = smem + C::OFF_UB;
+  if (EPI == kEpiDotS && tid == 0) {
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+      for (int b = 0; b < N; ++b) smem[C::OFF_WT + a * N + b] = ea.wint[a] * ea.wint[b];
+  }
+  const bool act = jx < ex && jy < ey;  // kEpiDotS: lanes of cells outside the mesh add nothing
   double *const zd = smem + C::OFF_ZD;
   for (int i = tid; i < 4 * (nlay + 2); i += C::THREADS) zd[i] = g.ax[2][4 * (z0 - 1) + i];
   double *const zs = smem + C::OFF_ZS;
@@ -600,6 +613,11 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
           double w[N], e[NE], o[HO], E[NE], O[HO], g0, g1;
 #pragma unroll
           for (int z = 0; z < N; ++z) w[z] = up[z * N2 + k];
+          if (EPI == kEpiDotS) {  // u of this layer stays readable for the y phase
+            double *ub = ubuf + c * CSTR + s * N + l0;
+#pragma unroll
+            for (int z = 0; z < N; ++z) ub[z * N2 + k] = w[z];
+          }
           double la0 = lp[k], lg = T.dL[0] * la0;
 #pragma unroll
           for (int z = 1; z < N; ++z) lg += T.dL[z] * lp[z * N2 + k];
@@ -713,10 +731,26 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
           eo_merge<N>(E, O, yv);
 #pragma unroll
           for (int yy = 0; yy < N; ++yy) wp[yy * N + x] = yv[yy];
+          if (EPI == kEpiDotS) {  // u.Lu, sum(Lu), u.w of this line
+            const double *ub = ubuf + c * CSTR + s * N2 + x;
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll
+            for (int yy = 0; yy < N; ++yy) {
+              const double pu = ub[yy * N];
+              t0 += pu * yv[yy];
+              t1 += yv[yy];
+              t2 += pu * ea.wint[yy];
+            }
+            if (act) {
+              eacc[0] += t0;
+              eacc[1] += t1;
+              eacc[2] += t2 * (smem[C::OFF_WT + s * N + x] * (0.5 * q[0] * hz));
+            }
+          }
         }
       }
     }
-    if (tma && EPI == kEpiStore) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (tma && (EPI == kEpiStore || EPI == kEpiDotS)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();  // B_b: out complete in the slot
     if (EPI == kEpiCheb && (N & 1)) {
       // Chebyshev epilogue, odd N (a tile row of cells is one contiguous run
@@ -755,7 +789,7 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
         }
       }
       __syncthreads();  // the slot is refilled by a later z phase
-    } else if (EPI != kEpiStore) {
+    } else if (EPI != kEpiStore && EPI != kEpiDotS) {
       // epilogue on this layer's cells: out / Chebyshev vectors / partial sums
       const double hzl = hz;
       for (int i = tid; i < ex * ey * NP; i += C::THREADS) {
@@ -791,8 +825,8 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       __syncthreads();
     }
   }
-  if (EPI == kEpiDot) epi_reduce(eacc, rbuf, ea, blockIdx.x);
-  if (tid < 32 && tma && EPI == kEpiStore) bulk_wait_read();
+  if (EPI == kEpiDot || EPI == kEpiDotS) epi_reduce(eacc, rbuf, ea, blockIdx.x);
+  if (tid < 32 && tma && (EPI == kEpiStore || EPI == kEpiDotS)) bulk_wait_read();
 }
 
 }  // namespace dg

@@ -212,6 +212,21 @@ class SlabLaplace:
                   2 if overlap else 0, ms)
         return dst
 
+    def vmult_dots(self, p, Lp, tau_scale, out3):
+        """Lp = L p with the rank-local [p.Lp, sum(Lp), p.w] in out3 (device):
+        one fused launch on a single rank (dg_laplace_vmult_dots); x-slab
+        ranks run the overlapped vmult, then dg_cg_dots."""
+        import torch
+        P = lambda t: ctypes.c_void_p(t.data_ptr())
+        ms = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        if self.nranks == 1:
+            _lib.call("dg_laplace_vmult_dots", self.ctx.handle, P(p), P(Lp), float(tau_scale),
+                      P(out3), ms)
+        else:
+            self.vmult(p, Lp, tau_scale)
+            _lib.call("dg_cg_dots", self.ctx.handle, P(p), P(Lp), P(out3), ms)
+        return Lp
+
     def diagonal(self, tau_scale=1.0):
         """Exact Jacobi diagonal of this slab (operators.py:675-730)."""
         import torch
@@ -312,8 +327,11 @@ class SlabPCG:
         sc, ops = self.scal, self.ops
         self.it += 1
         it = self.it
-        self.lap.vmult(self.p, self.Lp, self.ts)
-        ops.dots(self.p, self.Lp, sc[1:])
+        if hasattr(self.lap, "vmult_dots"):  # device slabs: fused on a single rank
+            self.lap.vmult_dots(self.p, self.Lp, self.ts, sc[1:])
+        else:
+            self.lap.vmult(self.p, self.Lp, self.ts)
+            ops.dots(self.p, self.Lp, sc[1:])
         self.comm.allreduce(sc[1:4])
         ops.update(self.x, self.r, self.p, self.Lp, sc, self.project,
                    self.diag if self.cheb is None else None, self.z, sc[4:])

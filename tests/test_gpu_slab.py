@@ -103,3 +103,36 @@ def test_sharded_pcg_matches_single_context(world, k, prec, neumann):
                                    atol=1e-13 * s1.history[0])
     ref = x1.reshape(-1).cpu().numpy()
     assert np.linalg.norm(x2 - ref) <= (1e-10 if prec == "cheb" else 1e-8) * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("counts,k,neumann", [
+    ((32, 32, 16), 4, True),    # fused column epilogue, TMA rows, periodic x / z
+    ((30, 33, 17), 4, False),   # fused, ragged tiles, odd nx (no TMA)
+    ((34, 32, 16), 4, False),   # fused, TMA with a partial tile column
+    ((6, 5, 4), 3, False),      # below the fused range: vmult + dg_cg_dots
+])
+def test_vmult_dots_equals_vmult_then_dots(counts, k, neumann):
+    """dg_laplace_vmult_dots (the CG step's Ap and [p.Ap, sum(Ap), p.w] in one
+    launch, reference solvers.py:56-60) against dg_laplace_vmult followed by
+    dg_cg_dots: Lp bitwise, the sums to 1e-13 relative."""
+    import ctypes
+    from paper_1607_01323_b200 import _lib
+    mesh, space, bcs, _ = setup(counts, k, neumann)
+    lap = SlabLaplace(mesh, k, bcs.kinds, 0, 1)
+    rng = np.random.default_rng(5)
+    p = torch.as_tensor(rng.uniform(-1, 1, space.n_dofs), device="cuda")
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    ref = torch.empty_like(p)
+    _lib.call("dg_laplace_vmult", lap.ctx.handle, P(p), P(ref), 1.0, st)
+    s_ref = torch.zeros(3, dtype=torch.float64, device="cuda")
+    _lib.call("dg_cg_dots", lap.ctx.handle, P(p), P(ref), P(s_ref), st)
+    out = torch.full_like(p, float("nan"))
+    s = torch.zeros(3, dtype=torch.float64, device="cuda")
+    lap.vmult_dots(p, out, 1.0, s)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    a, b = s.cpu().numpy(), s_ref.cpu().numpy()
+    scale = np.array([float(p.abs().dot(ref.abs())), float(ref.abs().sum()), float(p.abs().sum())])
+    # sum(Lp) cancels to ~0: compare against the magnitude sums
+    assert np.all(np.abs(a - b) <= 1e-13 * np.maximum(scale, 1e-300)), (a, b)
