@@ -522,6 +522,10 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
       if (epi == kEpiDot) return launch_laplace8<5, 4, 8, 3, 1, kEpiDot, 2, 1>(c, src, dst, tau_scale, 0, st, ea);
     }
     if (epi == kEpiCheb) return launch_laplace8<5, 8, 4, 4, 1, kEpiCheb, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
+    // the dot epilogue from the shared-memory copy of u (kEpiDotS: out by TMA
+    // stores, no global re-read of u); DG_EPI_CFG=3: the cooperative one
+    if (epi == kEpiDot && ecfg != 3)
+      return launch_laplace8<5, 4, 8, 3, 1, kEpiDotS, 2, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
     if (epi == kEpiDot) return launch_laplace8<5, 8, 4, 4, 1, kEpiDot, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
   }
 #define DG_E(D, NN, X, Y, Z)                                                                     \
