@@ -395,6 +395,13 @@ int dg_cg_dots(dg_ctx *ctx, const double *p, const double *Lp, double *out3,
  * dg_laplace_vmult_split + dg_cg_dots): DG_EINVAL otherwise. */
 int dg_laplace_vmult_dots(dg_ctx *ctx, const double *p, double *Lp, double tau_scale,
                           double *out3, void *stream);
+/* The same on an x-slab rank, in the two phases of dg_laplace_vmult_split
+ * (traced-ghost 3D contexts): phase 1 = the whole slab on zero ghost traces
+ * with its sums -> out3 (no dependence on the exchange); phase 2 = the
+ * ghost-trace lifts, their share of p.Lp and sum(Lp) added to out3.  out3 is
+ * this rank's partial triple after phase 2 (all-reduce it). */
+int dg_laplace_vmult_split_dots(dg_ctx *ctx, const double *p, double *Lp, double tau_scale,
+                                int phase, double *out3, void *stream);
 /* alpha = scal[0] / pAp, pAp = p.Lp - (sum(Lp)/|Omega|) p.w (project_dual:
  * op = zero_mean_project_dual o L, solvers.py:187-198) or p.Lp; no update
  * when pAp <= 0 (breakdown, the caller stops).  x += alpha p ;

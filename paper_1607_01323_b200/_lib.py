@@ -128,6 +128,7 @@ PROTOTYPES = {
     "dg_laplace_vmult_split": [_P, _P, _P, _D, _I, _P],
     "dg_cg_dots": [_P, _P, _P, _P, _P],
     "dg_laplace_vmult_dots": [_P, _P, _P, _D, _P, _P],
+    "dg_laplace_vmult_split_dots": [_P, _P, _P, _D, _I, _P, _P],
     "dg_laplace_kernel_name": [_P, ctypes.c_char_p, _I],
     "dg_cg_update": [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P],
     "dg_cg_pupdate": [_P, _P, _P, _P, _P],

@@ -1132,9 +1132,13 @@ int dg_halo_count(const dg_ctx *c, int64_t *count) {
 // One group of N*N threads per (boundary cell, side); both ghost sides in one
 // launch (blockIdx.y, side0 + blockIdx.y; one launch instead of two: the
 // x-slab rank of P = 8 spends 21 -> 1x us here).
-template <int N>
+// DOTS: also the partial sums of p . (added terms) and sum(added terms) per
+// block -> partials[2 * block + {0, 1}] (dg_laplace_vmult_split_dots).
+template <int N, bool DOTS = false>
 __global__ void ghost_lift_kernel(const Geo g, const __grid_constant__ LapTab<N> T, double ts,
-                                  int side0, double *__restrict__ out) {
+                                  int side0, double *__restrict__ out,
+                                  const double *__restrict__ p = nullptr,
+                                  double *__restrict__ partials = nullptr) {
   const int side = side0 + (int)blockIdx.y;
   constexpr int N2 = N * N, G = 128 / N2, NP = N * N2;
   __shared__ double sv[G][N2], sg[G][N2], c1[G][N2], c2[G][N2];
@@ -1169,11 +1173,13 @@ __global__ void ghost_lift_kernel(const Geo g, const __grid_constant__ LapTab<N>
     c2[grp][t] = -B * vn;
   }
   __syncthreads();
+  double a0 = 0.0, a1 = 0.0;
   if (ok) {  // thread (z, x): y-mass, add into the x-line ends / derivative rows
     const int z = t / N, x = t - z * N;
     const int end = side ? N - 1 : 0;
     const double dx = side ? T.dR[x] : T.dL[x];
-    double *o = out + ((int64_t)ix + (int64_t)g.nx * (iy + (int64_t)g.ny * iz)) * NP + z * N2 + x;
+    const int64_t o0 = ((int64_t)ix + (int64_t)g.nx * (iy + (int64_t)g.ny * iz)) * NP + z * N2 + x;
+    double *o = out + o0;
 #pragma unroll
     for (int y = 0; y < N; ++y) {
       double m1 = 0.0, m2 = 0.0;
@@ -1182,8 +1188,44 @@ __global__ void ghost_lift_kernel(const Geo g, const __grid_constant__ LapTab<N>
         m1 += T.M[y * N + q] * c1[grp][z * N + q];
         m2 += T.M[y * N + q] * c2[grp][z * N + q];
       }
-      o[y * N] += (x == end ? m1 : 0.0) + dx * m2;
+      const double add = (x == end ? m1 : 0.0) + dx * m2;
+      o[y * N] += add;
+      if (DOTS) {
+        a0 += p[o0 + y * N] * add;
+        a1 += add;
+      }
     }
+  }
+  if (DOTS) {  // fixed-order block sums (128 threads)
+    __shared__ double red[2][4];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red[0][threadIdx.x >> 5] = a0;
+      red[1][threadIdx.x >> 5] = a1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      const double *r = red[threadIdx.x];
+      const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+      partials[2 * blk + threadIdx.x] = ((r[0] + r[1]) + r[2]) + r[3];
+    }
+  }
+}
+
+// out3[k] += sum_b partials[2 b + k], k < 2, fixed order (one block)
+__global__ void add_partials2_kernel(const double *__restrict__ partials, int64_t nb,
+                                     double *__restrict__ out3) {
+  __shared__ double sh[32];
+  for (int k = 0; k < 2; ++k) {
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) acc += partials[2 * i + k];
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) out3[k] += acc;
+    __syncthreads();
   }
 }
 
@@ -1193,8 +1235,26 @@ extern "C" {
 // slab with ZERO ghost traces (one launch, no dependence on the exchange),
 // phase 2 = out += the ghost-trace terms on the boundary x-layers
 // (ghost_lift_kernel).  Traced-ghost contexts (3D, Q3-Q5).
+static int vmult_split_impl(dg_ctx *c, const double *src, double *dst, double tau_scale, int phase,
+                            void *stream, double *out3);
+
 int dg_laplace_vmult_split(dg_ctx *c, const double *src, double *dst, double tau_scale,
                            int phase, void *stream) {
+  return vmult_split_impl(c, src, dst, tau_scale, phase, stream, nullptr);
+}
+
+}  // extern "C"
+
+// out3 != nullptr (dg_laplace_vmult_split_dots, slabcg.inc): the fused form,
+// phase 1 = column kernel with the kEpiDotS sums on zero traces -> out3,
+// phase 2 = ghost lifts with their share of p.Lp and sum(Lp) added to out3
+static bool split_dots_fused(const dg_ctx *c);
+static int split_phase1_dots(dg_ctx *c, const double *src, double *dst, double tau_scale,
+                             cudaStream_t st, double *out3);
+static int split_partials(dg_ctx *c, int64_t need);
+
+static int vmult_split_impl(dg_ctx *c, const double *src, double *dst, double tau_scale, int phase,
+                            void *stream, double *out3) {
   if (!c || !dst) return inval("null argument");
   if (phase != 1 && phase != 2) return inval("phase must be 1 or 2");
   if (!c->halo_traces || c->dim != 3) return inval("dg_laplace_vmult_split: traced-ghost 3D contexts");
@@ -1210,7 +1270,8 @@ int dg_laplace_vmult_split(dg_ctx *c, const double *src, double *dst, double tau
     const double *keep[2] = {c->d_recv[0], c->d_recv[1]};
     for (int s = 0; s < 2; ++s)
       if (c->mode[s] == kGhost) c->d_recv[s] = c->d_zero_ghost;
-    const int rc = laplace_dispatch(c, src, dst, tau_scale, 0, st);
+    const int rc = out3 ? split_phase1_dots(c, src, dst, tau_scale, st, out3)
+                        : laplace_dispatch(c, src, dst, tau_scale, 0, st);
     c->d_recv[0] = keep[0];
     c->d_recv[1] = keep[1];
     return rc;
@@ -1221,6 +1282,18 @@ int dg_laplace_vmult_split(dg_ctx *c, const double *src, double *dst, double tau
   if (lo || hi) {
     const int side0 = lo ? 0 : 1, nsides = (lo ? 1 : 0) + (hi ? 1 : 0);
     const int64_t cells = (int64_t)g.ny * g.nz;
+    if (out3) {  // n == 5 (split_dots_fused): the lifts with their dot shares
+      if (!src) return inval("null argument");
+      constexpr int G = 128 / 25;
+      const int64_t nb = (cells + G - 1) / G * nsides;
+      const int rc = split_partials(c, 2 * nb);
+      if (rc) return rc;
+      ghost_lift_kernel<5, true><<<dim3((unsigned)((cells + G - 1) / G), (unsigned)nsides), 128, 0, st>>>(
+          g, lap_tab<5>(c->basis), tau_scale, side0, dst, src, c->d_partials);
+      add_partials2_kernel<<<1, 1024, 0, st>>>(c->d_partials, nb, out3);
+      DG_LAUNCH_CHECK("ghost_lift_kernel (dots)");
+      return DG_OK;
+    }
 #define DG_GL(NN)                                                                             \
   if (c->n == NN) {                                                                           \
     constexpr int G = 128 / (NN * NN);                                                        \
@@ -1233,6 +1306,8 @@ int dg_laplace_vmult_split(dg_ctx *c, const double *src, double *dst, double tau
   DG_LAUNCH_CHECK("ghost_lift_kernel");
   return DG_OK;
 }
+
+extern "C" {
 
 int dg_halo_attach(dg_ctx *c, const double *recv_lo, const double *recv_hi) {
   if (!c) return inval("null context");

@@ -219,12 +219,28 @@ class SlabLaplace:
         import torch
         P = lambda t: ctypes.c_void_p(t.data_ptr())
         ms = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        h = self.ctx.handle
         if self.nranks == 1:
-            _lib.call("dg_laplace_vmult_dots", self.ctx.handle, P(p), P(Lp), float(tau_scale),
+            _lib.call("dg_laplace_vmult_dots", h, P(p), P(Lp), float(tau_scale), P(out3), ms)
+        elif self.traced:
+            # as vmult(): traces move on the side stream during phase 1
+            main = torch.cuda.current_stream()
+            self.comm.wait_stream(main)
+            with torch.cuda.stream(self.comm):
+                _lib.call("dg_halo_pack", h, P(p),
+                          ctypes.c_void_p(self.send[0].data_ptr() if self.has[0] else 0),
+                          ctypes.c_void_p(self.send[1].data_ptr() if self.has[1] else 0),
+                          ctypes.c_void_p(self.comm.cuda_stream))
+                self.comm_ops.exchange(self.send[0], self.send[1], self.recv[0], self.recv[1],
+                                       self.lo, self.hi)
+            _lib.call("dg_laplace_vmult_split_dots", h, P(p), P(Lp), float(tau_scale), 1,
+                      P(out3), ms)
+            main.wait_stream(self.comm)
+            _lib.call("dg_laplace_vmult_split_dots", h, P(p), P(Lp), float(tau_scale), 2,
                       P(out3), ms)
         else:
             self.vmult(p, Lp, tau_scale)
-            _lib.call("dg_cg_dots", self.ctx.handle, P(p), P(Lp), P(out3), ms)
+            _lib.call("dg_cg_dots", h, P(p), P(Lp), P(out3), ms)
         return Lp
 
     def diagonal(self, tau_scale=1.0):

@@ -105,6 +105,76 @@ def test_sharded_pcg_matches_single_context(world, k, prec, neumann):
     assert np.linalg.norm(x2 - ref) <= (1e-10 if prec == "cheb" else 1e-8) * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("prec", ["jacobi", "cheb"])
+def test_sharded_pcg_fused_dots_on_slabs(world, prec, monkeypatch):
+    """The sharded solve with the fused vmult + dots launches forced on the
+    small slabs (DG_DOTS_MIN_CELLS: column kernel with the kEpiDotS sums on
+    zero traces, ghost lifts adding their share of p.Lp and sum(Lp)):
+    dg_laplace_vmult_split_dots must reproduce the single-context solve like
+    the unfused path above."""
+    monkeypatch.setenv("DG_DOTS_MIN_CELLS", "1")
+    test_sharded_pcg_matches_single_context(world, 4, prec, True)
+
+
+def test_split_dots_sums_add_up(monkeypatch):
+    """Rank-local [p.Lp, sum(Lp), p.w] of dg_laplace_vmult_split_dots (fused and
+    fallback) summed over the slabs equal the single-context dg_cg_dots."""
+    import ctypes
+    from paper_1607_01323_b200 import _lib
+    mesh, space, bcs, _ = setup((12, 8, 6), 4, True)
+    p = np.random.default_rng(3).uniform(-1, 1, space.n_dofs)
+    pd = torch.as_tensor(p, device="cuda")
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    one = SlabLaplace(mesh, 4, bcs.kinds, 0, 1)
+    ref = torch.empty_like(pd)
+    one.vmult(pd, ref)
+    s_ref = torch.zeros(3, dtype=torch.float64, device="cuda")
+    _lib.call("dg_cg_dots", one.ctx.handle, P(pd), P(ref), P(s_ref), st)
+    s_ref = s_ref.cpu().numpy()
+    scale = np.array([float(pd.abs().dot(ref.abs())), float(ref.abs().sum()), float(pd.abs().sum())])
+    for min_cells in ("1", None):
+        if min_cells:
+            monkeypatch.setenv("DG_DOTS_MIN_CELLS", min_cells)
+        else:
+            monkeypatch.delenv("DG_DOTS_MIN_CELLS")
+        world = 3
+        comm = ThreadComm(world)
+        part = SlabPartition(mesh.counts[0], world, bool(mesh.periodic[0]))
+        sums, outs, err = [None] * world, [None] * world, []
+
+        def run(rank):
+            try:
+                torch.cuda.set_device(0)
+                with torch.cuda.stream(torch.cuda.Stream()):
+                    lap = SlabLaplace(mesh, 4, bcs.kinds, rank, world, comm=comm.view(rank))
+                    pl = torch.as_tensor(slab_of(p, part, rank, mesh.counts, space.n_local),
+                                         device="cuda")
+                    Lp = torch.full_like(pl, float("nan"))
+                    s = torch.zeros(3, dtype=torch.float64, device="cuda")
+                    lap.vmult_dots(pl, Lp, 1.0, s)
+                    torch.cuda.current_stream().synchronize()
+                    sums[rank], outs[rank] = s.cpu().numpy(), Lp.cpu().numpy()
+            except Exception as e:  # noqa: BLE001
+                err.append(e)
+                comm.bar.abort()
+
+        ths = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        if err:
+            raise err[0]
+        n, (nx, ny, nz) = space.n_local, mesh.counts
+        got = np.concatenate([o.reshape(nz, ny, -1, n) for o in outs], axis=2).ravel()
+        refh = ref.cpu().numpy()
+        assert np.linalg.norm(got - refh) <= 1e-14 * np.linalg.norm(refh)
+        tot = np.sum(sums, axis=0)
+        assert np.all(np.abs(tot - s_ref) <= 1e-13 * scale), (min_cells, tot, s_ref)
+
+
 @pytest.mark.parametrize("counts,k,neumann", [
     ((32, 32, 16), 4, True),    # fused column epilogue, TMA rows, periodic x / z
     ((30, 33, 17), 4, False),   # fused, ragged tiles, odd nx (no TMA)
