@@ -600,8 +600,10 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             cms = t.item()
         cgi = {"config": f"C5: {n}^3 Q{k} walls, Jacobi-PCG iteration (parallel.SlabPCG): x-slab "
-                         f"vmult with overlapped face-trace halo exchange + 2 NCCL all-reduces + "
-                         f"fused vector kernels + host stop test, {world} GPU(s)",
+                         f"vmult with p.Lp / sum(Lp) / p.w formed in its epilogue "
+                         f"(dg_laplace_vmult_dots / _split_dots), overlapped face-trace halo "
+                         f"exchange + 2 NCCL all-reduces + fused vector kernels + host stop "
+                         f"test, {world} GPU(s)",
                "iterations": KC, "ms_per_iteration": cms / KC,
                "dof_per_s_per_iteration": total / (cms / KC * 1e-3),
                "bytes_per_dof_algorithmic": 96,

@@ -492,7 +492,7 @@ static int launch_laplace6(dg_ctx *c, const double *src, double *dst, double tau
                            cudaStream_t st, const EpiArgs &ea = EpiArgs{});
 
 // fused-epilogue vmults for the CG / Chebyshev loop (default bricks, k = 2..5)
-template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore, int HSM = 0, int HMAP = 0, int FSD = 0>
+template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore, int HSM = 0, int HMAP = 0, int FSD = 0, int UBC = 0>
 static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea = EpiArgs{});
 
@@ -521,6 +521,15 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
       if (epi == kEpiCheb) return launch_laplace8<5, 4, 8, 3, 1, kEpiCheb, 2, 1>(c, src, dst, tau_scale, 0, st, ea);
       if (epi == kEpiDot) return launch_laplace8<5, 4, 8, 3, 1, kEpiDot, 2, 1>(c, src, dst, tau_scale, 0, st, ea);
     }
+    // Chebyshev epilogue with d from the shared-memory copy (UBC); DG_EPI_CFG=4: re-read
+    if (epi == kEpiCheb && ecfg == 5)
+      return launch_laplace8<5, 4, 8, 3, 1, kEpiCheb, 2, 1, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
+    // (C2 PCG, ms per iteration: 8x4 ring 3 + UBC 0.479, ring 3 0.494, ring 4 0.501,
+    // 4x8 ring 3 HSM 2 + UBC 0.540; profiles/r02/cmd_s6e.sh)
+    if (epi == kEpiCheb && ecfg == 7)
+      return launch_laplace8<5, 8, 4, 3, 1, kEpiCheb, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
+    if (epi == kEpiCheb && ecfg != 4)
+      return launch_laplace8<5, 8, 4, 3, 1, kEpiCheb, 1, 1, 0, 1>(c, src, dst, tau_scale, 0, st, ea);
     if (epi == kEpiCheb) return launch_laplace8<5, 8, 4, 4, 1, kEpiCheb, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
     // the dot epilogue from the shared-memory copy of u (kEpiDotS: out by TMA
     // stores, no global re-read of u); DG_EPI_CFG=3: the cooperative one
@@ -652,18 +661,19 @@ static int launch_laplace7(dg_ctx *c, const double *src, double *dst, double tau
 }
 
 // half-plane column kernel (laplace8.cuh)
-template <int N, int TX, int TY, int NRING, int MINB, int EPI, int HSM, int HMAP, int FSD>
+template <int N, int TX, int TY, int NRING, int MINB, int EPI, int HSM, int HMAP, int FSD, int UBC>
 static int launch_laplace8(dg_ctx *c, const double *src, double *dst, double tau_scale, int part,
                            cudaStream_t st, const EpiArgs &ea) {
   if (t_kname) {
-    *t_kname = FSD ? kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI, HSM, HMAP, FSD})
+    *t_kname = UBC ? kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI, HSM, HMAP, FSD, UBC})
+               : FSD ? kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI, HSM, HMAP, FSD})
                : (HSM || HMAP) ? kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI, HSM, HMAP})
                              : kname("laplace8_kernel", {N, TX, TY, NRING, MINB, EPI});
     return DG_OK;
   }
   using C = Lap8Cfg<N, TX, TY, NRING, HSM>;
-  auto kern = laplace8_kernel<N, TX, TY, NRING, MINB, EPI, HSM, HMAP, FSD>;
-  constexpr size_t kSmem = EPI == kEpiDotS ? C::SMEM_DOTS : C::SMEM;
+  auto kern = laplace8_kernel<N, TX, TY, NRING, MINB, EPI, HSM, HMAP, FSD, UBC>;
+  constexpr size_t kSmem = (EPI == kEpiDotS || UBC) ? C::SMEM_DOTS : C::SMEM;
   static_assert(kSmem <= 232448, "laplace8: more than 227 KB of shared memory");
   static int nsm = 0, occ = 1;
   if (!nsm) {

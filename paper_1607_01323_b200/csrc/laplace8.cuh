@@ -86,7 +86,7 @@ __device__ __forceinline__ int l8_role(int w) {
 // (laplace.cuh epi_store) applied cooperatively to each finished layer of
 // the tile; kEpiDot leaves one partial-sum triple per CTA in ea.partials.
 template <int N, int TX, int TY, int NRING, int MINB, int EPI = kEpiStore, int HSM = 0, int HMAP = 0,
-          int FSD = 0>
+          int FSD = 0, int UBC = 0>
 __global__ void __launch_bounds__(Lap8Cfg<N, TX, TY, NRING>::THREADS, MINB)
 laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Geo g,
                 const __grid_constant__ LapTab<N> T, const double ts, const int part,
@@ -580,7 +580,7 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
     halo_stage2(par);
     if (EPI == kEpiCheb && (N & 1)) {  // this layer's epilogue operands -> L2
       const int R = ex * NP;
-      for (int i = tid * 16; i < 4 * ey * R; i += 16 * C::THREADS) {  // 128 B lines
+      for (int i = tid * 16; i < (UBC ? 3 : 4) * ey * R; i += 16 * C::THREADS) {  // 128 B lines
         const int v = i / (ey * R), rem = i - v * (ey * R), yy = rem / R, j = rem - yy * R;
         const size_t gi = ((size_t)x0 + (size_t)g.nx * (y0 + yy) + nxy * iz) * NP + j;
         const double *p = v == 0 ? ea.rc : (v == 1 ? ea.diag : (v == 2 ? ea.x : u));
@@ -613,7 +613,7 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
           double w[N], e[NE], o[HO], E[NE], O[HO], g0, g1;
 #pragma unroll
           for (int z = 0; z < N; ++z) w[z] = up[z * N2 + k];
-          if (EPI == kEpiDotS) {  // u of this layer stays readable for the y phase
+          if (EPI == kEpiDotS || (EPI == kEpiCheb && UBC)) {  // u of this layer stays readable
             double *ub = ubuf + c * CSTR + s * N + l0;
 #pragma unroll
             for (int z = 0; z < N; ++z) ub[z * N2 + k] = w[z];
@@ -762,6 +762,7 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
       for (int yy = 0; yy < ey; ++yy) {
         const size_t rb = ((size_t)x0 + (size_t)g.nx * (y0 + yy) + nxy * iz) * NP;
         const double *sl = slot + TX * yy * CSTR;
+        const double *ul = ubuf + TX * yy * CSTR;  // UBC: d of this layer from shared memory
         for (int j0 = tid; j0 < R; j0 += U * C::THREADS) {
           double yv[U], rc[U], dg[U], xv[U], uv[U];
 #pragma unroll
@@ -772,7 +773,7 @@ laplace8_kernel(const double *__restrict__ u, double *__restrict__ out, const Ge
               rc[q] = ea.rc[rb + j];
               dg[q] = ea.diag[rb + j];
               xv[q] = ea.x[rb + j];
-              uv[q] = u[rb + j];
+              uv[q] = UBC ? ul[j] : u[rb + j];
             }
           }
 #pragma unroll
