@@ -5,6 +5,9 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <algorithm>
+#include <map>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -607,17 +610,72 @@ static int chunk_len(int nz, int cols, int slots, int occ, int lcmin, int lcmax)
     const int want = (4 * slots + cols - 1) / cols;
     return std::min(std::max(lcmin, (nz + want - 1) / want), lcmax);
   }
+  const char *cm = getenv("DG_CHUNK_MODEL");  // 0: the wave model (A/B, read per call)
+  if (cm && atoi(cm) == 0) {
+    int best = lcmax;
+    double best_t = 1e300;
+    for (int lc = lcmax; lc >= lcmin; --lc) {
+      const int64_t nch = (nz + lc - 1) / lc;
+      const int64_t waves = ((int64_t)cols * nch + slots - 1) / slots;
+      const double t = (double)waves * (lc + 2.0);
+      if (t < best_t - 1e-9) {
+        best_t = t;
+        best = lc;
+      }
+    }
+    return best;
+  }
+  // List-scheduling model: the CTAs start in blockIdx order (chunk-major: all
+  // columns of chunk 0, of chunk 1, ...; the LAST chunk of a column is the
+  // short one, nz - (nch - 1) lc layers), each on the slot that frees first,
+  // and take their layer count + 2.  The makespan of that schedule, not the
+  // wave count, is what the launch costs: a short last chunk fills the slots
+  // the long chunks leave idle (x-slab of P = 8, 64 columns x 128 layers on
+  // 148 SMs: lc = 58 -> 128 CTAs of 58 layers + 64 of 12 layers, makespan 60
+  // instead of 66 for 2 x 64).  Cached per argument tuple.
+  struct Key {
+    int nz, cols, slots, lcmin, lcmax;
+    bool operator<(const Key &o) const {
+      return std::tie(nz, cols, slots, lcmin, lcmax) < std::tie(o.nz, o.cols, o.slots, o.lcmin, o.lcmax);
+    }
+  };
+  static std::map<Key, int> cache;
+  static std::mutex mu;
+  const Key key{nz, cols, slots, lcmin, lcmax};
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
   int best = lcmax;
   double best_t = 1e300;
+  std::vector<double> heap;
   for (int lc = lcmax; lc >= lcmin; --lc) {
-    const int64_t nch = (nz + lc - 1) / lc;
-    const int64_t waves = ((int64_t)cols * nch + slots - 1) / slots;
-    const double t = (double)waves * (lc + 2.0);
+    const int nch = (nz + lc - 1) / lc;
+    const int last = nz - (nch - 1) * lc;
+    double t;
+    if ((int64_t)cols * nch <= slots) {
+      t = lc + 2.0;
+    } else {
+      heap.assign((size_t)slots, 0.0);  // min-heap of slot free times
+      auto cmp = [](double a, double b) { return a > b; };
+      double end = 0.0;
+      for (int ch = 0; ch < nch; ++ch) {
+        const double d = (ch == nch - 1 ? last : lc) + 2.0;
+        for (int j = 0; j < cols; ++j) {
+          std::pop_heap(heap.begin(), heap.end(), cmp);
+          const double f = heap.back() + d;
+          heap.back() = f;
+          std::push_heap(heap.begin(), heap.end(), cmp);
+          if (f > end) end = f;
+        }
+      }
+      t = end;
+    }
     if (t < best_t - 1e-9) {
       best_t = t;
       best = lc;
     }
   }
+  cache[key] = best;
   return best;
 }
 
