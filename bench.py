@@ -416,12 +416,14 @@ def run_cg(dist_on):
     cfg = sol.ChebyshevConfig(5, 20.0, lmax)
     sol.laplace_pcg(space, bcs, b, project_dual=True, cheb=cfg, diag=diag, rel_tol=1e-10,
                     max_iter=5)  # warm-up
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    x, st = sol.laplace_pcg(space, bcs, b, project_dual=True, cheb=cfg, diag=diag,
-                            rel_tol=1e-10, max_iter=5000)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    dt = 1e30
+    for _ in range(2):  # whole solves, wall clock; the faster of two (one-time set-up in the first)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x, st = sol.laplace_pcg(space, bcs, b, project_dual=True, cheb=cfg, diag=diag,
+                                rel_tol=1e-10, max_iter=5000)
+        torch.cuda.synchronize()
+        dt = min(dt, time.perf_counter() - t0)
     out = {"config": "C2: 32^3 Q4 periodic x,z / walls y, Chebyshev(5,20)-Jacobi PCG, rel_tol 1e-10",
            "dofs": space.n_dofs, "iterations": st.iterations, "converged": st.converged,
            "solve_ms": 1e3 * dt, "ms_per_iteration": 1e3 * dt / max(st.iterations, 1),
