@@ -594,23 +594,29 @@ static int l7_lcmin(int dflt) {
   return e ? std::max(1, atoi(e)) : dflt;
 }
 
-// z-chunk length of the column kernels.  One CTA per SM (occ 1): CTAs =
-// cols x ceil(nz / lc) run in waves of the SM count, each wave as long as its
-// longest chunk plus ~2 layers of ring fill / z halo; the lc in [lcmin,
-// lcmax] with the smallest predicted time waves x (lc + 2) (ties: longer
-// chunks).  The rule for several CTAs per SM (and DG_CHUNK_OLD=1, per call,
-// for A/B) is about 4 waves: lc = nz / ceil(4 slots / cols) -- at occ 1 it
-// left a part-filled last wave on the x-slab sizes (64x128x128 Q4: 768 CTAs
-// = 5.2 waves; 1.24 -> 1.10 ms with the model, profiles/r02/chunk_ab.py),
-// at occ > 1 the model measured worse (64^3 Q3 0.163 -> 0.180 ms).
+// z-chunk length of the column kernels: the lc in [lcmin, lcmax] with the
+// smallest makespan of a list-scheduling model of the launch (below; ties:
+// longer chunks).  History: the first rule was about 4 waves, lc = nz /
+// ceil(4 slots / cols) (DG_CHUNK_OLD=1, per call, for A/B) -- at one CTA per
+// SM it left a part-filled last wave on the x-slab sizes (64x128x128 Q4: 768
+// CTAs = 5.2 waves); then a wave model, waves x (lc + 2) (DG_CHUNK_MODEL=0;
+// 1.24 -> 1.10 ms there, profiles/r02/chunk_ab.py), which at several CTAs
+// per SM measured worse than the rule (64^3 Q3 0.163 -> 0.180 ms: few long
+// chunks); with several CTAs per SM the 4-wave length is therefore the upper
+// bound of the search.
 static int chunk_len(int nz, int cols, int slots, int occ, int lcmin, int lcmax) {
   lcmax = std::max(1, std::min(nz, lcmax));
   lcmin = std::max(1, std::min(lcmin, lcmax));
+  const char *cm = getenv("DG_CHUNK_MODEL");  // 0: the wave model (A/B, read per call)
   if (occ > 1 || getenv("DG_CHUNK_OLD")) {
     const int want = (4 * slots + cols - 1) / cols;
-    return std::min(std::max(lcmin, (nz + want - 1) / want), lcmax);
+    const int lc4 = std::min(std::max(lcmin, (nz + want - 1) / want), lcmax);
+    // several CTAs per SM: the list model below with chunks no longer than
+    // the 4-wave rule's (never slower; 128^3 Q3 +7.1 %, 64^3 Q5 +6.0 %, 96^3
+    // Q5 +2.0 %, profiles/r02/chunk_occ_ab.py); DG_CHUNK_MODEL=0: the rule
+    if ((cm && atoi(cm) == 0) || getenv("DG_CHUNK_OLD")) return lc4;
+    lcmax = lc4;
   }
-  const char *cm = getenv("DG_CHUNK_MODEL");  // 0: the wave model (A/B, read per call)
   if (cm && atoi(cm) == 0) {
     int best = lcmax;
     double best_t = 1e300;

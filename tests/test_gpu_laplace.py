@@ -310,6 +310,26 @@ def test_slab_split_equals_full_on_one_gpu(k):
                 assert relerr(got2, full) < 1e-14, ("split", nranks, per, relerr(got2, full))
 
 
+@pytest.mark.parametrize("cells,k", [(64, 4), (40, 3), (40, 5)])
+def test_chunk_models_bitwise_equal(cells, k, monkeypatch):
+    """The z-chunk length of the column kernels (list-scheduling model: a short
+    last chunk per column) only cuts the march differently: the vmult is
+    bitwise identical to the one chunked by the older rule (DG_CHUNK_MODEL=0)
+    and to one long chunk per column is not required -- chunks re-derive the
+    z-neighbour functionals from the same data."""
+    mesh = M.build_box_mesh(((0, 1),) * 3, (cells,) * 3, periodic=(False, True, False))
+    space = DgSpace(mesh, k)
+    bcs = ops.BoundarySpec({t: ops.DirichletBC(None) for t in mesh.boundary_tags()}).resolve(space)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    p = torch.rand(space.n_dofs, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    a = ops.apply_pressure_laplace(space, p, bcs).clone()
+    monkeypatch.setenv("DG_CHUNK_MODEL", "0")
+    b = ops.apply_pressure_laplace(space, p, bcs).clone()
+    monkeypatch.setenv("DG_CHUNK_OLD", "1")
+    c = ops.apply_pressure_laplace(space, p, bcs).clone()
+    assert torch.equal(a, b) and torch.equal(a, c)
+
+
 def test_large_periodic_properties():
     """Size-independent properties at 64^3 Q4 (33.5M DoFs): L 1 = 0 on the
     fully periodic box, symmetry <Lp, q> = <p, Lq>, linearity."""
