@@ -336,7 +336,7 @@ def run_small_configs():
     return out
 
 
-def run_slab_emulation(n, k, t1_ms):
+def run_slab_emulation(n, k, t1_ms, cg1_ms=None):
     """Per-rank compute of the C5 x-slab vmult at P = 2, 4, 8 on ONE GPU: an
     interior slab of the 128^3 mesh with its ghost face traces in device
     buffers (what the NCCL exchange delivers), timed as the production
@@ -388,6 +388,39 @@ def run_slab_emulation(n, k, t1_ms):
                              "compute_efficiency": t1_ms / (nranks * tp),
                              "halo_bytes_per_rank": halo_bytes,
                              "nvlink_ms_at_900GBs": halo_bytes / 2 / 900e9 * 1e3}
+        if cg1_ms is not None:
+            # the rank's kernels of one SlabPCG Jacobi iteration (projected
+            # operator as in cg_iteration_c5): split vmult with its dot shares,
+            # x / r / z update with r.z, p update; all-reduces (two of <= 3
+            # doubles) and the exchange excluded
+            x, r, z, dg = (torch.rand(nloc, dtype=torch.float64, device="cuda") + 0.5
+                           for _ in range(4))
+            scal = torch.tensor([1.0, 2.0, 0.0, 0.0, 1.0, 0, 0, 0], dtype=torch.float64,
+                                device="cuda")
+            s3 = torch.zeros(3, dtype=torch.float64, device="cuda")
+
+            def it():
+                for ph in (1, 2):
+                    _lib.call("dg_laplace_vmult_split_dots", c.handle, P(src), P(dst), 1.0, ph,
+                              P(s3), st)
+                _lib.call("dg_cg_update", c.handle, P(x), P(r), P(src), P(dst), P(scal), 1, P(dg),
+                          P(z), P(s3), st)
+                _lib.call("dg_cg_pupdate", c.handle, P(src), P(z), P(scal), st)
+                scal[0] = 1.0  # keep beta bounded over the repetitions
+            it()
+            torch.cuda.synchronize()
+            best = 1e9
+            for _ in range(3):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(10):
+                    it()
+                b.record()
+                torch.cuda.synchronize()
+                best = min(best, a.elapsed_time(b) / 10)
+            out[f"P{nranks}"]["rank_cg_iteration_ms"] = best
+            out[f"P{nranks}"]["cg_compute_efficiency"] = cg1_ms / (nranks * best)
+            del x, r, z, dg
         del c, src, dst, rcv
     out["note"] = ("one GPU, interior slab, ghost traces from device buffers; communication "
                    "excluded (overlapped with the whole-slab phase in the product)")
@@ -630,7 +663,7 @@ def main():
     slab_emu = None
     if rank == 0 and world == 1 and not args.no_step:
         try:
-            slab_emu = run_slab_emulation(n, k, ms_step)
+            slab_emu = run_slab_emulation(n, k, ms_step, cgi["ms_per_iteration"] if cgi else None)
         except Exception as exc:  # reported, never fatal for the headline line
             slab_emu = {"error": repr(exc)[:200]}
     sweep = []
