@@ -531,8 +531,11 @@ static int laplace_dispatch_epi(dg_ctx *c, const double *src, double *dst, doubl
     // 4x8 ring 3 HSM 2 + UBC 0.540; profiles/r02/cmd_s6e.sh)
     if (epi == kEpiCheb && ecfg == 7)
       return launch_laplace8<5, 8, 4, 3, 1, kEpiCheb, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
-    if (epi == kEpiCheb && ecfg != 4)
+    if (epi == kEpiCheb && ecfg == 6)
       return launch_laplace8<5, 8, 4, 3, 1, kEpiCheb, 1, 1, 0, 1>(c, src, dst, tau_scale, 0, st, ea);
+    // default: + per-cell / per-layer side coefficients (FSD): 0.479 -> 0.475 (cmd_s6p.sh)
+    if (epi == kEpiCheb && ecfg != 4)
+      return launch_laplace8<5, 8, 4, 3, 1, kEpiCheb, 1, 1, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
     if (epi == kEpiCheb) return launch_laplace8<5, 8, 4, 4, 1, kEpiCheb, 1, 1>(c, src, dst, tau_scale, 0, st, ea);
     // the dot epilogue from the shared-memory copy of u (kEpiDotS: out by TMA
     // stores, no global re-read of u); DG_EPI_CFG=3: the cooperative one
